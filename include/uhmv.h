@@ -1,0 +1,113 @@
+/*
+ * uhmv.h -- C ABI of the B200-native uniform-H matrix-vector product (sm_100a).
+ *
+ * The reference (uhm-kit, pure Python) has no FFI: its boundary is the Python callable
+ *   matvec_uh(u, v, workers=1, adjoint=False, stats=None)
+ *     /root/reference/pkg/src/uhm_kit/uniform.py:476-556
+ * plus UniformHMatrix.matvec (uniform.py:116-117).  This library replaces the body of that
+ * callable; the Python layer (paper_2405_15573_b200/matvec.py) keeps its signature, argument
+ * meaning and error behaviour and binds these entry points with ctypes.
+ *
+ * Ownership: every device buffer named in uhmv_desc is allocated and kept alive by the caller
+ * (PyTorch tensors in the Python layer).  The plan never frees them; it only owns launch
+ * configuration.  All entry points return 0 on success and a negative code on failure; the text
+ * of the last failure of the calling thread is available from uhmv_last_error().
+ */
+#ifndef UHMV_H
+#define UHMV_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UHMV_ABI_VERSION 1
+#define UHMV_MAX_PHASES 8
+
+/* Execution modes of uhmv_execute. */
+#define UHMV_MODE_PHASED 0 /* one launch per phase (P1+NEAR, RED, U, Z, FAR)          */
+#define UHMV_MODE_FUSED 1  /* one persistent launch, dependency counters between ops     */
+
+/* Error codes. */
+#define UHMV_OK 0
+#define UHMV_EINVAL (-1)
+#define UHMV_ECUDA (-2)
+#define UHMV_ENOMEM (-3)
+
+/* One op program (forward or adjoint) -- device pointers to the tables built by the packer
+ * (paper_2405_15573_b200/packer.py).  ops: n_ops x 16 int32; segs: n_segs x 8 int64;
+ * runs: n_runs x 5 int64; waits: n_waits x 2 int32; sigs: int32; fused_order: n_ops int32. */
+typedef struct uhmv_program {
+    int32_t n_ops;
+    const int32_t* ops;
+    const int64_t* segs;
+    const int64_t* runs;
+    const int32_t* waits;
+    const int32_t* sigs;
+    const int32_t* fused_order;
+    int32_t n_phases;
+    int32_t phase_lo[UHMV_MAX_PHASES];
+    int32_t phase_hi[UHMV_MAX_PHASES];
+    int32_t in_max;     /* largest gathered input vector of any op (complex elements)  */
+    int32_t out_max;    /* largest output vector of any op (complex elements)          */
+    int32_t n_counters; /* dependency counters used by the fused mode                  */
+} uhmv_program;
+
+/* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */
+typedef struct uhmv_desc {
+    int32_t abi_version;      /* = UHMV_ABI_VERSION */
+    int32_t device;           /* CUDA device ordinal */
+    int64_t n_rows, n_cols;   /* operator shape (bct.shape, clustering.py:196-198) */
+    const void* arena;        /* complex128 bases, coupling and dense slabs (read-only) */
+    void* work;               /* complex128 scratch: partials, y, staging u, z */
+    int64_t work_len;
+    uint32_t* counters;       /* >= max(n_counters) zero-initialised uint32 */
+    unsigned long long* ticket; /* one zero-initialised uint64 (fused dispatch) */
+    uint32_t* exit_count;     /* one zero-initialised uint32 (fused self-reset) */
+    void* x_scratch;          /* complex128 device buffers used by uhmv_matvec_host, */
+    void* w_scratch;          /* each >= max(n_rows, n_cols) elements (may be NULL)  */
+    uhmv_program fwd;
+    uhmv_program adj;
+} uhmv_desc;
+
+typedef struct uhmv_plan uhmv_plan;
+
+/* ABI version compiled into the library. */
+int uhmv_abi_version(void);
+
+/* Validate a descriptor and prepare launch configuration (occupancy, shared memory).
+ * Replaces: nothing in the reference -- the reference walks dicts on every call
+ * (uniform.py:505-548); packing happens once per operator. */
+int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out);
+
+/* w = A x (adjoint=0) or w = A^H x (adjoint=1); x, w device complex128 in tree order.
+ * Replaces: matvec_uh body, uniform.py:496-556 (phase 1 :509-520, phase 2 :524-556).
+ * stream: a cudaStream_t (NULL = legacy default stream).  Asynchronous. */
+int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode, void* stream);
+
+/* Phased execution of phases [phase_lo, phase_hi) only (multi-GPU: the Python layer
+ * inserts the NCCL all-gather of y/u between the halves).  Asynchronous. */
+int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, int phase_lo,
+                        int phase_hi, void* stream);
+
+/* End-to-end call with HOST buffers: H2D copy of x, execute, D2H copy of w, stream sync.
+ * x_host / w_host: complex128 (interleaved re,im doubles), length n_in / n_out.
+ * Replaces: the whole matvec_uh call as a caller sees it (uniform.py:476-556). */
+int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
+                     void* stream);
+
+/* Launch geometry chosen for the fused mode (grid CTAs, dynamic shared memory bytes). */
+int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int* fused_grid, int* smem_bytes,
+                   int* threads_per_cta);
+
+int uhmv_plan_destroy(uhmv_plan* plan);
+
+/* Thread-local text of the last failure ("" if none). */
+const char* uhmv_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* UHMV_H */

@@ -1,0 +1,78 @@
+"""NumPy interpreter of a packed op program.
+
+TEST INFRASTRUCTURE ONLY (see oracle/matvec_oracle.py header): it walks the packed
+arena and op tables exactly as the CUDA kernel does, so the packer's layout can be
+pinned against ``oracle_matvec_uh`` on the CPU (and the multi-rank exchange logic
+exercised under gloo) without a GPU.  It is never a fallback for the product path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from paper_2405_15573_b200.packer import (
+    BUF_ARENA,
+    BUF_W,
+    BUF_WORK,
+    BUF_X,
+    MODE_H,
+    MODE_N,
+    MODE_S,
+    RUN_ADD,
+)
+
+__all__ = ["run_program", "vm_matvec"]
+
+
+def run_op(prog, i, bufs):
+    n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e = (int(v) for v in prog.ops[i, :8])
+    xin = np.zeros(n_in, dtype=np.complex128)
+    for buf, off, ln, dst, _ in prog.runs[in_b:in_e]:
+        xin[dst : dst + ln] = bufs[buf][off : off + ln]
+    out = np.zeros(n_out, dtype=np.complex128)
+    for m_off, buf, rows, cols, ld, mode, in_off, out_off in prog.segs[seg_b:seg_e]:
+        src = bufs[buf]
+        idx = m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]
+        m = src[idx] if rows and cols else np.zeros((rows, cols), dtype=np.complex128)
+        if mode == MODE_N:
+            out[out_off : out_off + rows] += m @ xin[in_off : in_off + cols]
+        elif mode == MODE_H:
+            out[out_off : out_off + cols] += np.conj(m).T @ xin[in_off : in_off + rows]
+        elif mode == MODE_S:
+            out[out_off : out_off + cols] += m.sum(axis=0)
+        else:
+            raise ValueError(mode)
+    for buf, off, ln, dst, flags in prog.runs[out_b:out_e]:
+        if flags & RUN_ADD:
+            bufs[buf][off : off + ln] += out[dst : dst + ln]
+        else:
+            bufs[buf][off : off + ln] = out[dst : dst + ln]
+
+
+def run_program(prog, arena, work, x, w, order="phased", op_range=None):
+    bufs = {BUF_ARENA: arena, BUF_WORK: work, BUF_X: x, BUF_W: w}
+    if order == "fused":
+        seq = prog.fused_order.tolist()
+        done = np.zeros(prog.n_counters, dtype=np.int64)
+        for i in seq:
+            wb, we, sb, se = (int(v) for v in prog.ops[i, 8:12])
+            for c, cnt in prog.waits[wb:we]:
+                assert done[c] >= cnt, f"op {i} waits on counter {c} ({done[c]}<{cnt}): order not topological"
+            run_op(prog, i, bufs)
+            for c in prog.sigs[sb:se]:
+                done[c] += 1
+    else:
+        lo, hi = (0, prog.n_ops) if op_range is None else op_range
+        for i in range(lo, hi):
+            run_op(prog, i, bufs)
+
+
+def vm_matvec(packed, v, adjoint=False, order="phased"):
+    prog = packed.adj if adjoint else packed.fwd
+    n_in, n_out = (packed.n_rows, packed.n_cols) if adjoint else (packed.n_cols, packed.n_rows)
+    x = np.asarray(v, dtype=np.complex128)
+    assert x.shape == (n_in,)
+    w = np.full(n_out, np.nan + 1j * np.nan)  # every entry must be written
+    work = np.zeros(packed.work_len, dtype=np.complex128)
+    run_program(prog, packed.arena, work, x, w, order=order)
+    return w

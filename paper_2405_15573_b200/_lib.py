@@ -1,0 +1,107 @@
+"""ctypes binding of the C ABI declared in include/uhmv.h (libuhmv.so, sm_100a).
+
+The product path has no CPU fallback: if the shared library is missing or cannot be
+loaded, every entry point raises.  Build it with ``python -c "import __graft_entry__ as g;
+g.build()"`` (nvcc -gencode arch=compute_100a,code=sm_100a).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+__all__ = ["lib", "UhmvProgram", "UhmvDesc", "check", "LIB_PATH", "MAX_PHASES"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
+MAX_PHASES = 8
+ABI_VERSION = 1
+MODE_PHASED, MODE_FUSED = 0, 1
+
+
+class UhmvProgram(ctypes.Structure):
+    _fields_ = [
+        ("n_ops", ctypes.c_int32),
+        ("ops", ctypes.c_void_p),
+        ("segs", ctypes.c_void_p),
+        ("runs", ctypes.c_void_p),
+        ("waits", ctypes.c_void_p),
+        ("sigs", ctypes.c_void_p),
+        ("fused_order", ctypes.c_void_p),
+        ("n_phases", ctypes.c_int32),
+        ("phase_lo", ctypes.c_int32 * MAX_PHASES),
+        ("phase_hi", ctypes.c_int32 * MAX_PHASES),
+        ("in_max", ctypes.c_int32),
+        ("out_max", ctypes.c_int32),
+        ("n_counters", ctypes.c_int32),
+    ]
+
+
+class UhmvDesc(ctypes.Structure):
+    _fields_ = [
+        ("abi_version", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("n_rows", ctypes.c_int64),
+        ("n_cols", ctypes.c_int64),
+        ("arena", ctypes.c_void_p),
+        ("work", ctypes.c_void_p),
+        ("work_len", ctypes.c_int64),
+        ("counters", ctypes.c_void_p),
+        ("ticket", ctypes.c_void_p),
+        ("exit_count", ctypes.c_void_p),
+        ("x_scratch", ctypes.c_void_p),
+        ("w_scratch", ctypes.c_void_p),
+        ("fwd", UhmvProgram),
+        ("adj", UhmvProgram),
+    ]
+
+
+_lib = None
+
+EXPORTS = (
+    "uhmv_abi_version",
+    "uhmv_plan_create",
+    "uhmv_execute",
+    "uhmv_execute_phases",
+    "uhmv_matvec_host",
+    "uhmv_plan_info",
+    "uhmv_plan_destroy",
+    "uhmv_last_error",
+)
+
+
+def lib():
+    """Load libuhmv.so once; raise (never fall back) when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"uniform-H CUDA library not built: {LIB_PATH} is missing "
+            "(run __graft_entry__.build()); there is no CPU fallback"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32 = ctypes.c_void_p, ctypes.c_int
+    L.uhmv_abi_version.restype = i32
+    L.uhmv_plan_create.argtypes = [ctypes.POINTER(UhmvDesc), ctypes.POINTER(vp)]
+    L.uhmv_plan_create.restype = i32
+    L.uhmv_execute.argtypes = [vp, vp, vp, i32, i32, vp]
+    L.uhmv_execute.restype = i32
+    L.uhmv_execute_phases.argtypes = [vp, vp, vp, i32, i32, i32, vp]
+    L.uhmv_execute_phases.restype = i32
+    L.uhmv_matvec_host.argtypes = [vp, vp, vp, i32, i32, vp]
+    L.uhmv_matvec_host.restype = i32
+    L.uhmv_plan_info.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    L.uhmv_plan_info.restype = i32
+    L.uhmv_plan_destroy.argtypes = [vp]
+    L.uhmv_plan_destroy.restype = i32
+    L.uhmv_last_error.restype = ctypes.c_char_p
+    if L.uhmv_abi_version() != ABI_VERSION:
+        raise RuntimeError("libuhmv.so ABI version mismatch; rebuild")
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = lib().uhmv_last_error().decode(errors="replace")
+        raise RuntimeError(f"{what} failed ({rc}): {msg}")

@@ -1,0 +1,593 @@
+// uhmv.cu -- sm_100a kernels + C ABI for the uniform-H matrix-vector product.
+//
+// One kernel body executes "ops" of a packed program (paper_2405_15573_b200/packer.py):
+//   gather input runs -> shared-memory vector xin
+//   sum of GEMV segments streamed from HBM (complex128, 16 B per lane per load)
+//   scatter the shared-memory output vector (store or add)
+// This replaces the dict walk and NumPy GEMVs of matvec_uh
+// (/root/reference/pkg/src/uhm_kit/uniform.py:509-556):
+//   phase 1 V_t^H x|_t  ........ P1 ops (H segments) + RED ops (S segments)
+//   stage_b = s_y^H pre ........ U ops (H segments over the concatenated s_y of a cluster)
+//   acc_s = sum s_x stage ...... Z ops (one N segment over the concatenated coupling row X_s)
+//   w|_s += U_s acc ............ FAR ops (N segments, owned output rows, no atomics)
+//   dense w|_r += D v|_c ....... NEAR ops (N segments; adjoint: H segments)
+//
+// Thread mapping (128 threads = 4 warps = 16 row-groups of 8 lanes): a row-group streams one
+// matrix row at a time, its 8 lanes covering 8 consecutive complex128 (128 B, one L2 line) per
+// load, so every warp-wide load instruction moves 4 fully used 128-B lines.
+//   N segment: out[r] = sum_j M[r,j] xin[j]  -- row r owned by row-group (out_off+r) % 16,
+//              8-lane shuffle reduction, owner writes the shared-memory output: no atomics.
+//   H segment: out[j] = sum_r conj(M[r,j]) xin[r] -- lane accumulators per column j = g+8k,
+//              reduced over row-groups with shuffles + a fixed-order cross-warp sum
+//              (deterministic, bit-reproducible).
+//   S segment: out[j] = sum_r M[r,j] (partial-vector reduction, coherent ld.cg loads).
+//
+// Modes: PHASED = one launch per phase (one CTA per op); FUSED = one persistent launch where
+// CTAs claim ops from a ticket counter in a topological order and spin on per-op dependency
+// counters (ld.acquire.gpu) -- the nearfield ops fill the dependency bubbles of the farfield
+// chain.  Waits only target ops with a smaller ticket, which were claimed by running CTAs, so
+// progress does not depend on co-residency.  The last CTA to exit resets all counters, so the
+// launch is self-cleaning and CUDA-graph capturable.
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/uhmv.h"
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr int kWarps = kThreads / 32;
+constexpr int kLanesPerRow = 8;
+constexpr int kRowGroups = kThreads / kLanesPerRow;  // 16
+constexpr int kHAcc = 4;                             // H/S accumulators per lane
+constexpr int kHColsMax = kHAcc * kLanesPerRow;      // 32 (= packer.HCOLS_MAX)
+
+constexpr int kModeN = 0, kModeH = 1, kModeS = 2;
+constexpr int kBufArena = 0, kBufWork = 1, kBufX = 2, kBufW = 3;
+constexpr int kOpFields = 16, kSegFields = 8, kRunFields = 5;
+
+struct ExecParams {
+    const double2* arena;
+    double2* work;
+    const double2* x;
+    double2* w;
+    const int32_t* ops;
+    const int64_t* segs;
+    const int64_t* runs;
+    const int32_t* waits;
+    const int32_t* sigs;
+    const int32_t* fused_order;
+    int32_t op_begin;
+    int32_t op_count;
+    uint32_t* counters;
+    unsigned long long* ticket;
+    uint32_t* exit_count;
+    int32_t n_counters;
+    int32_t in_max;
+    int32_t out_max;
+};
+
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(r.x), "=d"(r.y)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// acc += m * x
+__device__ __forceinline__ void cmac(double& ar, double& ai, const double2 m, const double2 x) {
+    ar = fma(m.x, x.x, ar);
+    ar = fma(-m.y, x.y, ar);
+    ai = fma(m.x, x.y, ai);
+    ai = fma(m.y, x.x, ai);
+}
+
+// acc += conj(m) * x
+__device__ __forceinline__ void cmac_conj(double& ar, double& ai, const double2 m, const double2 x) {
+    ar = fma(m.x, x.x, ar);
+    ar = fma(m.y, x.y, ar);
+    ai = fma(m.x, x.y, ai);
+    ai = fma(-m.y, x.x, ai);
+}
+
+struct SegDesc {
+    int64_t m_off;
+    int32_t buf, rows, cols, ld, mode, in_off, out_off;
+};
+
+__device__ __forceinline__ SegDesc load_seg(const int64_t* segs, int s) {
+    const int64_t* d = segs + (int64_t)s * kSegFields;
+    SegDesc r;
+    r.m_off = __ldg(d + 0);
+    r.buf = (int32_t)__ldg(d + 1);
+    r.rows = (int32_t)__ldg(d + 2);
+    r.cols = (int32_t)__ldg(d + 3);
+    r.ld = (int32_t)__ldg(d + 4);
+    r.mode = (int32_t)__ldg(d + 5);
+    r.in_off = (int32_t)__ldg(d + 6);
+    r.out_off = (int32_t)__ldg(d + 7);
+    return r;
+}
+
+// ---- N group: consecutive N segments sharing (out_off, rows) ------------------------------
+__device__ __forceinline__ void run_ngroup(const ExecParams& p, int s_begin, int s_end, int rows,
+                                           int out_off, const double2* xin, double2* outv) {
+    const int tid = threadIdx.x;
+    const int g = tid & (kLanesPerRow - 1);
+    const int rg = tid / kLanesPerRow;
+    const unsigned gmask = 0xffu << ((tid & 31) & ~(kLanesPerRow - 1));
+    int r0 = (rg - (out_off % kRowGroups)) % kRowGroups;
+    if (r0 < 0) r0 += kRowGroups;
+    for (int r = r0; r < rows; r += kRowGroups) {
+        double ar = 0.0, ai = 0.0;
+        for (int s = s_begin; s < s_end; ++s) {
+            const SegDesc d = load_seg(p.segs, s);
+            const double2* M = p.arena + d.m_off + (int64_t)r * d.ld;
+            const double2* xv = xin + d.in_off;
+            const int cols = d.cols;
+            int j = g;
+            for (; j + 3 * kLanesPerRow < cols; j += 4 * kLanesPerRow) {
+                const double2 m0 = ld_stream(M + j);
+                const double2 m1 = ld_stream(M + j + kLanesPerRow);
+                const double2 m2 = ld_stream(M + j + 2 * kLanesPerRow);
+                const double2 m3 = ld_stream(M + j + 3 * kLanesPerRow);
+                cmac(ar, ai, m0, xv[j]);
+                cmac(ar, ai, m1, xv[j + kLanesPerRow]);
+                cmac(ar, ai, m2, xv[j + 2 * kLanesPerRow]);
+                cmac(ar, ai, m3, xv[j + 3 * kLanesPerRow]);
+            }
+            for (; j < cols; j += kLanesPerRow) cmac(ar, ai, ld_stream(M + j), xv[j]);
+        }
+#pragma unroll
+        for (int o = 1; o < kLanesPerRow; o <<= 1) {
+            ar += __shfl_xor_sync(gmask, ar, o);
+            ai += __shfl_xor_sync(gmask, ai, o);
+        }
+        if (g == 0) {
+            double2 v = outv[out_off + r];
+            v.x += ar;
+            v.y += ai;
+            outv[out_off + r] = v;
+        }
+    }
+}
+
+// ---- H / S group: consecutive segments sharing (mode, out_off, cols), cols <= kHColsMax ----
+template <int MODE>
+__device__ __forceinline__ void run_hgroup(const ExecParams& p, int s_begin, int s_end, int cols,
+                                           int out_off, const double2* xin, double2* outv,
+                                           double2* red) {
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int g = tid & (kLanesPerRow - 1);
+    const int rg = tid / kLanesPerRow;
+    double ar[kHAcc], ai[kHAcc];
+#pragma unroll
+    for (int k = 0; k < kHAcc; ++k) ar[k] = ai[k] = 0.0;
+    for (int s = s_begin; s < s_end; ++s) {
+        const SegDesc d = load_seg(p.segs, s);
+        const double2* base = (MODE == kModeS) ? p.work : p.arena;
+        for (int r = rg; r < d.rows; r += kRowGroups) {
+            const double2* M = base + d.m_off + (int64_t)r * d.ld;
+            double2 m[kHAcc];
+#pragma unroll
+            for (int k = 0; k < kHAcc; ++k) {
+                const int j = g + k * kLanesPerRow;
+                if (j < cols) {
+                    m[k] = (MODE == kModeS) ? __ldcg(M + j) : ld_stream(M + j);
+                } else {
+                    m[k] = make_double2(0.0, 0.0);
+                }
+            }
+            if (MODE == kModeS) {
+#pragma unroll
+                for (int k = 0; k < kHAcc; ++k) {
+                    ar[k] += m[k].x;
+                    ai[k] += m[k].y;
+                }
+            } else {
+                const double2 xv = xin[d.in_off + r];
+#pragma unroll
+                for (int k = 0; k < kHAcc; ++k) cmac_conj(ar[k], ai[k], m[k], xv);
+            }
+        }
+    }
+    // reduce over the 4 row-groups of the warp (lanes g, g+8, g+16, g+24)
+#pragma unroll
+    for (int k = 0; k < kHAcc; ++k) {
+        ar[k] += __shfl_xor_sync(0xffffffffu, ar[k], 8);
+        ai[k] += __shfl_xor_sync(0xffffffffu, ai[k], 8);
+        ar[k] += __shfl_xor_sync(0xffffffffu, ar[k], 16);
+        ai[k] += __shfl_xor_sync(0xffffffffu, ai[k], 16);
+    }
+    if (lane < kLanesPerRow) {
+#pragma unroll
+        for (int k = 0; k < kHAcc; ++k) {
+            const int j = g + k * kLanesPerRow;
+            if (j < cols) red[warp * kHColsMax + j] = make_double2(ar[k], ai[k]);
+        }
+    }
+    __syncthreads();
+    for (int j = tid; j < cols; j += kThreads) {
+        double2 acc = outv[out_off + j];
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const double2 v = red[w * kHColsMax + j];
+            acc.x += v.x;
+            acc.y += v.y;
+        }
+        outv[out_off + j] = acc;
+    }
+    __syncthreads();
+}
+
+template <bool FUSED>
+__device__ void run_op(const ExecParams& p, int op, double2* xin, double2* outv, double2* red,
+                       int* hdr) {
+    const int tid = threadIdx.x;
+    if (tid < kOpFields) hdr[tid] = __ldg(p.ops + (int64_t)op * kOpFields + tid);
+    __syncthreads();
+    const int n_out = hdr[1];
+    const int in_b = hdr[2], in_e = hdr[3];
+    const int seg_b = hdr[4], seg_e = hdr[5];
+    const int out_b = hdr[6], out_e = hdr[7];
+    if (FUSED) {
+        if (tid == 0) {
+            const int wb = hdr[8], we = hdr[9];
+            for (int i = wb; i < we; ++i) {
+                const int c = __ldg(p.waits + 2 * i);
+                const uint32_t need = (uint32_t)__ldg(p.waits + 2 * i + 1);
+                while (ld_acquire(p.counters + c) < need) __nanosleep(32);
+            }
+        }
+        __syncthreads();
+    }
+    // gather the op's input vector into shared memory
+    for (int r = in_b; r < in_e; ++r) {
+        const int64_t* rd = p.runs + (int64_t)r * kRunFields;
+        const int buf = (int)__ldg(rd + 0);
+        const int64_t off = __ldg(rd + 1);
+        const int len = (int)__ldg(rd + 2);
+        const int dst = (int)__ldg(rd + 3);
+        if (buf == kBufX) {
+            for (int i = tid; i < len; i += kThreads) xin[dst + i] = __ldg(p.x + off + i);
+        } else {
+            for (int i = tid; i < len; i += kThreads) xin[dst + i] = __ldcg(p.work + off + i);
+        }
+    }
+    for (int i = tid; i < n_out; i += kThreads) outv[i] = make_double2(0.0, 0.0);
+    __syncthreads();
+
+    int s = seg_b;
+    while (s < seg_e) {
+        const SegDesc d = load_seg(p.segs, s);
+        int e = s + 1;
+        if (d.mode == kModeN) {
+            while (e < seg_e) {
+                const SegDesc n = load_seg(p.segs, e);
+                if (n.mode != kModeN || n.out_off != d.out_off || n.rows != d.rows) break;
+                ++e;
+            }
+            run_ngroup(p, s, e, d.rows, d.out_off, xin, outv);
+        } else {
+            while (e < seg_e) {
+                const SegDesc n = load_seg(p.segs, e);
+                if (n.mode != d.mode || n.out_off != d.out_off || n.cols != d.cols) break;
+                ++e;
+            }
+            // N groups precede H/S groups (packer order); the barrier inside run_hgroup orders
+            // the owner-written N rows before the cross-warp sums touch the output.
+            if (d.mode == kModeH)
+                run_hgroup<kModeH>(p, s, e, d.cols, d.out_off, xin, outv, red);
+            else
+                run_hgroup<kModeS>(p, s, e, d.cols, d.out_off, xin, outv, red);
+        }
+        s = e;
+    }
+    __syncthreads();
+    // scatter the output vector
+    for (int r = out_b; r < out_e; ++r) {
+        const int64_t* rd = p.runs + (int64_t)r * kRunFields;
+        const int buf = (int)__ldg(rd + 0);
+        const int64_t off = __ldg(rd + 1);
+        const int len = (int)__ldg(rd + 2);
+        const int dst = (int)__ldg(rd + 3);
+        const int add = (int)(__ldg(rd + 4) & 1);
+        double2* dp = (buf == kBufW ? p.w : p.work) + off;
+        for (int i = tid; i < len; i += kThreads) {
+            double2 v = outv[dst + i];
+            if (add) {
+                const double2 o = __ldcg(dp + i);
+                v.x += o.x;
+                v.y += o.y;
+            }
+            __stcg(dp + i, v);
+        }
+    }
+    if (FUSED) {
+        __syncthreads();
+        if (tid == 0) {
+            const int sb = hdr[10], se = hdr[11];
+            if (se > sb) {
+                __threadfence();
+                for (int i = sb; i < se; ++i) atomicAdd(p.counters + __ldg(p.sigs + i), 1u);
+            }
+        }
+    }
+    __syncthreads();
+}
+
+struct SmemLayout {
+    int xin_off, out_off, red_off, hdr_off, total;
+};
+
+__host__ __device__ inline SmemLayout smem_layout(int in_max, int out_max) {
+    SmemLayout L;
+    L.xin_off = 0;
+    L.out_off = L.xin_off + in_max * 16;
+    L.red_off = L.out_off + out_max * 16;
+    L.hdr_off = L.red_off + kWarps * kHColsMax * 16;
+    L.total = L.hdr_off + (kOpFields + 4) * 4;
+    return L;
+}
+
+__global__ void __launch_bounds__(kThreads) uhmv_phase_kernel(const ExecParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemLayout L = smem_layout(p.in_max, p.out_max);
+    double2* xin = reinterpret_cast<double2*>(smem + L.xin_off);
+    double2* outv = reinterpret_cast<double2*>(smem + L.out_off);
+    double2* red = reinterpret_cast<double2*>(smem + L.red_off);
+    int* hdr = reinterpret_cast<int*>(smem + L.hdr_off);
+    run_op<false>(p, p.op_begin + (int)blockIdx.x, xin, outv, red, hdr);
+}
+
+__global__ void __launch_bounds__(kThreads) uhmv_fused_kernel(const ExecParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const SmemLayout L = smem_layout(p.in_max, p.out_max);
+    double2* xin = reinterpret_cast<double2*>(smem + L.xin_off);
+    double2* outv = reinterpret_cast<double2*>(smem + L.out_off);
+    double2* red = reinterpret_cast<double2*>(smem + L.red_off);
+    int* hdr = reinterpret_cast<int*>(smem + L.hdr_off);
+    int* slot = hdr + kOpFields;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            const unsigned long long t = atomicAdd(p.ticket, 1ull);
+            slot[0] = (t < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t) : -1;
+        }
+        __syncthreads();
+        const int op = slot[0];
+        __syncthreads();
+        if (op < 0) break;
+        run_op<true>(p, op, xin, outv, red, hdr);
+    }
+    // self-reset: the last CTA out zeroes the counters for the next launch
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(p.exit_count, 1u);
+        slot[1] = (prev == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (slot[1]) {
+        __threadfence();
+        for (int i = threadIdx.x; i < p.n_counters; i += kThreads) p.counters[i] = 0u;
+        if (threadIdx.x == 0) {
+            *p.ticket = 0ull;
+            *p.exit_count = 0u;
+        }
+        __threadfence();
+    }
+}
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(UHMV_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+struct uhmv_plan {
+    uhmv_desc d;
+    int fused_grid[2];
+    int smem[2];
+    int sm_count;
+};
+
+extern "C" {
+
+int uhmv_abi_version(void) { return UHMV_ABI_VERSION; }
+
+const char* uhmv_last_error(void) { return g_last_error.c_str(); }
+
+static int check_program(const uhmv_program& pr, const char* name) {
+    if (pr.n_ops < 0 || pr.n_phases < 0 || pr.n_phases > UHMV_MAX_PHASES)
+        return fail(UHMV_EINVAL, std::string(name) + ": bad op/phase count");
+    if (pr.n_ops > 0 && (!pr.ops || !pr.segs || !pr.runs || !pr.fused_order))
+        return fail(UHMV_EINVAL, std::string(name) + ": null table pointer");
+    if (pr.in_max < 0 || pr.out_max < 0 || pr.n_counters < 0)
+        return fail(UHMV_EINVAL, std::string(name) + ": negative size");
+    for (int i = 0; i < pr.n_phases; ++i)
+        if (pr.phase_lo[i] < 0 || pr.phase_hi[i] < pr.phase_lo[i] || pr.phase_hi[i] > pr.n_ops)
+            return fail(UHMV_EINVAL, std::string(name) + ": bad phase bounds");
+    return UHMV_OK;
+}
+
+int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
+    if (!desc || !out) return fail(UHMV_EINVAL, "uhmv_plan_create: null argument");
+    *out = nullptr;
+    if (desc->abi_version != UHMV_ABI_VERSION)
+        return fail(UHMV_EINVAL, "uhmv_plan_create: ABI version mismatch");
+    if (desc->n_rows < 0 || desc->n_cols < 0) return fail(UHMV_EINVAL, "negative shape");
+    if (!desc->counters || !desc->ticket || !desc->exit_count || !desc->arena || !desc->work)
+        return fail(UHMV_EINVAL, "uhmv_plan_create: null device buffer");
+    int rc = check_program(desc->fwd, "fwd");
+    if (rc) return rc;
+    rc = check_program(desc->adj, "adj");
+    if (rc) return rc;
+    cudaError_t e = cudaSetDevice(desc->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    uhmv_plan* p = new (std::nothrow) uhmv_plan;
+    if (!p) return fail(UHMV_ENOMEM, "uhmv_plan_create: out of host memory");
+    std::memset(p, 0, sizeof(*p));
+    p->d = *desc;
+    e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, desc->device);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "cudaDeviceGetAttribute");
+    }
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, desc->device);
+    const uhmv_program* progs[2] = {&desc->fwd, &desc->adj};
+    int need = 0;
+    for (int k = 0; k < 2; ++k) {
+        p->smem[k] = smem_layout(progs[k]->in_max, progs[k]->out_max).total;
+        if (p->smem[k] > need) need = p->smem[k];
+    }
+    if (need > smem_optin) {
+        delete p;
+        return fail(UHMV_EINVAL, "op vectors exceed shared memory (" + std::to_string(need) +
+                                     " > " + std::to_string(smem_optin) + " bytes)");
+    }
+    e = cudaFuncSetAttribute(uhmv_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(uhmv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 need);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "cudaFuncSetAttribute");
+    }
+    for (int k = 0; k < 2; ++k) {
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, uhmv_fused_kernel, kThreads,
+                                                          p->smem[k]);
+        if (e != cudaSuccess) {
+            delete p;
+            return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+        }
+        if (per_sm < 1) per_sm = 1;
+        int grid = per_sm * p->sm_count;
+        if (grid > progs[k]->n_ops) grid = progs[k]->n_ops > 0 ? progs[k]->n_ops : 1;
+        p->fused_grid[k] = grid;
+    }
+    *out = p;
+    return UHMV_OK;
+}
+
+static ExecParams make_params(const uhmv_plan* plan, const uhmv_program& pr, const void* x,
+                              void* w) {
+    ExecParams ep;
+    ep.arena = static_cast<const double2*>(plan->d.arena);
+    ep.work = static_cast<double2*>(plan->d.work);
+    ep.x = static_cast<const double2*>(x);
+    ep.w = static_cast<double2*>(w);
+    ep.ops = pr.ops;
+    ep.segs = pr.segs;
+    ep.runs = pr.runs;
+    ep.waits = pr.waits;
+    ep.sigs = pr.sigs;
+    ep.fused_order = pr.fused_order;
+    ep.op_begin = 0;
+    ep.op_count = pr.n_ops;
+    ep.counters = plan->d.counters;
+    ep.ticket = plan->d.ticket;
+    ep.exit_count = plan->d.exit_count;
+    ep.n_counters = pr.n_counters;
+    ep.in_max = pr.in_max;
+    ep.out_max = pr.out_max;
+    return ep;
+}
+
+int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, int phase_lo,
+                        int phase_hi, void* stream) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_execute_phases: null plan");
+    const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
+    const int k = adjoint ? 1 : 0;
+    if (phase_lo < 0 || phase_hi > pr.n_phases || phase_lo > phase_hi)
+        return fail(UHMV_EINVAL, "uhmv_execute_phases: bad phase range");
+    if (pr.n_ops > 0 && (!x || !w)) return fail(UHMV_EINVAL, "null vector pointer");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ExecParams ep = make_params(plan, pr, x, w);
+    for (int ph = phase_lo; ph < phase_hi; ++ph) {
+        const int n = pr.phase_hi[ph] - pr.phase_lo[ph];
+        if (n <= 0) continue;
+        ep.op_begin = pr.phase_lo[ph];
+        uhmv_phase_kernel<<<n, kThreads, plan->smem[k], st>>>(ep);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "uhmv_phase_kernel launch");
+    return UHMV_OK;
+}
+
+int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode, void* stream) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_execute: null plan");
+    const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
+    if (mode == UHMV_MODE_PHASED)
+        return uhmv_execute_phases(plan, x, w, adjoint, 0, pr.n_phases, stream);
+    if (mode != UHMV_MODE_FUSED) return fail(UHMV_EINVAL, "uhmv_execute: unknown mode");
+    if (pr.n_ops == 0) return UHMV_OK;
+    if (!x || !w) return fail(UHMV_EINVAL, "null vector pointer");
+    const int k = adjoint ? 1 : 0;
+    ExecParams ep = make_params(plan, pr, x, w);
+    uhmv_fused_kernel<<<plan->fused_grid[k], kThreads, plan->smem[k],
+                        static_cast<cudaStream_t>(stream)>>>(ep);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "uhmv_fused_kernel launch");
+    return UHMV_OK;
+}
+
+int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
+                     void* stream) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_matvec_host: null plan");
+    if (!plan->d.x_scratch || !plan->d.w_scratch)
+        return fail(UHMV_EINVAL, "uhmv_matvec_host: plan has no scratch vectors");
+    if (!x_host || !w_host) return fail(UHMV_EINVAL, "uhmv_matvec_host: null host pointer");
+    const int64_t n_in = adjoint ? plan->d.n_rows : plan->d.n_cols;
+    const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(plan->d.x_scratch, x_host, (size_t)n_in * 16,
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");
+    int rc = uhmv_execute(plan, plan->d.x_scratch, plan->d.w_scratch, adjoint, mode, stream);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(w_host, plan->d.w_scratch, (size_t)n_out * 16, cudaMemcpyDeviceToHost,
+                        st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy of w");
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "uhmv_matvec_host synchronize");
+    return UHMV_OK;
+}
+
+int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int* fused_grid, int* smem_bytes,
+                   int* threads_per_cta) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_info: null plan");
+    const int k = adjoint ? 1 : 0;
+    if (fused_grid) *fused_grid = plan->fused_grid[k];
+    if (smem_bytes) *smem_bytes = plan->smem[k];
+    if (threads_per_cta) *threads_per_cta = kThreads;
+    return UHMV_OK;
+}
+
+int uhmv_plan_destroy(uhmv_plan* plan) {
+    delete plan;
+    return UHMV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,194 @@
+"""Device-resident packed operator: PyTorch owns the buffers, libuhmv.so runs the kernels.
+
+PyTorch is plumbing here (device memory, streams, torch.distributed); every FLOP of the
+matvec runs in the hand-written sm_100a kernels of csrc/uhmv.cu behind the C ABI of
+include/uhmv.h.  There is no CPU or PyTorch fallback: without CUDA this raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import _lib
+from .packer import PackedOperator, Program
+
+__all__ = ["DeviceOperator", "default_mode"]
+
+_MODES = {"phased": _lib.MODE_PHASED, "fused": _lib.MODE_FUSED}
+
+
+def default_mode() -> str:
+    return os.environ.get("UHMV_MODE", "fused")
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("uniform-H matvec needs a CUDA device (sm_100a); there is no CPU fallback")
+    return torch
+
+
+class _DeviceProgram:
+    def __init__(self, torch, prog: Program, device):
+        def up(a, dtype):
+            a = np.ascontiguousarray(a)
+            if a.size == 0:
+                a = np.zeros(1, dtype=a.dtype)
+            return torch.from_numpy(a).to(device=device, dtype=dtype)
+
+        self.prog = prog
+        self.ops = up(prog.ops, torch.int32)
+        self.segs = up(prog.segs, torch.int64)
+        self.runs = up(prog.runs, torch.int64)
+        self.waits = up(prog.waits, torch.int32)
+        self.sigs = up(prog.sigs, torch.int32)
+        self.fused_order = up(prog.fused_order, torch.int32)
+
+    def struct(self) -> _lib.UhmvProgram:
+        p = self.prog
+        s = _lib.UhmvProgram()
+        s.n_ops = p.n_ops
+        s.ops = self.ops.data_ptr()
+        s.segs = self.segs.data_ptr()
+        s.runs = self.runs.data_ptr()
+        s.waits = self.waits.data_ptr()
+        s.sigs = self.sigs.data_ptr()
+        s.fused_order = self.fused_order.data_ptr()
+        if len(p.phases) > _lib.MAX_PHASES:
+            raise ValueError("too many phases")
+        s.n_phases = len(p.phases)
+        for i, (a, b) in enumerate(p.phases):
+            s.phase_lo[i] = a
+            s.phase_hi[i] = b
+        s.in_max = p.in_max
+        s.out_max = p.out_max
+        s.n_counters = p.n_counters
+        return s
+
+
+class DeviceOperator:
+    """A packed uniform H-matrix resident in HBM, with its C-ABI plan."""
+
+    def __init__(self, packed: PackedOperator, device=None):
+        torch = _torch()
+        L = _lib.lib()
+        self.torch = torch
+        self.packed = packed
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.arena = torch.from_numpy(packed.arena).to(dev)
+        self.work = torch.zeros(packed.work_len, dtype=torch.complex128, device=dev)
+        n_ctr = max(packed.fwd.n_counters, packed.adj.n_counters, 1)
+        self.counters = torch.zeros(n_ctr, dtype=torch.int32, device=dev)
+        self.ticket = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.exit_count = torch.zeros(1, dtype=torch.int32, device=dev)
+        nmax = max(packed.n_rows, packed.n_cols, 1)
+        self.x_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
+        self.w_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
+        self.fwd = _DeviceProgram(torch, packed.fwd, dev)
+        self.adj = _DeviceProgram(torch, packed.adj, dev)
+        d = _lib.UhmvDesc()
+        d.abi_version = _lib.ABI_VERSION
+        d.device = dev.index
+        d.n_rows = packed.n_rows
+        d.n_cols = packed.n_cols
+        d.arena = self.arena.data_ptr()
+        d.work = self.work.data_ptr()
+        d.work_len = packed.work_len
+        d.counters = self.counters.data_ptr()
+        d.ticket = self.ticket.data_ptr()
+        d.exit_count = self.exit_count.data_ptr()
+        d.x_scratch = self.x_scratch.data_ptr()
+        d.w_scratch = self.w_scratch.data_ptr()
+        d.fwd = self.fwd.struct()
+        d.adj = self.adj.struct()
+        self._desc = d
+        handle = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            _lib.check(L.uhmv_plan_create(ctypes.byref(d), ctypes.byref(handle)), "uhmv_plan_create")
+        self._plan = handle
+        self._lock = threading.Lock()
+
+    # ---- info ----
+    def launch_info(self, adjoint=False):
+        g, s, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _lib.check(
+            _lib.lib().uhmv_plan_info(self._plan, int(adjoint), ctypes.byref(g), ctypes.byref(s), ctypes.byref(t)),
+            "uhmv_plan_info",
+        )
+        return {"fused_grid": g.value, "smem_bytes": s.value, "threads": t.value}
+
+    def kernel_launches(self, adjoint=False, mode=None) -> int:
+        """Number of our kernel launches one matvec issues."""
+        mode = mode or default_mode()
+        prog = self.packed.adj if adjoint else self.packed.fwd
+        if prog.n_ops == 0:
+            return 0
+        return 1 if mode == "fused" else len(prog.phases)
+
+    # ---- execution ----
+    def _stream(self, stream):
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def matvec(self, x, adjoint=False, out=None, mode=None, stream=None):
+        """Device API: x is a CUDA complex128 tensor (n_in,), returns/fills out (n_out,)."""
+        torch = self.torch
+        p = self.packed
+        n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
+        if x.shape != (n_in,) or x.dtype != torch.complex128 or x.device != self.device:
+            raise ValueError(f"x must be a complex128 {self.device} tensor of shape ({n_in},)")
+        x = x.contiguous()
+        if out is None:
+            out = torch.empty(n_out, dtype=torch.complex128, device=self.device)
+        mode = mode or default_mode()
+        rc = _lib.lib().uhmv_execute(
+            self._plan, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), int(adjoint),
+            _MODES[mode], self._stream(stream),
+        )
+        _lib.check(rc, "uhmv_execute")
+        return out
+
+    def execute_phases(self, x, out, adjoint, lo, hi, stream=None):
+        rc = _lib.lib().uhmv_execute_phases(
+            self._plan, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), int(adjoint),
+            int(lo), int(hi), self._stream(stream),
+        )
+        _lib.check(rc, "uhmv_execute_phases")
+
+    def matvec_host(self, x_host: np.ndarray, adjoint=False, out: np.ndarray | None = None, mode=None, stream=None):
+        """End-to-end C-ABI call with host buffers (H2D, kernels, D2H, sync)."""
+        p = self.packed
+        n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
+        x_host = np.ascontiguousarray(x_host, dtype=np.complex128)
+        if x_host.shape != (n_in,):
+            raise ValueError(f"x must have shape ({n_in},)")
+        if out is None:
+            out = np.empty(n_out, dtype=np.complex128)
+        mode = mode or default_mode()
+        with self._lock, self.torch.cuda.device(self.device):
+            rc = _lib.lib().uhmv_matvec_host(
+                self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data), int(adjoint),
+                _MODES[mode], self._stream(stream),
+            )
+        _lib.check(rc, "uhmv_matvec_host")
+        return out
+
+    def close(self):
+        if getattr(self, "_plan", None):
+            _lib.lib().uhmv_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

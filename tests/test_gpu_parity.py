@@ -1,0 +1,135 @@
+"""GPU parity through the C ABI: every golden operator, parity view, direction and mode.
+
+Gates: G1 full, G2 farfield-only, G3 nearfield-only, G4 adjoint of each --
+relative l2 <= 1e-12 against the reference's stored outputs AND the CPU oracle.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden, rel, views
+from matvec_oracle import oracle_matvec_uh
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from conftest import ensure_built
+
+    ensure_built()
+
+
+def _dev(u):
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer import pack
+
+    return DeviceOperator(pack(u), device="cuda:0")
+
+
+@pytest.mark.parametrize("mode", ["phased", "fused"])
+def test_device_matches_reference(golden, mode):
+    name, u, ex = golden
+    for vname, view, pfx in views():
+        uv = view(u)
+        dop = _dev(uv)
+        for k in range(int(ex["nvec"])):
+            for adj, vkey, okey in ((False, f"vf_{k}", f"{pfx}_fwd_{k}"), (True, f"va_{k}", f"{pfx}_adj_{k}")):
+                v = ex[vkey]
+                x = torch.from_numpy(np.asarray(v, dtype=np.complex128)).cuda()
+                w = dop.matvec(x, adjoint=adj, mode=mode).cpu().numpy()
+                assert rel(w, ex[okey]) <= TOL, (name, vname, adj, mode, rel(w, ex[okey]))
+                assert rel(w, oracle_matvec_uh(uv, v, adjoint=adj)) <= TOL
+                assert np.isfinite(w).all()
+
+
+def test_modes_bit_identical(golden):
+    name, u, ex = golden
+    dop = _dev(u)
+    x = torch.from_numpy(np.asarray(ex["vf_0"], dtype=np.complex128)).cuda()
+    a = dop.matvec(x, mode="phased").cpu().numpy()
+    b = dop.matvec(x, mode="fused").cpu().numpy()
+    c = dop.matvec(x, mode="fused").cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(b, c)
+
+
+def test_dropin_matvec_uh(golden):
+    """The reference-facing call: numpy in, numpy out, reference dtype and stats semantics."""
+    import paper_2405_15573_b200 as pk
+    from paper_2405_15573_b200.uh_types import MatvecStats
+
+    name, u, ex = golden
+    v = ex["vf_0"]
+    st = MatvecStats()
+    w = pk.matvec_uh(u, v, stats=st)
+    assert w.dtype == np.result_type(v.dtype, u._dtype)
+    assert rel(w, ex["ref_fwd_0"]) <= TOL
+    assert st.leaves_touched == int(ex["leaves_touched"])
+    wa = pk.matvec_uh(u, ex["va_0"], adjoint=True, workers=8)
+    assert rel(wa, ex["ref_adj_0"]) <= TOL
+    z = pk.matvec_uh(u, np.zeros(u.shape[1]))
+    assert not z.any()
+    assert not v.flags.writeable or np.array_equal(v, ex["vf_0"])  # input untouched
+    with pytest.raises(ValueError):
+        pk.matvec_uh(u, np.zeros(u.shape[1] + 1))
+    if "dense_fwd_0" in ex:
+        assert np.linalg.norm(w - ex["dense_fwd_0"]) <= 1e-12 * np.linalg.norm(w)
+
+
+def test_reference_pins_on_device():
+    """tests/test_uniform.py:315-361 + test_acceptance.py:165-195 re-asserted on the GPU path."""
+    import paper_2405_15573_b200 as pk
+
+    u, ex = load_golden("uh800_laplace")
+    assert not pk.matvec_uh(u, np.zeros(800)).any()
+    v = ex["vf_0"]
+    ref = ex["exact_fwd_0"]
+    vn = v / np.linalg.norm(v)
+    assert np.linalg.norm(pk.matvec_uh(u, vn) - ref / np.linalg.norm(v)) / np.linalg.norm(ref / np.linalg.norm(v)) <= 1e-3
+    w = pk.matvec_uh(u, v)
+    assert np.linalg.norm(w - ex["dense_fwd_0"]) <= 1e-12 * np.linalg.norm(w)
+    w1 = pk.matvec_uh(u, v, workers=1)
+    w8 = pk.matvec_uh(u, v, workers=8)
+    assert np.linalg.norm(w1 - w8) <= 1e-12 * np.linalg.norm(w1)
+    wa = pk.matvec_uh(u, ex["va_1"], adjoint=True)
+    assert np.linalg.norm(wa - ex["dense_adj_1"]) <= 1e-12 * np.linalg.norm(wa)
+    uc, exc = load_golden("helm400")
+    wc = pk.matvec_uh(uc, exc["vf_0"])
+    assert np.linalg.norm(wc - exc["exact_fwd_0"]) / np.linalg.norm(exc["exact_fwd_0"]) <= 1e-4
+
+
+def test_device_tensor_api():
+    import paper_2405_15573_b200 as pk
+
+    u, ex = load_golden("helm400")
+    x = torch.from_numpy(ex["vf_0"]).cuda()
+    w = pk.matvec_uh(u, x)
+    assert isinstance(w, torch.Tensor) and w.is_cuda
+    assert rel(w.cpu().numpy(), ex["ref_fwd_0"]) <= TOL
+
+
+def test_host_abi_entry():
+    """uhmv_matvec_host: host buffers in/out through the C ABI."""
+    u, ex = load_golden("ico2_helm_compress")
+    dop = _dev(u)
+    for mode in ("phased", "fused"):
+        w = dop.matvec_host(ex["vf_0"], mode=mode)
+        assert rel(w, ex["ref_fwd_0"]) <= TOL
+        wa = dop.matvec_host(ex["va_0"], adjoint=True, mode=mode)
+        assert rel(wa, ex["ref_adj_0"]) <= TOL
+
+
+def test_repeated_fused_launches_self_reset():
+    u, ex = load_golden("ico2_helm_compress")
+    dop = _dev(u)
+    x = torch.from_numpy(ex["vf_0"]).cuda()
+    first = dop.matvec(x, mode="fused").cpu().numpy()
+    for _ in range(50):
+        w = dop.matvec(x, mode="fused")
+    torch.cuda.synchronize()
+    assert np.array_equal(w.cpu().numpy(), first)
+    assert int(dop.counters.abs().sum()) == 0 and int(dop.ticket.item()) == 0

@@ -1,0 +1,82 @@
+"""Full-size parity at the BASELINE configs (seeded synthetic values on the reference
+structures): GPU vs the CPU oracle and vs the reference samples recorded in the build
+container; size-independent properties (linearity, adjoint identity, determinism)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel
+from matvec_oracle import farfield_only, nearfield_only, oracle_matvec_uh
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from conftest import ensure_built
+
+    ensure_built()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_config_parity(cfg):
+    from paper_2405_15573_b200 import workloads
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer import pack
+
+    if not os.path.exists(workloads.workload_path(cfg)):
+        pytest.skip("fixture missing")
+    u = workloads.build_operator(cfg)
+    _, d = workloads.load_structure(cfg)
+    x_np = workloads.seeded_vector(u.shape[1], 0)
+    x = torch.from_numpy(x_np).cuda()
+    for view in (lambda a: a, farfield_only, nearfield_only):
+        uv = view(u)
+        dop = DeviceOperator(pack(uv), device="cuda:0")
+        for adj in (False, True):
+            ref = oracle_matvec_uh(uv, x_np, adjoint=adj)
+            for mode in ("phased", "fused"):
+                w = dop.matvec(x, adjoint=adj, mode=mode).cpu().numpy()
+                assert rel(w, ref) <= TOL, (cfg, adj, mode, rel(w, ref))
+        del dop
+    if "x_ref_synth_sample" in d:
+        from paper_2405_15573_b200.device import DeviceOperator
+
+        dop = DeviceOperator(pack(u), device="cuda:0")
+        s = int(d["x_ref_synth_stride"])
+        w = dop.matvec(x).cpu().numpy()
+        assert rel(w[::s], d["x_ref_synth_sample"]) <= TOL
+        wa = dop.matvec(x, adjoint=True).cpu().numpy()
+        assert rel(wa[::s], d["x_ref_synth_adj_sample"]) <= TOL
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_config_properties(cfg):
+    """Linearity, <Ax,y> = <x,A^H y>, bitwise determinism -- size-independent checks."""
+    from paper_2405_15573_b200 import workloads
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer import pack
+
+    if not os.path.exists(workloads.workload_path(cfg)):
+        pytest.skip("fixture missing")
+    u = workloads.build_operator(cfg)
+    dop = DeviceOperator(pack(u), device="cuda:0")
+    n = u.shape[1]
+    x = torch.from_numpy(workloads.seeded_vector(n, 1)).cuda()
+    y = torch.from_numpy(workloads.seeded_vector(n, 2)).cuda()
+    a, b = 0.3 - 1.1j, -2.0 + 0.5j
+    ax = dop.matvec(x)
+    ay = dop.matvec(y)
+    lin = dop.matvec(a * x + b * y)
+    assert (torch.linalg.norm(lin - (a * ax + b * ay)) / torch.linalg.norm(lin)).item() <= 1e-12
+    lhs = torch.vdot(ay, x)  # <A y, x>
+    rhs = torch.vdot(y, dop.matvec(x, adjoint=True))  # <y, A^H x>
+    assert abs((lhs - rhs).item()) <= 1e-11 * abs(lhs.item())
+    again = dop.matvec(x, mode="phased")
+    assert torch.equal(again, ax)

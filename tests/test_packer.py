@@ -1,0 +1,144 @@
+"""Packed layout + op programs (P0 packer) checked on the CPU with the NumPy VM.
+
+The VM (oracle/packed_vm.py) walks the arena and op tables exactly as the CUDA kernel
+does; matching the reference's stored outputs here pins the layout before any GPU
+run.  Structure gate G6: packed block ranges and slabs equal the
+reference objects bit for bit.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rel, views
+from packed_vm import vm_matvec
+from paper_2405_15573_b200.packer import (
+    BUF_ARENA,
+    BUF_WORK,
+    HCOLS_MAX,
+    KIND_FAR,
+    KIND_NEAR,
+    MODE_N,
+    MODE_S,
+    pack,
+)
+
+TOL = 1e-12
+
+
+@pytest.mark.parametrize("order", ["phased", "fused"])
+def test_vm_matches_reference(golden, order):
+    name, u, ex = golden
+    for vname, view, pfx in views():
+        p = pack(view(u))
+        for k in range(int(ex["nvec"])):
+            w = vm_matvec(p, ex[f"vf_{k}"], order=order)
+            assert rel(w, ex[f"{pfx}_fwd_{k}"]) <= TOL, (name, vname, order)
+            w = vm_matvec(p, ex[f"va_{k}"], adjoint=True, order=order)
+            assert rel(w, ex[f"{pfx}_adj_{k}"]) <= TOL, (name, vname, order, "adj")
+
+
+def test_program_invariants(golden):
+    name, u, ex = golden
+    p = pack(u)
+    for prog, n_out in ((p.fwd, p.n_rows), (p.adj, p.n_cols)):
+        # fused order is a permutation; every wait targets an earlier ticket
+        assert sorted(prog.fused_order.tolist()) == list(range(prog.n_ops))
+        pos = np.empty(prog.n_ops, dtype=np.int64)
+        pos[prog.fused_order] = np.arange(prog.n_ops)
+        producers = {}
+        for i in range(prog.n_ops):
+            sb, se = prog.ops[i, 10], prog.ops[i, 11]
+            for c in prog.sigs[sb:se]:
+                producers.setdefault(int(c), []).append(i)
+        for i in range(prog.n_ops):
+            wb, we = prog.ops[i, 8], prog.ops[i, 9]
+            for c, cnt in prog.waits[wb:we]:
+                ps = producers.get(int(c), [])
+                assert len(ps) == cnt, (name, i, c)
+                assert all(pos[q] < pos[i] for q in ps)
+        # each output element is written by exactly one store (NEAR/ZERO/FAR), FAR adds after NEAR
+        cover = np.zeros(n_out, dtype=np.int64)
+        for i in range(prog.n_ops):
+            ob, oe = prog.ops[i, 6], prog.ops[i, 7]
+            for buf, off, ln, dst, flags in prog.runs[ob:oe]:
+                if buf == 3 and not (flags & 1):
+                    cover[off : off + ln] += 1
+        assert (cover == 1).all()
+        # segment limits the kernel relies on
+        segs = prog.segs
+        hmask = segs[:, 5] != MODE_N
+        assert (segs[hmask, 3] <= HCOLS_MAX).all()
+        assert ((segs[:, 1] == BUF_WORK) == (segs[:, 5] == MODE_S)).all()
+        assert (segs[:, 1] == BUF_ARENA).sum() + (segs[:, 1] == BUF_WORK).sum() == len(segs)
+        assert (segs[:, 2] > 0).all() and (segs[:, 3] > 0).all()
+        # slabs stay inside the arena
+        arena_seg = segs[segs[:, 1] == BUF_ARENA]
+        last = arena_seg[:, 0] + (arena_seg[:, 2] - 1) * arena_seg[:, 4] + arena_seg[:, 3]
+        assert (last <= p.arena.size).all()
+
+
+def test_structure_bit_exact(golden):
+    """G6: every packed slab is the reference array bit for bit; ranges match block_ranges."""
+    name, u, ex = golden
+    p = pack(u)
+    bct = u.bct
+    # dense slabs: find each dense block through the forward NEAR ops
+    prog = p.fwd
+    seen = 0
+    for i in np.nonzero(prog.kinds == KIND_NEAR)[0]:
+        sb, se = prog.ops[i, 4], prog.ops[i, 5]
+        ib = prog.ops[i, 2]
+        for s in prog.segs[sb:se]:
+            m_off, _, rows, cols, ld = s[:5]
+            slab = p.arena[m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]]
+            # locate the block by its column range
+            run = [r for r in prog.runs[ib : prog.ops[i, 3]] if r[3] == s[6]][0]
+            c_lo, c_len = run[1], run[2]
+            out = [r for r in prog.runs[prog.ops[i, 6] : prog.ops[i, 7]]][0]
+            r_lo = out[1]
+            matches = [
+                b for b in u.dense
+                if bct.block_ranges(b)[2] == c_lo and bct.block_ranges(b)[3] == c_lo + c_len
+                and bct.block_ranges(b)[0] <= r_lo < bct.block_ranges(b)[1]
+            ]
+            assert len(matches) == 1
+            b = matches[0]
+            r0 = r_lo - bct.block_ranges(b)[0]
+            ref = np.asarray(u.dense[b], dtype=np.complex128)[r0 : r0 + rows]
+            assert np.array_equal(slab, ref)
+            seen += rows * cols
+    assert seen == sum(d.size for d in u.dense.values())
+    # basis slabs through the FAR ops: rows of U_s for the chunk
+    for i in np.nonzero(prog.kinds == KIND_FAR)[0]:
+        out = prog.runs[prog.ops[i, 6]]
+        r_lo = out[1]
+        for s in prog.segs[prog.ops[i, 4] : prog.ops[i, 5]]:
+            m_off, _, rows, cols, ld = s[:5]
+            slab = p.arena[m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]]
+            hits = [
+                c for c, m in u.row_basis.matrices.items()
+                if c in bct.row_map and m.shape[1] == cols
+                and bct.row_tree.nodes[c].lo <= r_lo < bct.row_tree.nodes[c].hi
+                and np.array_equal(slab, np.asarray(m, dtype=np.complex128)[r_lo - bct.row_tree.nodes[c].lo :][:rows])
+            ]
+            assert hits
+
+
+def test_bytes_accounting(golden):
+    name, u, ex = golden
+    p = pack(u)
+    bases = sum(
+        u.row_basis.matrices[s].size for s in u.bct.row_map
+    ) + sum(u.col_basis.matrices[t].size for t in u.bct.col_map)
+    coup = 0
+    for b, pair in u.coeffs.items():
+        blk = u.bct.nodes[b]
+        ls = u.row_basis.matrices[blk.row].shape[1]
+        lt = u.col_basis.matrices[blk.col].shape[1]
+        k = pair.s_x.shape[1]
+        coup += min(k * (ls + lt), ls * lt)
+    dense = sum(d.size for d in u.dense.values())
+    assert p.bytes_alg == 16 * (bases + coup + dense)
+    # the arena is the algorithmic bytes plus 128-B alignment padding only
+    assert p.bytes_arena >= p.bytes_alg
+    assert p.bytes_arena - p.bytes_alg <= 128 * (len(u.coeffs) + len(u.dense) + 4 * len(u.bct.nodes) + 8)
