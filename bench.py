@@ -34,7 +34,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--mode", default="fused", choices=["fused", "phased"])
+    ap.add_argument("--mode", default="bulk", choices=["bulk", "fused", "phased"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--adjoint", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -291,7 +291,7 @@ def main():
         "frac_vs_8000_nominal": achieved / 8000.0,
         "traffic": traffic,
         "algorithmic_bytes_per_launch": int(alg_bytes_total / world),
-        "kernel": "uhmv_fused_kernel" if args.mode == "fused" else "uhmv_phase_kernel (5 launches)",
+        "kernel": {"bulk": "bulk::uhmv_bulk_kernel", "fused": "uhmv_fused_kernel"}.get(args.mode, "uhmv_phase_kernel (5 launches)"),
     }
     if rank != 0:
         if world > 1:

@@ -22,12 +22,15 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 1
+#define UHMV_ABI_VERSION 2
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
 #define UHMV_MODE_PHASED 0 /* one launch per phase (P1+NEAR, RED, U, Z, FAR)          */
-#define UHMV_MODE_FUSED 1  /* one persistent launch, dependency counters between ops     */
+#define UHMV_MODE_FUSED 1  /* one persistent launch, register-streaming op engine         */
+#define UHMV_MODE_BULK 2   /* one persistent launch, warp-specialised bulk-copy (TMA) op
+                              engine: producer lane streams arena pieces with cp.async.bulk
+                              into an mbarrier stage ring ahead of dependency waits      */
 
 /* Error codes. */
 #define UHMV_OK 0
@@ -46,12 +49,14 @@ typedef struct uhmv_program {
     const int32_t* waits;
     const int32_t* sigs;
     const int32_t* fused_order;
+    const int64_t* pieces; /* n_pieces x 8 int64 (bulk engine) */
     int32_t n_phases;
     int32_t phase_lo[UHMV_MAX_PHASES];
     int32_t phase_hi[UHMV_MAX_PHASES];
     int32_t in_max;     /* largest gathered input vector of any op (complex elements)  */
     int32_t out_max;    /* largest output vector of any op (complex elements)          */
     int32_t n_counters; /* dependency counters used by the fused mode                  */
+    int32_t xin_max;    /* largest work-buffer input of any op (bulk engine)           */
 } uhmv_program;
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */
@@ -97,9 +102,10 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
 int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
                      void* stream);
 
-/* Launch geometry chosen for the fused mode (grid CTAs, dynamic shared memory bytes). */
-int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int* fused_grid, int* smem_bytes,
-                   int* threads_per_cta);
+/* Launch geometry chosen for a mode (grid CTAs, dynamic shared memory bytes, threads per CTA,
+ * shared-memory stages of the bulk engine). */
+int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int* smem_bytes,
+                   int* threads_per_cta, int* stages);
 
 int uhmv_plan_destroy(uhmv_plan* plan);
 

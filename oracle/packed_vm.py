@@ -18,26 +18,44 @@ from paper_2405_15573_b200.packer import (
     MODE_H,
     MODE_N,
     MODE_S,
+    PI_DIRECT,
+    PI_XGLOBAL,
     RUN_ADD,
 )
 
 __all__ = ["run_program", "vm_matvec"]
 
 
-def run_op(prog, i, bufs):
-    n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e = (int(v) for v in prog.ops[i, :8])
+def _segments(prog, i, engine):
+    """(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_global) of op i, as the register
+    kernel (``segs``) or the bulk-copy kernel (``pieces``) sees them."""
+    if engine == "segs":
+        for s in prog.segs[prog.ops[i, 4] : prog.ops[i, 5]]:
+            yield (*s, False)
+    else:
+        for m_off, ld, rows, cols, mode, in_off, out_off, info in prog.pieces[prog.ops[i, 13] : prog.ops[i, 14]]:
+            buf = BUF_WORK if info & PI_DIRECT else BUF_ARENA
+            yield (m_off, buf, rows, cols, ld, mode, in_off, out_off, bool(info & PI_XGLOBAL))
+
+
+def run_op(prog, i, bufs, engine="segs"):
+    n_in, n_out, in_b, in_e = (int(v) for v in prog.ops[i, :4])
+    out_b, out_e = (int(v) for v in prog.ops[i, 6:8])
     xin = np.zeros(n_in, dtype=np.complex128)
     for buf, off, ln, dst, _ in prog.runs[in_b:in_e]:
+        if engine == "pieces" and buf == BUF_X:
+            continue  # the bulk kernel reads x in place
         xin[dst : dst + ln] = bufs[buf][off : off + ln]
     out = np.zeros(n_out, dtype=np.complex128)
-    for m_off, buf, rows, cols, ld, mode, in_off, out_off in prog.segs[seg_b:seg_e]:
+    for m_off, buf, rows, cols, ld, mode, in_off, out_off, xg in _segments(prog, i, engine):
         src = bufs[buf]
+        vin = bufs[BUF_X] if xg else xin
         idx = m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]
         m = src[idx] if rows and cols else np.zeros((rows, cols), dtype=np.complex128)
         if mode == MODE_N:
-            out[out_off : out_off + rows] += m @ xin[in_off : in_off + cols]
+            out[out_off : out_off + rows] += m @ vin[in_off : in_off + cols]
         elif mode == MODE_H:
-            out[out_off : out_off + cols] += np.conj(m).T @ xin[in_off : in_off + rows]
+            out[out_off : out_off + cols] += np.conj(m).T @ vin[in_off : in_off + rows]
         elif mode == MODE_S:
             out[out_off : out_off + cols] += m.sum(axis=0)
         else:
@@ -49,7 +67,7 @@ def run_op(prog, i, bufs):
             bufs[buf][off : off + ln] = out[dst : dst + ln]
 
 
-def run_program(prog, arena, work, x, w, order="phased", op_range=None):
+def run_program(prog, arena, work, x, w, order="phased", op_range=None, engine="segs"):
     bufs = {BUF_ARENA: arena, BUF_WORK: work, BUF_X: x, BUF_W: w}
     if order == "fused":
         seq = prog.fused_order.tolist()
@@ -58,21 +76,21 @@ def run_program(prog, arena, work, x, w, order="phased", op_range=None):
             wb, we, sb, se = (int(v) for v in prog.ops[i, 8:12])
             for c, cnt in prog.waits[wb:we]:
                 assert done[c] >= cnt, f"op {i} waits on counter {c} ({done[c]}<{cnt}): order not topological"
-            run_op(prog, i, bufs)
+            run_op(prog, i, bufs, engine)
             for c in prog.sigs[sb:se]:
                 done[c] += 1
     else:
         lo, hi = (0, prog.n_ops) if op_range is None else op_range
         for i in range(lo, hi):
-            run_op(prog, i, bufs)
+            run_op(prog, i, bufs, engine)
 
 
-def vm_matvec(packed, v, adjoint=False, order="phased"):
+def vm_matvec(packed, v, adjoint=False, order="phased", engine="segs"):
     prog = packed.adj if adjoint else packed.fwd
     n_in, n_out = (packed.n_rows, packed.n_cols) if adjoint else (packed.n_cols, packed.n_rows)
     x = np.asarray(v, dtype=np.complex128)
     assert x.shape == (n_in,)
     w = np.full(n_out, np.nan + 1j * np.nan)  # every entry must be written
     work = np.zeros(packed.work_len, dtype=np.complex128)
-    run_program(prog, packed.arena, work, x, w, order=order)
+    run_program(prog, packed.arena, work, x, w, order=order, engine=engine)
     return w

@@ -14,8 +14,8 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "check", "LIB_PATH", "MAX_PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 1
-MODE_PHASED, MODE_FUSED = 0, 1
+ABI_VERSION = 2
+MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
 class UhmvProgram(ctypes.Structure):
@@ -27,12 +27,14 @@ class UhmvProgram(ctypes.Structure):
         ("waits", ctypes.c_void_p),
         ("sigs", ctypes.c_void_p),
         ("fused_order", ctypes.c_void_p),
+        ("pieces", ctypes.c_void_p),
         ("n_phases", ctypes.c_int32),
         ("phase_lo", ctypes.c_int32 * MAX_PHASES),
         ("phase_hi", ctypes.c_int32 * MAX_PHASES),
         ("in_max", ctypes.c_int32),
         ("out_max", ctypes.c_int32),
         ("n_counters", ctypes.c_int32),
+        ("xin_max", ctypes.c_int32),
     ]
 
 
@@ -90,7 +92,8 @@ def lib():
     L.uhmv_execute_phases.restype = i32
     L.uhmv_matvec_host.argtypes = [vp, vp, vp, i32, i32, vp]
     L.uhmv_matvec_host.restype = i32
-    L.uhmv_plan_info.argtypes = [vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    pi = ctypes.POINTER(i32)
+    L.uhmv_plan_info.argtypes = [vp, i32, i32, pi, pi, pi, pi]
     L.uhmv_plan_info.restype = i32
     L.uhmv_plan_destroy.argtypes = [vp]
     L.uhmv_plan_destroy.restype = i32

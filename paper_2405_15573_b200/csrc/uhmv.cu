@@ -33,6 +33,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -330,6 +331,12 @@ __device__ void run_op(const ExecParams& p, int op, double2* xin, double2* outv,
     __syncthreads();
 }
 
+}  // namespace
+
+#include "uhmv_bulk.cuh"
+
+namespace {
+
 struct SmemLayout {
     int xin_off, out_off, red_off, hdr_off, total;
 };
@@ -408,6 +415,9 @@ struct uhmv_plan {
     uhmv_desc d;
     int fused_grid[2];
     int smem[2];
+    int bulk_grid[2];
+    int bulk_smem[2];
+    int bulk_nstage[2];
     int sm_count;
 };
 
@@ -487,8 +497,77 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         if (grid > progs[k]->n_ops) grid = progs[k]->n_ops > 0 ? progs[k]->n_ops : 1;
         p->fused_grid[k] = grid;
     }
+    // bulk engine: as many 16-KiB stages as fit with the requested CTAs per SM
+    int smem_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, desc->device);
+    int want_ctas = 2;
+    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 2;
+    int want_stages = 0;
+    if (const char* ev = getenv("UHMV_NSTAGE")) want_stages = atoi(ev);
+    int bulk_need = 0;
+    for (int k = 0; k < 2; ++k) {
+        const uhmv_program* pr = progs[k];
+        int budget = smem_sm / want_ctas - 1024;
+        if (budget > smem_optin) budget = smem_optin;
+        const int fixed = bulk::layout(0, pr->xin_max, pr->out_max).total;
+        int ns = (budget - fixed) / bulk::kStageBytes;
+        if (want_stages > 0) ns = want_stages;
+        if (ns > 12) ns = 12;
+        if (ns < 2) ns = 2;
+        p->bulk_nstage[k] = ns;
+        p->bulk_smem[k] = bulk::layout(ns, pr->xin_max, pr->out_max).total;
+        if (p->bulk_smem[k] > bulk_need) bulk_need = p->bulk_smem[k];
+    }
+    if (bulk_need > smem_optin) {
+        delete p;
+        return fail(UHMV_EINVAL, "bulk engine shared memory exceeds the opt-in limit");
+    }
+    e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             bulk_need);
+    if (e != cudaSuccess) {
+        delete p;
+        return cuda_fail(e, "cudaFuncSetAttribute(bulk)");
+    }
+    for (int k = 0; k < 2; ++k) {
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk::uhmv_bulk_kernel,
+                                                          bulk::kThreads, p->bulk_smem[k]);
+        if (e != cudaSuccess) {
+            delete p;
+            return cuda_fail(e, "occupancy(bulk)");
+        }
+        if (per_sm < 1) per_sm = 1;
+        int grid = per_sm * p->sm_count;
+        if (grid > progs[k]->n_ops) grid = progs[k]->n_ops > 0 ? progs[k]->n_ops : 1;
+        p->bulk_grid[k] = grid;
+    }
     *out = p;
     return UHMV_OK;
+}
+
+static bulk::Params make_bulk_params(const uhmv_plan* plan, const uhmv_program& pr, int k,
+                                     const void* x, void* w) {
+    bulk::Params bp;
+    bp.arena = static_cast<const double2*>(plan->d.arena);
+    bp.work = static_cast<double2*>(plan->d.work);
+    bp.x = static_cast<const double2*>(x);
+    bp.w = static_cast<double2*>(w);
+    bp.ops = pr.ops;
+    bp.pieces = pr.pieces;
+    bp.runs = pr.runs;
+    bp.waits = pr.waits;
+    bp.sigs = pr.sigs;
+    bp.fused_order = pr.fused_order;
+    bp.op_count = pr.n_ops;
+    bp.nstage = plan->bulk_nstage[k];
+    bp.counters = plan->d.counters;
+    bp.ticket = plan->d.ticket;
+    bp.exit_count = plan->d.exit_count;
+    bp.n_counters = pr.n_counters;
+    bp.xin_max = pr.xin_max;
+    bp.out_max = pr.out_max;
+    bp.skip_waits = 0;
+    return bp;
 }
 
 static ExecParams make_params(const uhmv_plan* plan, const uhmv_program& pr, const void* x,
@@ -541,10 +620,20 @@ int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode,
     const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
     if (mode == UHMV_MODE_PHASED)
         return uhmv_execute_phases(plan, x, w, adjoint, 0, pr.n_phases, stream);
-    if (mode != UHMV_MODE_FUSED) return fail(UHMV_EINVAL, "uhmv_execute: unknown mode");
+    if (mode != UHMV_MODE_FUSED && mode != UHMV_MODE_BULK)
+        return fail(UHMV_EINVAL, "uhmv_execute: unknown mode");
     if (pr.n_ops == 0) return UHMV_OK;
     if (!x || !w) return fail(UHMV_EINVAL, "null vector pointer");
     const int k = adjoint ? 1 : 0;
+    if (mode == UHMV_MODE_BULK) {
+        if (!pr.pieces) return fail(UHMV_EINVAL, "bulk mode needs the piece table");
+        bulk::Params bp = make_bulk_params(plan, pr, k, x, w);
+        bulk::uhmv_bulk_kernel<<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k],
+                                 static_cast<cudaStream_t>(stream)>>>(bp);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "uhmv_bulk_kernel launch");
+        return UHMV_OK;
+    }
     ExecParams ep = make_params(plan, pr, x, w);
     uhmv_fused_kernel<<<plan->fused_grid[k], kThreads, plan->smem[k],
                         static_cast<cudaStream_t>(stream)>>>(ep);
@@ -575,13 +664,15 @@ int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjo
     return UHMV_OK;
 }
 
-int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int* fused_grid, int* smem_bytes,
-                   int* threads_per_cta) {
+int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int* smem_bytes,
+                   int* threads_per_cta, int* stages) {
     if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_info: null plan");
     const int k = adjoint ? 1 : 0;
-    if (fused_grid) *fused_grid = plan->fused_grid[k];
-    if (smem_bytes) *smem_bytes = plan->smem[k];
-    if (threads_per_cta) *threads_per_cta = kThreads;
+    const bool b = (mode == UHMV_MODE_BULK);
+    if (grid) *grid = b ? plan->bulk_grid[k] : plan->fused_grid[k];
+    if (smem_bytes) *smem_bytes = b ? plan->bulk_smem[k] : plan->smem[k];
+    if (threads_per_cta) *threads_per_cta = b ? bulk::kThreads : kThreads;
+    if (stages) *stages = b ? plan->bulk_nstage[k] : 0;
     return UHMV_OK;
 }
 

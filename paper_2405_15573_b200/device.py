@@ -18,11 +18,12 @@ from .packer import PackedOperator, Program
 
 __all__ = ["DeviceOperator", "default_mode"]
 
-_MODES = {"phased": _lib.MODE_PHASED, "fused": _lib.MODE_FUSED}
+_MODES = {"phased": _lib.MODE_PHASED, "fused": _lib.MODE_FUSED, "bulk": _lib.MODE_BULK}
+MODES = tuple(_MODES)
 
 
 def default_mode() -> str:
-    return os.environ.get("UHMV_MODE", "fused")
+    return os.environ.get("UHMV_MODE", "bulk")
 
 
 def _torch():
@@ -48,6 +49,7 @@ class _DeviceProgram:
         self.waits = up(prog.waits, torch.int32)
         self.sigs = up(prog.sigs, torch.int32)
         self.fused_order = up(prog.fused_order, torch.int32)
+        self.pieces = up(prog.pieces, torch.int64)
 
     def struct(self) -> _lib.UhmvProgram:
         p = self.prog
@@ -59,6 +61,7 @@ class _DeviceProgram:
         s.waits = self.waits.data_ptr()
         s.sigs = self.sigs.data_ptr()
         s.fused_order = self.fused_order.data_ptr()
+        s.pieces = self.pieces.data_ptr()
         if len(p.phases) > _lib.MAX_PHASES:
             raise ValueError("too many phases")
         s.n_phases = len(p.phases)
@@ -68,6 +71,7 @@ class _DeviceProgram:
         s.in_max = p.in_max
         s.out_max = p.out_max
         s.n_counters = p.n_counters
+        s.xin_max = p.xin_max
         return s
 
 
@@ -117,13 +121,16 @@ class DeviceOperator:
         self._lock = threading.Lock()
 
     # ---- info ----
-    def launch_info(self, adjoint=False):
-        g, s, t = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    def launch_info(self, adjoint=False, mode=None):
+        mode = mode or default_mode()
+        g, s, t, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _lib.check(
-            _lib.lib().uhmv_plan_info(self._plan, int(adjoint), ctypes.byref(g), ctypes.byref(s), ctypes.byref(t)),
+            _lib.lib().uhmv_plan_info(
+                self._plan, int(adjoint), _MODES[mode], ctypes.byref(g), ctypes.byref(s), ctypes.byref(t), ctypes.byref(n)
+            ),
             "uhmv_plan_info",
         )
-        return {"fused_grid": g.value, "smem_bytes": s.value, "threads": t.value}
+        return {"grid": g.value, "smem_bytes": s.value, "threads": t.value, "stages": n.value}
 
     def kernel_launches(self, adjoint=False, mode=None) -> int:
         """Number of our kernel launches one matvec issues."""
@@ -131,7 +138,7 @@ class DeviceOperator:
         prog = self.packed.adj if adjoint else self.packed.fwd
         if prog.n_ops == 0:
             return 0
-        return 1 if mode == "fused" else len(prog.phases)
+        return len(prog.phases) if mode == "phased" else 1
 
     # ---- execution ----
     def _stream(self, stream):

@@ -1,36 +1,41 @@
 """P0 packer: UniformHMatrix -> one aligned complex128 arena + two op programs.
 
-Replaces the dict-walking of ``matvec_uh`` (reference uniform.py:505-548) with flat,
+Replaces the dict walk of ``matvec_uh`` (reference uniform.py:505-548) with flat,
 device-resident tables.  Reads the operator duck-typed through the attributes the
 reference defines (uniform.py:90-117, clustering.py:31-209); every slab is copied,
 because fresh bases from the reference are non-contiguous views.
 
-Arena (complex128, every slab 128-byte aligned = 8 elements):
+Arena (complex128, every slab 128-byte aligned = 8 elements, every slab contiguous):
   V_t   column bases, row-major |t| x l_t            (reference layout, uniform.py:43-53)
   U_s   row bases,    row-major |s| x l_s
-  X_s   per row cluster s, row-major l_s x K_s: the coupling of every admissible block
-        b in row(s), factorized blocks first (s_x,b: l_s x k_b) then product blocks
-        (S_b = s_x s_y^H: l_s x l_t).  Per block the cheaper form is stored
-        (min(k_b (l_s+l_t), l_s l_t)).
-  Y_t   per column cluster t, row-major l_t x K'_t: s_y,b of the factorized blocks in col(t)
+  F_s   per row cluster s, row-major l_s x K_s: s_x,b of the *factorized* blocks of row(s)
+  S_b   per *product* block, row-major l_s x l_t, S_b = s_x s_y^H (uniform.py:67-68)
+  Y_t   per column cluster t, row-major l_t x K'_t: s_y,b of the factorized blocks of col(t)
   D_b   dense leaves, row-major, grouped by row leaf
+Per block the cheaper form is stored (min(k_b (l_s+l_t), l_s l_t)).
 
-Programs (one forward, one adjoint) are lists of *ops*; every op is
-  gather input runs -> smem vector xin
-  sum of GEMV segments over arena/work slabs  (N: out[r] += M[r,:] xin,
-                                               H: out[j] += sum_r conj(M[r,j]) xin[r],
-                                               S: out[j] += sum_r M[r,j])
-  scatter the smem output vector to output runs (store or add)
-and carries a wait list / signal list of dependency counters for the fused
-persistent launch.  The forward program (reference phase 1/2, uniform.py:509-548):
+Programs (one forward, one adjoint) are lists of *ops*.  Every op
+  gathers its work-buffer inputs (y / u / z vectors) into a shared-memory vector xin,
+  sums GEMV *segments* streamed from the arena
+      N: out[r] += M[r,:] . in        H: out[j] += sum_r conj(M[r,j]) in[r]
+      S: out[j] += sum_r M[r,j]       (the fixed-order reduction of partial vectors)
+  (``in`` is xin, or x itself read straight from HBM/L2 for the P1 and NEAR ops),
+  scatters its output vector (store or add), and carries wait / signal lists of
+  dependency counters for the fused persistent launch.
+Forward program (reference phase 1 / phase 2, uniform.py:509-548):
   P1   per in-leaf chunk:  partial[t] = V_t[chunk]^H x[chunk]  for all ancestors t
-  NEAR per out-leaf chunk: w[chunk]  = sum_b D_b[chunk,:] x[c_b]          (store)
-  RED  per t:              y_t = sum of partials                      (fixed order)
-  U    per t:              u_t = Y_t^H y_t   (the stage_b vectors, uniform.py:518)
-  Z    per s:              z_s = X_s [u_b | y_t]_b  (row-cluster owned, no atomics)
+  NEAR per out-leaf chunk: w[chunk]  = sum_b D_b[chunk,:] x[c_b]           (store)
+  RED  per t:              y_t = sum of its partials                    (fixed order)
+  U    per t:              u_t = Y_t^H y_t   -- the stage_b vectors of uniform.py:518
+  Z    per s:              z_s = F_s [u_b] + sum_product S_b y_t  (row-cluster owned)
   FAR  per out-leaf chunk: w[chunk] += sum_{s ancestor} U_s[chunk,:] z_s
-The adjoint program mirrors it with the roles of row/column swapped and conjugate
-transposes taken on the fly (uniform.py:498-503, :543-544) -- no slab is stored twice.
+The adjoint program mirrors it with rows/columns swapped and conjugate transposes taken
+on the fly (uniform.py:498-503, :543-544) -- no slab is stored twice.
+
+Two device encodings of the same segments are emitted:
+  ``segs``   for the register-streaming kernel (H segments split in <= 32-column panels);
+  ``pieces`` for the bulk-copy (TMA engine) kernel: each segment cut into row ranges
+             packed into shared-memory stages of STAGE_ELEMS complex128 (16 KiB).
 """
 
 from __future__ import annotations
@@ -47,17 +52,23 @@ RUN_ADD = 1
 
 OP_FIELDS = 16  # int32 per op
 # op layout: n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, wait_b, wait_e,
-#            sig_b, sig_e, kind, pad, pad, pad
+#            sig_b, sig_e, kind, pc_b, pc_e, xin_len
 SEG_FIELDS = 8  # int64: m_off, buf, rows, cols, ld, mode, in_off, out_off
 RUN_FIELDS = 5  # int64: buf, off, len, dst, flags
+PIECE_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_off, out_off, info
+# piece info bits: [0,24) smem element offset in its stage, 24 stage_begin, 25 stage_end,
+# 26 direct (no stage: coherent loads from the work buffer), 27 input read from x directly,
+# [32,56) elements of the stage (on stage_begin pieces)
+PI_BEGIN, PI_END, PI_DIRECT, PI_XGLOBAL = 1 << 24, 1 << 25, 1 << 26, 1 << 27
 
 KIND_P1, KIND_NEAR, KIND_RED, KIND_U, KIND_Z, KIND_FAR, KIND_ZERO = range(7)
 KIND_NAMES = ["P1", "NEAR", "RED", "U", "Z", "FAR", "ZERO"]
 
 ALIGN = 8  # complex128 elements per 128 B
-HCOLS_MAX = 32  # widest H/S segment (= csrc kHColsMax: 4 accumulators x 8 lanes)
-ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op (= row-groups per CTA)
+HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
+ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op
 P1_CHUNK = 256  # max input rows per P1 op
+STAGE_ELEMS = 1024  # complex128 per shared-memory stage (16 KiB) of the bulk-copy kernel
 
 
 def _align(n: int) -> int:
@@ -69,13 +80,15 @@ class Program:
     """Host copy of one op program (int arrays ready for upload)."""
 
     ops: np.ndarray  # (n_ops, OP_FIELDS) int32
-    segs: np.ndarray  # (n_segs, SEG_FIELDS) int64
+    segs: np.ndarray  # (n_segs, SEG_FIELDS) int64  (register kernel)
+    pieces: np.ndarray  # (n_pieces, PIECE_FIELDS) int64  (bulk-copy kernel)
     runs: np.ndarray  # (n_runs, RUN_FIELDS) int64
     waits: np.ndarray  # (n_waits, 2) int32: counter id, arrivals per matvec
     sigs: np.ndarray  # (n_sigs,) int32 counter ids
     phases: list  # [(op_begin, op_end)] for the phased (multi-launch) mode
     fused_order: np.ndarray  # (n_ops,) int32: op index claimed by ticket i in the fused launch
-    in_max: int
+    in_max: int  # largest gathered input (register kernel: all inputs staged)
+    xin_max: int  # largest work-buffer input (bulk kernel: x is read in place)
     out_max: int
     n_counters: int
     kinds: np.ndarray  # (n_ops,) op kind
@@ -102,36 +115,32 @@ class PackedOperator:
 
 
 def _leaves_under(tree):
-    """For every node id: (first leaf position, one-past-last) into the DFS leaf list."""
+    """DFS leaf list and, for every node id, its (first, one-past-last) leaf position."""
     nodes = tree.nodes
     leaves = []
     span = [None] * len(nodes)
-
-    def walk(i):
+    stack = [(getattr(tree, "root", 0), False)]
+    first = {}
+    while stack:
+        i, done = stack.pop()
         n = nodes[i]
-        first = len(leaves)
+        if done:
+            span[i] = (first[i], len(leaves))
+            continue
+        first[i] = len(leaves)
         if not n.children:
             leaves.append(i)
-        else:
-            for c in n.children:
-                walk(c)
-        span[i] = (first, len(leaves))
-
-    import sys
-
-    old = sys.getrecursionlimit()
-    sys.setrecursionlimit(max(old, 10000))
-    try:
-        walk(getattr(tree, "root", 0))
-    finally:
-        sys.setrecursionlimit(old)
+            span[i] = (first[i], len(leaves))
+            continue
+        stack.append((i, True))
+        for c in reversed(n.children):
+            stack.append((c, False))
     return leaves, span
 
 
 def _ancestors_in(tree, leaves, span, cset):
     """For every leaf position: the clusters of ``cset`` that contain it (root to leaf)."""
     anc = [[] for _ in leaves]
-    # order clusters by level so each list is root -> leaf
     for cid in sorted(cset, key=lambda c: tree.nodes[c].level):
         a, b = span[cid]
         for p in range(a, b):
@@ -155,37 +164,29 @@ def _chunks(lo, hi, step):
     return out
 
 
-def _hpanels(cols):
-    return _chunks(0, cols, HCOLS_MAX)
-
-
 def pack(u, *, rows_per_chunk: int = ROWS_PER_CHUNK, near_interleave=(0.4, 0.3, 0.3)) -> PackedOperator:
     """Pack a UniformHMatrix (reference object or mirror) into arena + programs."""
     bct = u.bct
-    rtree, ctree = bct.row_tree, bct.col_tree
     n_rows, n_cols = bct.shape
-    rnodes, cnodes = rtree.nodes, ctree.nodes
+    rnodes, cnodes = bct.row_tree.nodes, bct.col_tree.nodes
 
     # ---- which blocks / clusters take part (exactly what the reference walks) ----
-    adm = []  # (bid, s, t) in row_map order per s
+    adm = []
     for s in bct.row_map:
         for t in bct.row_map[s]:
             adm.append((bct.block_of[(s, t)], s, t))
     rank_r = {s: int(u.row_basis.matrices[s].shape[1]) for s in bct.row_map}
     rank_c = {t: int(u.col_basis.matrices[t].shape[1]) for t in bct.col_map}
-    kb = {}
-    factorized = {}
+    kb, factorized = {}, {}
     bytes_coupling = 0
     for bid, s, t in adm:
-        pair = u.coeffs[bid]
-        k = int(pair.s_x.shape[1])
+        k = int(u.coeffs[bid].s_x.shape[1])
         kb[bid] = k
         ls, lt = rank_r[s], rank_c[t]
-        fac = k * (ls + lt) < ls * lt
-        factorized[bid] = fac
+        factorized[bid] = k * (ls + lt) < ls * lt
         bytes_coupling += min(k * (ls + lt), ls * lt)
-
     dense_ids = list(u.dense.keys())
+
     # ---- arena layout ----
     offs = {}
     cursor = 0
@@ -199,28 +200,23 @@ def pack(u, *, rows_per_chunk: int = ROWS_PER_CHUNK, near_interleave=(0.4, 0.3, 
         alloc(("V", t), cnodes[t].size * rank_c[t])
     for s in sorted(bct.row_map):
         alloc(("U", s), rnodes[s].size * rank_r[s])
-    # X_s columns: factorized blocks first, then product blocks (row_map order within)
-    xcols = {}
+    fcols = {}  # s -> ([(bid, t, pos, k)], kfac)
     for s in sorted(bct.row_map):
-        pos = 0
-        cols = []
+        pos, cols = 0, []
         for t in bct.row_map[s]:
             bid = bct.block_of[(s, t)]
             if factorized[bid]:
-                cols.append((bid, t, pos, kb[bid], True))
+                cols.append((bid, t, pos, kb[bid]))
                 pos += kb[bid]
-        kfac = pos
+        fcols[s] = (cols, pos)
+        alloc(("F", s), rank_r[s] * pos)
         for t in bct.row_map[s]:
             bid = bct.block_of[(s, t)]
             if not factorized[bid]:
-                cols.append((bid, t, pos, rank_c[t], False))
-                pos += rank_c[t]
-        xcols[s] = (cols, kfac, pos)
-        alloc(("X", s), rank_r[s] * pos)
-    ycols = {}
+                alloc(("S", bid), rank_r[s] * rank_c[t])
+    ycols = {}  # t -> ([(bid, s, pos, k)], K')
     for t in sorted(bct.col_map):
-        pos = 0
-        cols = []
+        pos, cols = 0, []
         for s in bct.col_map[t]:
             bid = bct.block_of[(s, t)]
             if factorized[bid]:
@@ -228,9 +224,7 @@ def pack(u, *, rows_per_chunk: int = ROWS_PER_CHUNK, near_interleave=(0.4, 0.3, 
                 pos += kb[bid]
         ycols[t] = (cols, pos)
         alloc(("Y", t), rank_c[t] * pos)
-    # dense grouped by row leaf (for the forward NEAR ops), column order within
-    dense_by_rleaf = {}
-    dense_by_cleaf = {}
+    dense_by_rleaf, dense_by_cleaf = {}, {}
     for bid in dense_ids:
         b = bct.nodes[bid]
         dense_by_rleaf.setdefault(b.row, []).append(bid)
@@ -255,23 +249,24 @@ def pack(u, *, rows_per_chunk: int = ROWS_PER_CHUNK, near_interleave=(0.4, 0.3, 
         put(("V", t), u.col_basis.matrices[t])
     for s in bct.row_map:
         put(("U", s), u.row_basis.matrices[s])
-    for s, (cols, kfac, ktot) in xcols.items():
+    for s, (cols, kfac) in fcols.items():
         ls = rank_r[s]
-        if ls == 0 or ktot == 0:
-            continue
-        xs = np.empty((ls, ktot), dtype=np.complex128)
-        for bid, t, pos, w, fac in cols:
+        if ls and kfac:
+            fs = np.empty((ls, kfac), dtype=np.complex128)
+            for bid, t, pos, k in cols:
+                fs[:, pos : pos + k] = u.coeffs[bid].s_x
+            put(("F", s), fs)
+    for bid, s, t in adm:
+        if not factorized[bid]:
             pair = u.coeffs[bid]
-            xs[:, pos : pos + w] = pair.s_x if fac else pair.s_x @ np.conj(pair.s_y).T
-        put(("X", s), xs)
+            put(("S", bid), pair.s_x @ np.conj(pair.s_y).T)
     for t, (cols, ktot) in ycols.items():
         lt = rank_c[t]
-        if lt == 0 or ktot == 0:
-            continue
-        ys = np.empty((lt, ktot), dtype=np.complex128)
-        for bid, s, pos, w in cols:
-            ys[:, pos : pos + w] = u.coeffs[bid].s_y
-        put(("Y", t), ys)
+        if lt and ktot:
+            ys = np.empty((lt, ktot), dtype=np.complex128)
+            for bid, s, pos, k in cols:
+                ys[:, pos : pos + k] = u.coeffs[bid].s_y
+            put(("Y", t), ys)
     bytes_dense = 0
     for bid in dense_ids:
         d = u.dense[bid]
@@ -282,9 +277,8 @@ def pack(u, *, rows_per_chunk: int = ROWS_PER_CHUNK, near_interleave=(0.4, 0.3, 
         rnodes[s].size * rank_r[s] for s in bct.row_map
     )
     geo = dict(
-        bct=bct, rnodes=rnodes, cnodes=cnodes, rank_r=rank_r, rank_c=rank_c, kb=kb,
-        factorized=factorized, xcols=xcols, ycols=ycols, offs=offs,
-        dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
+        bct=bct, rank_r=rank_r, rank_c=rank_c, kb=kb, factorized=factorized,
+        fcols=fcols, ycols=ycols, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
     )
     fwd, work_f = _build_program(geo, adjoint=False, rows_per_chunk=rows_per_chunk, near_interleave=near_interleave)
     adj, work_a = _build_program(geo, adjoint=True, rows_per_chunk=rows_per_chunk, near_interleave=near_interleave)
@@ -311,10 +305,16 @@ def pack(u, *, rows_per_chunk: int = ROWS_PER_CHUNK, near_interleave=(0.4, 0.3, 
     )
 
 
+def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
+    """Logical segment; ``x_off`` >= 0 means the input vector is x[x_off : ...] (read in place
+    by the bulk kernel, staged into xin at ``in_off`` by the register kernel)."""
+    return (int(m_off), int(buf), int(rows), int(cols), int(ld), int(mode), int(in_off), int(out_off), int(x_off))
+
+
 def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     bct = geo["bct"]
     offs = geo["offs"]
-    xcols, ycols = geo["xcols"], geo["ycols"]
+    fcols, ycols = geo["fcols"], geo["ycols"]
     factorized = geo["factorized"]
     if adjoint:
         in_tree, out_tree = bct.row_tree, bct.col_tree
@@ -344,15 +344,13 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     in_anc = _ancestors_in(in_tree, in_leaves, in_span, [t for t in in_map if in_rank[t] > 0])
     out_anc = _ancestors_in(out_tree, out_leaves, out_span, [s for s in out_map if out_rank[s] > 0])
 
-    # P1 chunks: every in-leaf split in <= P1_CHUNK rows
-    p1_items = []  # (leafpos, lo, hi)
+    p1_items = []  # (leafpos, lo, hi): every in-leaf split in <= P1_CHUNK rows
     for p, leaf in enumerate(in_leaves):
         if not in_anc[p]:
             continue
         n = in_nodes[leaf]
         for a, b in _chunks(n.lo, n.hi, P1_CHUNK):
             p1_items.append((p, a, b))
-    # partial slots per in-cluster t: one per P1 chunk under t
     chunks_of = {t: [] for t in in_map}
     for idx, (p, a, b) in enumerate(p1_items):
         for t in in_anc[p]:
@@ -361,33 +359,23 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
         y_off[t] = walloc(in_rank[t])
     for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
-        nchunk = len(chunks_of[t])
-        if in_rank[t] == 0:
-            continue
-        part_off[t] = y_off[t] if nchunk == 1 else walloc(nchunk * in_rank[t])
-    # staging vectors u: forward per column cluster t (Y_t columns), adjoint per row cluster s
-    # (factorized columns [0, kfac) of X_s)
+        if in_rank[t]:
+            part_off[t] = y_off[t] if len(chunks_of[t]) == 1 else walloc(len(chunks_of[t]) * in_rank[t])
+    # staging vectors u: forward per column cluster t (columns of Y_t), adjoint per row
+    # cluster s (columns of F_s)
     u_off, u_len = {}, {}
     for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
-        n = ycols[t][1] if not adjoint else xcols[t][1]
-        u_len[t] = n
-        u_off[t] = walloc(n)
+        u_len[t] = ycols[t][1] if not adjoint else fcols[t][1]
+        u_off[t] = walloc(u_len[t])
     z_off = {}
     for s in sorted(out_map, key=lambda s: out_nodes[s].lo):
         z_off[s] = walloc(out_rank[s])
-
-    # position of block b's staging vector inside u of its in-cluster
     u_pos = {}
     for t in in_map:
-        if not adjoint:
-            for bid, s, pos, w in ycols[t][0]:
-                u_pos[bid] = pos
-        else:
-            for bid, tt, pos, w, fac in xcols[t][0]:
-                if fac:
-                    u_pos[bid] = pos
+        for entry in (ycols[t][0] if not adjoint else fcols[t][0]):
+            u_pos[entry[0]] = entry[2]
 
-    # ---- counters ----
+    # ---- dependency counters ----
     n_ctr = 0
 
     def ctr():
@@ -399,37 +387,27 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     c_y = {t: ctr() for t in in_map}
     c_u = {t: ctr() for t in in_map}
     c_z = {s: ctr() for s in out_map}
+    ops = {k: [] for k in range(7)}
 
-    phase_ops = {k: [] for k in range(7)}
-
-    # P1: partial_t = B_in,t[chunk rows]^H x[chunk]
+    # P1: partial_t = B_t[chunk rows]^H x[chunk]
     for idx, (p, a, b) in enumerate(p1_items):
         segs, outs, sigs = [], [], []
         oo = 0
         for t in in_anc[p]:
             lt = in_rank[t]
-            tl = in_nodes[t].lo
-            for c0, c1 in _hpanels(lt):
-                segs.append((offs[(in_basis_key, t)] + (a - tl) * lt + c0, BUF_ARENA, b - a, c1 - c0, lt, MODE_H, 0, oo + c0))
-            slot = chunks_of[t].index(idx)
-            outs.append((BUF_WORK, part_off[t] + slot * lt, lt, oo, 0))
+            segs.append(_seg(offs[(in_basis_key, t)] + (a - in_nodes[t].lo) * lt, BUF_ARENA, b - a, lt, lt, MODE_H, 0, oo, a))
+            outs.append((BUF_WORK, part_off[t] + chunks_of[t].index(idx) * lt, lt, oo, 0))
             sigs.append(c_part[t])
             oo += lt
-        phase_ops[KIND_P1].append(
-            (KIND_P1, b - a, oo, [(BUF_X, a, b - a, 0, 0)], segs, outs, [], sigs, (b - a) * oo)
-        )
-    # RED: y_t = sum over chunk partials (skipped when the single partial is y_t itself)
+        ops[KIND_P1].append((KIND_P1, b - a, oo, [(BUF_X, a, b - a, 0, 0)], segs, outs, [], sigs, (b - a) * oo))
+    # RED: y_t = sum of chunk partials (skipped when the single partial is y_t itself)
     for t in in_map:
-        lt = in_rank[t]
-        nchunk = len(chunks_of[t])
-        if lt == 0:
+        lt, nchunk = in_rank[t], len(chunks_of[t])
+        if lt == 0 or nchunk <= 1:
             continue
-        waits = [(c_part[t], nchunk)]
-        if nchunk <= 1:
-            continue
-        segs = [(part_off[t] + c0, BUF_WORK, nchunk, c1 - c0, lt, MODE_S, 0, c0) for c0, c1 in _hpanels(lt)]
-        phase_ops[KIND_RED].append(
-            (KIND_RED, 0, lt, [], segs, [(BUF_WORK, y_off[t], lt, 0, 0)], waits, [c_y[t]], nchunk * lt)
+        segs = [_seg(part_off[t], BUF_WORK, nchunk, lt, lt, MODE_S, 0, 0)]
+        ops[KIND_RED].append(
+            (KIND_RED, 0, lt, [], segs, [(BUF_WORK, y_off[t], lt, 0, 0)], [(c_part[t], nchunk)], [c_y[t]], nchunk * lt)
         )
     y_wait = {}
     for t in in_map:
@@ -439,142 +417,129 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
             y_wait[t] = [(c_part[t], len(chunks_of[t]))]
         else:
             y_wait[t] = [(c_y[t], 1)]
-    # U: staging vectors of the factorized blocks, u_t = C_t^H y_t.  When l_t = 0 the
-    # staging vectors are exact zeros (reference: (k x 0) @ (0,)), which the zero-initialised,
-    # never-written work region already holds -- no op, no wait.
+    # U: staging vectors of the factorized blocks.  l_t = 0 gives exact zeros (reference:
+    # (k x 0) @ (0,)), which the zero-initialised, never-written work region already holds.
     u_wait = {}
     for t in in_map:
-        n = u_len[t]
-        lt = in_rank[t]
+        n, lt = u_len[t], in_rank[t]
         u_wait[t] = []
         if n == 0 or lt == 0:
             continue
         u_wait[t] = [(c_u[t], 1)]
-        if not adjoint:
-            base, ld = offs[("Y", t)], ycols[t][1]
-        else:
-            base, ld = offs[("X", t)], xcols[t][2]
-        segs = [(base + c0, BUF_ARENA, lt, c1 - c0, ld, MODE_H, 0, c0) for c0, c1 in _hpanels(n)]
-        phase_ops[KIND_U].append(
+        base = offs[("Y", t)] if not adjoint else offs[("F", t)]
+        segs = [_seg(base, BUF_ARENA, lt, n, n, MODE_H, 0, 0)]
+        ops[KIND_U].append(
             (KIND_U, lt, n, [(BUF_WORK, y_off[t], lt, 0, 0)], segs, [(BUF_WORK, u_off[t], n, 0, 0)],
              list(y_wait[t]), [c_u[t]], lt * n)
         )
-    # Z: row-cluster (forward) / column-cluster (adjoint) owned coupling
+    # Z: coupling, owned by the output cluster (row cluster forward, column cluster adjoint)
     for s in out_map:
         ls = out_rank[s]
         if ls == 0:
             continue
         in_runs, segs, waits = [], [], []
         if not adjoint:
-            cols, kfac, ktot = xcols[s]
-            # gathered input in X_s column order: u_b for factorized, y_t for product blocks
-            for bid, t, pos, w, fac in cols:
-                if w == 0:
-                    continue
-                if fac:
-                    in_runs.append((BUF_WORK, u_off[t] + u_pos[bid], w, pos, 0))
+            cols, kfac = fcols[s]
+            for bid, t, pos, k in cols:  # F_s [u_b ...]
+                if k:
+                    in_runs.append((BUF_WORK, u_off[t] + u_pos[bid], k, pos, 0))
                     waits.extend(u_wait[t])
-                else:
-                    in_runs.append((BUF_WORK, y_off[t], w, pos, 0))
-                    waits.extend(y_wait[t])
-            if ktot:
-                segs.append((offs[("X", s)], BUF_ARENA, ls, ktot, ktot, MODE_N, 0, 0))
-            n_in = ktot
-            nbytes = ls * ktot
+            if kfac:
+                segs.append(_seg(offs[("F", s)], BUF_ARENA, ls, kfac, kfac, MODE_N, 0, 0))
+            n_in = kfac
+            nbytes = ls * kfac
+            for t in out_map[s]:  # + S_b y_t for product blocks
+                bid = bct.block_of[(s, t)]
+                lt = in_rank[t]
+                if factorized[bid] or lt == 0:
+                    continue
+                in_runs.append((BUF_WORK, y_off[t], lt, n_in, 0))
+                waits.extend(y_wait[t])
+                segs.append(_seg(offs[("S", bid)], BUF_ARENA, ls, lt, lt, MODE_N, n_in, 0))
+                n_in += lt
+                nbytes += ls * lt
         else:
-            # adjoint: z_t = Y_t [u'_b] (N) + sum_{product b} S_b^H y'_s (H)
             cols, ktot = ycols[s]
-            for bid, r, pos, w in cols:
-                if w == 0:
-                    continue
-                in_runs.append((BUF_WORK, u_off[r] + u_pos[bid], w, pos, 0))
-                waits.extend(u_wait[r])
+            for bid, r, pos, k in cols:  # Y_t [u'_b ...]
+                if k:
+                    in_runs.append((BUF_WORK, u_off[r] + u_pos[bid], k, pos, 0))
+                    waits.extend(u_wait[r])
             if ktot:
-                segs.append((offs[("Y", s)], BUF_ARENA, ls, ktot, ktot, MODE_N, 0, 0))
+                segs.append(_seg(offs[("Y", s)], BUF_ARENA, ls, ktot, ktot, MODE_N, 0, 0))
             n_in = ktot
             nbytes = ls * ktot
-            for r in out_map[s]:
+            for r in out_map[s]:  # + S_b^H y'_r for product blocks
                 bid = bct.block_of[(r, s)]
-                if factorized[bid]:
-                    continue
                 lr = in_rank[r]
-                if lr == 0:
+                if factorized[bid] or lr == 0:
                     continue
-                xc, kfac, kx = xcols[r]
-                pos = next(p for (b2, tt, p, w, fac) in xc if b2 == bid)
                 in_runs.append((BUF_WORK, y_off[r], lr, n_in, 0))
                 waits.extend(y_wait[r])
-                for c0, c1 in _hpanels(ls):
-                    segs.append((offs[("X", r)] + pos + c0, BUF_ARENA, lr, c1 - c0, kx, MODE_H, n_in, c0))
+                segs.append(_seg(offs[("S", bid)], BUF_ARENA, lr, ls, ls, MODE_H, n_in, 0))
                 n_in += lr
                 nbytes += lr * ls
-        waits = sorted(set(waits))
-        phase_ops[KIND_Z].append(
-            (KIND_Z, n_in, ls, in_runs, segs, [(BUF_WORK, z_off[s], ls, 0, 0)], waits, [c_z[s]], nbytes)
+        ops[KIND_Z].append(
+            (KIND_Z, n_in, ls, in_runs, segs, [(BUF_WORK, z_off[s], ls, 0, 0)], sorted(set(waits)), [c_z[s]], nbytes)
         )
 
-    # NEAR + FAR per output leaf chunk
-    near_ctr = {}
-    far_list = []
+    # NEAR + FAR per output-leaf chunk
+    near_ctr = {}  # leaf -> [(a, b, counter)]
     for p, leaf in enumerate(out_leaves):
         n = out_nodes[leaf]
         dlist = dense_by_outleaf.get(leaf, [])
+        # forward: row chunks of the leaf; adjoint: the whole column leaf (H segments reduce
+        # over the block rows, so the op owns all |c| output entries of the leaf)
+        near_chunks = _chunks(n.lo, n.hi, rows_per_chunk) if not adjoint else [(n.lo, n.hi)]
+        for a, b in near_chunks:
+            if not dlist:
+                continue
+            rows = b - a
+            in_runs, segs = [], []
+            pos = 0
+            nbytes = 0
+            for bid in dlist:
+                blk = bct.nodes[bid]
+                if not adjoint:
+                    c = bct.col_tree.nodes[blk.col]
+                    in_runs.append((BUF_X, c.lo, c.size, pos, 0))
+                    segs.append(_seg(offs[("D", bid)] + (a - n.lo) * c.size, BUF_ARENA, rows, c.size, c.size, MODE_N, pos, 0, c.lo))
+                    pos += c.size
+                    nbytes += rows * c.size
+                else:
+                    r = bct.row_tree.nodes[blk.row]
+                    in_runs.append((BUF_X, r.lo, r.size, pos, 0))
+                    segs.append(_seg(offs[("D", bid)], BUF_ARENA, r.size, n.size, n.size, MODE_H, pos, 0, r.lo))
+                    pos += r.size
+                    nbytes += r.size * n.size
+            cid = ctr()
+            near_ctr.setdefault(leaf, []).append((a, b, cid))
+            ops[KIND_NEAR].append((KIND_NEAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, 0)], [], [cid], nbytes))
         for a, b in _chunks(n.lo, n.hi, rows_per_chunk):
             rows = b - a
-            has_near = False
-            if dlist:
-                in_runs, segs = [], []
-                pos = 0
-                nbytes = 0
-                for bid in dlist:
-                    blk = bct.nodes[bid]
-                    if not adjoint:
-                        c = bct.col_tree.nodes[blk.col]
-                        width = c.size
-                        in_runs.append((BUF_X, c.lo, width, pos, 0))
-                        segs.append((offs[("D", bid)] + (a - n.lo) * width, BUF_ARENA, rows, width, width, MODE_N, pos, 0))
-                        pos += width
-                        nbytes += rows * width
-                    else:
-                        r = bct.row_tree.nodes[blk.row]
-                        width = n.size  # dense block is |r| x |c|, c = this out-leaf
-                        in_runs.append((BUF_X, r.lo, r.size, pos, 0))
-                        for c0, c1 in _hpanels(rows):
-                            segs.append((offs[("D", bid)] + (a - n.lo) + c0, BUF_ARENA, r.size, c1 - c0, width, MODE_H, pos, c0))
-                        pos += r.size
-                        nbytes += rows * r.size
-                cid = ctr()
-                near_ctr[(a, b)] = cid
-                phase_ops[KIND_NEAR].append(
-                    (KIND_NEAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, 0)], [], [cid], nbytes)
-                )
-                has_near = True
+            near_key = next((c for (na, nb, c) in near_ctr.get(leaf, []) if na <= a and b <= nb), None)
             anc = out_anc[p]
             if anc:
                 in_runs, segs, waits = [], [], []
                 pos = 0
                 for s in anc:
                     ls = out_rank[s]
-                    sl = out_nodes[s].lo
                     in_runs.append((BUF_WORK, z_off[s], ls, pos, 0))
-                    segs.append((offs[(out_basis_key, s)] + (a - sl) * ls, BUF_ARENA, rows, ls, ls, MODE_N, pos, 0))
+                    segs.append(_seg(offs[(out_basis_key, s)] + (a - out_nodes[s].lo) * ls, BUF_ARENA, rows, ls, ls, MODE_N, pos, 0))
                     waits.append((c_z[s], 1))
                     pos += ls
-                if has_near:
-                    waits.append((near_ctr[(a, b)], 1))
-                far_list.append(
-                    (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ADD if has_near else 0)],
+                if near_key is not None:
+                    waits.append((near_key, 1))
+                ops[KIND_FAR].append(
+                    (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ADD if near_key is not None else 0)],
                      waits, [], rows * pos)
                 )
-            elif not has_near:
-                phase_ops[KIND_ZERO].append((KIND_ZERO, 0, rows, [], [], [(BUF_W, a, rows, 0, 0)], [], [], 0))
-    phase_ops[KIND_FAR] = far_list
+            elif near_key is None:
+                ops[KIND_ZERO].append((KIND_ZERO, 0, rows, [], [], [(BUF_W, a, rows, 0, 0)], [], [], 0))
 
-    # ---- order: largest first inside each phase (reference uniform.py:505-506) ----
-    for k in phase_ops:
-        phase_ops[k].sort(key=lambda o: -o[-1])
-
-    near = phase_ops[KIND_NEAR]
+    # ---- order: largest first inside each kind (reference uniform.py:505-506) ----
+    for k in ops:
+        ops[k].sort(key=lambda o: -o[-1])
+    near = ops[KIND_NEAR]
     f = np.cumsum([0.0] + list(near_interleave))
     f = f / f[-1]
     cut = [int(round(x * len(near))) for x in f]
@@ -582,21 +547,79 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     while len(near_parts) < 3:
         near_parts.append([])
     # phased launches (multi-launch mode): [P1 + NEAR + ZERO] [RED] [U] [Z] [FAR]
-    phased = [phase_ops[KIND_P1] + near + phase_ops[KIND_ZERO]]
-    phased += [phase_ops[k] for k in (KIND_RED, KIND_U, KIND_Z, KIND_FAR)]
+    phased = [ops[KIND_P1] + near + ops[KIND_ZERO]]
+    phased += [ops[k] for k in (KIND_RED, KIND_U, KIND_Z, KIND_FAR)]
     # fused persistent order: every op waits only on ops that come earlier
     fused = (
-        phase_ops[KIND_P1]
-        + near_parts[0]
-        + phase_ops[KIND_RED]
-        + phase_ops[KIND_U]
-        + near_parts[1]
-        + phase_ops[KIND_Z]
-        + near_parts[2]
-        + phase_ops[KIND_ZERO]
-        + phase_ops[KIND_FAR]
+        ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + ops[KIND_U] + near_parts[1]
+        + ops[KIND_Z] + near_parts[2] + ops[KIND_ZERO] + ops[KIND_FAR]
     )
     return _finish(phased, fused, n_ctr), work
+
+
+def _panel_split(s):
+    """Register-kernel form of a logical segment: H/S split in <= HCOLS_MAX columns."""
+    m_off, buf, rows, cols, ld, mode, in_off, out_off, _x = s
+    if mode == MODE_N or cols <= HCOLS_MAX:
+        return [(m_off, buf, rows, cols, ld, mode, in_off, out_off)]
+    return [(m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0) for c0, c1 in _chunks(0, cols, HCOLS_MAX)]
+
+
+def _order_segments(segs):
+    """N segments first (grouped by out_off/rows), then H/S groups (by out_off/cols).
+
+    Both kernels rely on it: N rows are owner-updated without a barrier, and one barrier
+    at the N -> H switch orders them before the H owners touch the same outputs."""
+    n = [s for s in segs if s[5] == MODE_N]
+    h = [s for s in segs if s[5] != MODE_N]
+    n.sort(key=lambda s: (s[7], s[2]))
+    h.sort(key=lambda s: (s[5], s[7], s[3]))
+    return n + h
+
+
+def _pieces(segs, has_x):
+    """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages."""
+    out = []
+    fill = 0  # elements used in the open stage
+    open_idx = None  # index in ``out`` of the open stage's first piece
+
+    def close():
+        nonlocal fill, open_idx
+        if open_idx is not None:
+            out[-1][7] |= PI_END
+            out[open_idx][7] |= fill << 32
+        fill = 0
+        open_idx = None
+
+    for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in segs:
+        xin = x_off if (x_off >= 0 and has_x) else in_off
+        xflag = PI_XGLOBAL if (x_off >= 0 and has_x) else 0
+        if buf == BUF_WORK:  # coherent in-kernel data: no bulk copy, no stage
+            out.append([m_off, ld, rows, cols, mode, xin, out_off, PI_DIRECT | xflag])
+            continue
+        if cols > STAGE_ELEMS:
+            raise ValueError(f"segment row of {cols} elements exceeds a {STAGE_ELEMS}-element stage")
+        r = 0
+        while r < rows:
+            room = (STAGE_ELEMS - fill) // cols
+            if room == 0:
+                close()
+                room = STAGE_ELEMS // cols
+            n = min(room, rows - r)
+            info = fill | xflag
+            if open_idx is None:
+                info |= PI_BEGIN
+                open_idx = len(out)
+            out.append([
+                m_off + r * ld, ld, n, cols, mode,
+                xin + (r if mode != MODE_N else 0),
+                out_off + (r if mode == MODE_N else 0),
+                info,
+            ])
+            fill += n * cols
+            r += n
+    close()
+    return out
 
 
 def _finish(phased, fused, n_ctr):
@@ -615,50 +638,49 @@ def _finish(phased, fused, n_ctr):
 
     n = len(order)
     ops = np.zeros((n, OP_FIELDS), dtype=np.int32)
-    segs, runs, waits, sigs = [], [], [], []
-    in_max = out_max = 0
+    segs, pieces, runs, waits, sigs = [], [], [], [], []
+    in_max = xin_max = out_max = 0
     for i, (kind, n_in, n_out, in_runs, sg, out_runs, wt, sgn, _) in enumerate(order):
+        has_x = any(r[0] == BUF_X for r in in_runs)
+        has_w = any(r[0] == BUF_WORK for r in in_runs)
+        assert not (has_x and has_w), "an op reads x or work inputs, never both"
         in_b = len(runs)
         runs.extend(in_runs)
         in_e = len(runs)
         out_b = len(runs)
         runs.extend(out_runs)
         out_e = len(runs)
+        ordered = _order_segments(sg)
         seg_b = len(segs)
-        segs.extend(_order_segments(sg))
+        for s in ordered:
+            segs.extend(_panel_split(s))
         seg_e = len(segs)
+        pc_b = len(pieces)
+        pieces.extend(_pieces(ordered, has_x))
+        pc_e = len(pieces)
         w_b = len(waits)
         waits.extend(wt)
         w_e = len(waits)
         s_b = len(sigs)
         sigs.extend(sgn)
         s_e = len(sigs)
-        ops[i, :13] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind)
+        xin_len = 0 if has_x else n_in
+        ops[i] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind, pc_b, pc_e, xin_len)
         in_max = max(in_max, n_in)
+        xin_max = max(xin_max, xin_len)
         out_max = max(out_max, n_out)
     return Program(
         ops=ops,
         segs=np.asarray(segs, dtype=np.int64).reshape(-1, SEG_FIELDS),
+        pieces=np.asarray(pieces, dtype=np.int64).reshape(-1, PIECE_FIELDS),
         runs=np.asarray(runs, dtype=np.int64).reshape(-1, RUN_FIELDS),
         waits=np.asarray(waits, dtype=np.int32).reshape(-1, 2),
         sigs=np.asarray(sigs, dtype=np.int32).reshape(-1),
         phases=bounds,
         fused_order=fused_order,
         in_max=in_max,
+        xin_max=xin_max,
         out_max=out_max,
         n_counters=n_ctr,
         kinds=ops[:, 12].copy(),
     )
-
-
-def _order_segments(segs):
-    """N segments first (grouped by out_off/rows), then H/S groups (by out_off/cols).
-
-    The device kernel accumulates consecutive segments that share (mode, out_off,
-    rows|cols) in registers and reduces once per group; N before H/S lets N rows be
-    owner-updated without a barrier (see csrc/uhmv_kernels.cu)."""
-    n = [s for s in segs if s[5] == MODE_N]
-    h = [s for s in segs if s[5] != MODE_N]
-    n.sort(key=lambda s: (s[7], s[2]))
-    h.sort(key=lambda s: (s[5], s[7], s[3]))
-    return n + h

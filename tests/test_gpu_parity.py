@@ -31,7 +31,7 @@ def _dev(u):
     return DeviceOperator(pack(u), device="cuda:0")
 
 
-@pytest.mark.parametrize("mode", ["phased", "fused"])
+@pytest.mark.parametrize("mode", ["phased", "fused", "bulk"])
 def test_device_matches_reference(golden, mode):
     name, u, ex = golden
     for vname, view, pfx in views():
@@ -55,6 +55,10 @@ def test_modes_bit_identical(golden):
     b = dop.matvec(x, mode="fused").cpu().numpy()
     c = dop.matvec(x, mode="fused").cpu().numpy()
     assert np.array_equal(a, b) and np.array_equal(b, c)
+    d = dop.matvec(x, mode="bulk").cpu().numpy()
+    e = dop.matvec(x, mode="bulk").cpu().numpy()
+    assert np.array_equal(d, e)  # the bulk engine sums in its own (fixed) order
+    assert np.linalg.norm(d - a) <= 1e-13 * np.linalg.norm(a)
 
 
 def test_dropin_matvec_uh(golden):
@@ -116,20 +120,21 @@ def test_host_abi_entry():
     """uhmv_matvec_host: host buffers in/out through the C ABI."""
     u, ex = load_golden("ico2_helm_compress")
     dop = _dev(u)
-    for mode in ("phased", "fused"):
+    for mode in ("phased", "fused", "bulk"):
         w = dop.matvec_host(ex["vf_0"], mode=mode)
         assert rel(w, ex["ref_fwd_0"]) <= TOL
         wa = dop.matvec_host(ex["va_0"], adjoint=True, mode=mode)
         assert rel(wa, ex["ref_adj_0"]) <= TOL
 
 
-def test_repeated_fused_launches_self_reset():
+@pytest.mark.parametrize("mode", ["fused", "bulk"])
+def test_repeated_fused_launches_self_reset(mode):
     u, ex = load_golden("ico2_helm_compress")
     dop = _dev(u)
     x = torch.from_numpy(ex["vf_0"]).cuda()
-    first = dop.matvec(x, mode="fused").cpu().numpy()
+    first = dop.matvec(x, mode=mode).cpu().numpy()
     for _ in range(50):
-        w = dop.matvec(x, mode="fused")
+        w = dop.matvec(x, mode=mode)
     torch.cuda.synchronize()
     assert np.array_equal(w.cpu().numpy(), first)
     assert int(dop.counters.abs().sum()) == 0 and int(dop.ticket.item()) == 0

@@ -41,7 +41,7 @@ def test_config_parity(cfg):
         dop = DeviceOperator(pack(uv), device="cuda:0")
         for adj in (False, True):
             ref = oracle_matvec_uh(uv, x_np, adjoint=adj)
-            for mode in ("phased", "fused"):
+            for mode in ("phased", "fused", "bulk"):
                 w = dop.matvec(x, adjoint=adj, mode=mode).cpu().numpy()
                 assert rel(w, ref) <= TOL, (cfg, adj, mode, rel(w, ref))
         del dop
@@ -78,5 +78,7 @@ def test_config_properties(cfg):
     lhs = torch.vdot(ay, x)  # <A y, x>
     rhs = torch.vdot(y, dop.matvec(x, adjoint=True))  # <y, A^H x>
     assert abs((lhs - rhs).item()) <= 1e-11 * abs(lhs.item())
-    again = dop.matvec(x, mode="phased")
+    again = dop.matvec(x, mode="bulk")
     assert torch.equal(again, ax)
+    other = dop.matvec(x, mode="fused")
+    assert (torch.linalg.norm(other - ax) / torch.linalg.norm(ax)).item() <= 1e-13

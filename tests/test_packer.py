@@ -25,16 +25,47 @@ from paper_2405_15573_b200.packer import (
 TOL = 1e-12
 
 
-@pytest.mark.parametrize("order", ["phased", "fused"])
-def test_vm_matches_reference(golden, order):
+@pytest.mark.parametrize("order,engine", [("phased", "segs"), ("fused", "segs"), ("fused", "pieces")])
+def test_vm_matches_reference(golden, order, engine):
     name, u, ex = golden
     for vname, view, pfx in views():
         p = pack(view(u))
         for k in range(int(ex["nvec"])):
-            w = vm_matvec(p, ex[f"vf_{k}"], order=order)
+            w = vm_matvec(p, ex[f"vf_{k}"], order=order, engine=engine)
             assert rel(w, ex[f"{pfx}_fwd_{k}"]) <= TOL, (name, vname, order)
-            w = vm_matvec(p, ex[f"va_{k}"], adjoint=True, order=order)
+            w = vm_matvec(p, ex[f"va_{k}"], adjoint=True, order=order, engine=engine)
             assert rel(w, ex[f"{pfx}_adj_{k}"]) <= TOL, (name, vname, order, "adj")
+
+
+def test_pieces_tile_stages(golden):
+    """Bulk-kernel pieces: stages never overflow, begin/end flags pair up, every arena
+    element of every segment is covered exactly once."""
+    from paper_2405_15573_b200.packer import PI_BEGIN, PI_DIRECT, PI_END, STAGE_ELEMS
+
+    name, u, ex = golden
+    p = pack(u)
+    for prog in (p.fwd, p.adj):
+        for i in range(prog.n_ops):
+            pcs = prog.pieces[prog.ops[i, 13] : prog.ops[i, 14]]
+            open_ = False
+            fill = 0
+            for m_off, ld, rows, cols, mode, in_off, out_off, info in pcs:
+                if info & PI_DIRECT:
+                    continue
+                if info & PI_BEGIN:
+                    assert not open_
+                    open_ = True
+                    stage = (int(info) >> 32) & 0xFFFFFF
+                    assert 0 < stage <= STAGE_ELEMS
+                    fill = 0
+                assert open_
+                assert (int(info) & 0xFFFFFF) == fill
+                fill += rows * cols
+                assert fill <= STAGE_ELEMS
+                if info & PI_END:
+                    assert fill == stage
+                    open_ = False
+            assert not open_
 
 
 def test_program_invariants(golden):
