@@ -55,8 +55,10 @@ struct Params {
     int32_t skip_waits;  // phased launches: dependencies are ordered by the stream
 };
 
+constexpr int kDescCache = 64;  // piece descriptors cached in shared memory per batch
+
 struct Layout {
-    int stage_off, xin_off, out_off, bar_off, slot_off, total;
+    int stage_off, xin_off, out_off, desc_off, bar_off, slot_off, total;
 };
 
 __host__ __device__ inline Layout layout(int nstage, int xin_max, int out_max) {
@@ -64,7 +66,8 @@ __host__ __device__ inline Layout layout(int nstage, int xin_max, int out_max) {
     L.stage_off = 0;
     L.xin_off = nstage * kStageBytes;
     L.out_off = L.xin_off + ((xin_max * 16 + 127) & ~127);
-    L.bar_off = L.out_off + ((out_max * 16 + 127) & ~127);
+    L.desc_off = L.out_off + ((out_max * 16 + 127) & ~127);
+    L.bar_off = L.desc_off + kDescCache * kPieceFields * 8;
     L.slot_off = L.bar_off + (2 * nstage + 2 * kOpSlots) * 8;
     L.total = L.slot_off + 16 * 4;
     return L;
@@ -107,53 +110,82 @@ __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
+// Whole producer warp runs this loop in lock-step; lane 0 issues barriers and copies, the 32
+// lanes fetch piece descriptors 32 at a time (one coalesced round trip per batch instead of one
+// per piece), and the next ticket is claimed while the current op's pieces are issued.
 __device__ __forceinline__ void producer(const Params& p, unsigned char* stages, uint64_t* full,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
                                          int* slots) {
+    const int lane = threadIdx.x & 31;
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
     int stage = 0;
     uint32_t sphase = 0;
     int q = 0;
     uint32_t qphase = 0;
+    unsigned long long t_next = 0;
+    if (lane == 0) t_next = atomicAdd(p.ticket, 1ull);
+    t_next = __shfl_sync(0xffffffffu, t_next, 0);
     for (;;) {
-        const unsigned long long t = atomicAdd(p.ticket, 1ull);
-        const int op = (t < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t) : -1;
+        const int op = (t_next < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t_next) : -1;
+        int pc_b = 0, pc_e = 0;
+        if (op >= 0) {
+            pc_b = __ldg(p.ops + (int64_t)op * 16 + 13);
+            pc_e = __ldg(p.ops + (int64_t)op * 16 + 14);
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(p.ticket, 1ull);  // next op, overlapped with this one
+            t_next = __shfl_sync(0xffffffffu, t, 0);
+        }
         mbar_wait(&opempty[q], qphase ^ 1u);
-        slots[q] = op;
-        mbar_arrive(&opfull[q]);
+        if (lane == 0) {
+            slots[q] = op;
+            mbar_arrive(&opfull[q]);
+        }
         if (++q == kOpSlots) {
             q = 0;
             qphase ^= 1u;
         }
         if (op < 0) break;
-        const int pc_b = __ldg(p.ops + (int64_t)op * 16 + 13);
-        const int pc_e = __ldg(p.ops + (int64_t)op * 16 + 14);
-        for (int pc = pc_b; pc < pc_e; ++pc) {
-            const int64_t* d = p.pieces + (int64_t)pc * kPieceFields;
-            const int64_t info = __ldg(d + 7);
-            if (info & kPiDirect) continue;
-            if (info & kPiBegin) {
-                mbar_wait(&empty[stage], sphase ^ 1u);
-                mbar_arrive_expect_tx(&full[stage], (uint32_t)(((info >> 32) & 0xFFFFFF) * 16));
+        for (int base = pc_b; base < pc_e; base += 32) {
+            const int nb = min(32, pc_e - base);
+            int64_t f0 = 0, f1 = 0, f7 = kPiDirect;
+            int rc = 0;
+            if (lane < nb) {
+                const int64_t* d = p.pieces + (int64_t)(base + lane) * kPieceFields;
+                f0 = __ldg(d + 0);
+                f1 = __ldg(d + 1);
+                rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));  // rows <= 2^15, cols <= 2^16
+                f7 = __ldg(d + 7);
             }
-            const int64_t m_off = __ldg(d + 0);
-            const int64_t ld = __ldg(d + 1);
-            const int rows = (int)__ldg(d + 2);
-            const int cols = (int)__ldg(d + 3);
-            unsigned char* dst = stages + (size_t)stage * kStageBytes + (size_t)(info & 0xFFFFFF) * 16;
-            const double2* src = p.arena + m_off;
-            if (ld == cols) {
-                bulk_g2s(dst, src, (uint32_t)rows * cols * 16, &full[stage], policy);
-            } else {
-                for (int r = 0; r < rows; ++r)
-                    bulk_g2s(dst + (size_t)r * cols * 16, src + (int64_t)r * ld, (uint32_t)cols * 16,
-                             &full[stage], policy);
-            }
-            if (info & kPiEnd) {
-                if (++stage == p.nstage) {
-                    stage = 0;
-                    sphase ^= 1u;
+            for (int k = 0; k < nb; ++k) {
+                const int64_t info = __shfl_sync(0xffffffffu, f7, k);
+                if (info & kPiDirect) continue;
+                const int64_t m_off = __shfl_sync(0xffffffffu, f0, k);
+                const int64_t ld = __shfl_sync(0xffffffffu, f1, k);
+                const int rcv = __shfl_sync(0xffffffffu, rc, k);
+                const int rows = rcv >> 16, cols = rcv & 0xFFFF;
+                if (info & kPiBegin) {
+                    mbar_wait(&empty[stage], sphase ^ 1u);
+                    if (lane == 0)
+                        mbar_arrive_expect_tx(&full[stage], (uint32_t)(((info >> 32) & 0xFFFFFF) * 16));
+                }
+                if (lane == 0) {
+                    unsigned char* dst =
+                        stages + (size_t)stage * kStageBytes + (size_t)(info & 0xFFFFFF) * 16;
+                    const double2* src = p.arena + m_off;
+                    if (ld == cols) {
+                        bulk_g2s(dst, src, (uint32_t)rows * cols * 16, &full[stage], policy);
+                    } else {
+                        for (int r = 0; r < rows; ++r)
+                            bulk_g2s(dst + (size_t)r * cols * 16, src + (int64_t)r * ld,
+                                     (uint32_t)cols * 16, &full[stage], policy);
+                    }
+                }
+                if (info & kPiEnd) {
+                    if (++stage == p.nstage) {
+                        stage = 0;
+                        sphase ^= 1u;
+                    }
                 }
             }
         }
@@ -161,8 +193,9 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
 }
 
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
-                                         double2* outv, uint64_t* full, uint64_t* empty,
-                                         uint64_t* opfull, uint64_t* opempty, int* slots) {
+                                         double2* outv, int64_t* pdesc, uint64_t* full,
+                                         uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
+                                         int* slots) {
     const int tid = threadIdx.x;  // 0..127
     const int lane = tid & 31;
     const int g = tid & (kLanesPerRow - 1);
@@ -206,16 +239,27 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             for (int i = tid; i < len; i += kConsumers) xin[dst + i] = __ldcg(p.work + off + i);
         }
         for (int i = tid; i < n_out; i += kConsumers) outv[i] = make_double2(0.0, 0.0);
+        {
+            const int nb = min(kDescCache, pc_e - pc_b) * kPieceFields;
+            for (int i = tid; i < nb; i += kConsumers) pdesc[i] = __ldg(p.pieces + (int64_t)pc_b * kPieceFields + i);
+        }
         consumer_sync();
         bool hsync = false;
         for (int pc = pc_b; pc < pc_e; ++pc) {
-            const int64_t* d = p.pieces + (int64_t)pc * kPieceFields;
-            const int64_t info = __ldg(d + 7);
-            const int rows = (int)__ldg(d + 2);
-            const int cols = (int)__ldg(d + 3);
-            const int mode = (int)__ldg(d + 4);
-            const int in_off = (int)__ldg(d + 5);
-            const int out_off = (int)__ldg(d + 6);
+            const int slot = (pc - pc_b) & (kDescCache - 1);
+            if (slot == 0 && pc > pc_b) {  // refill the descriptor cache (ops with > 64 pieces)
+                consumer_sync();
+                const int nb = min(kDescCache, pc_e - pc) * kPieceFields;
+                for (int i = tid; i < nb; i += kConsumers) pdesc[i] = __ldg(p.pieces + (int64_t)pc * kPieceFields + i);
+                consumer_sync();
+            }
+            const int64_t* d = pdesc + slot * kPieceFields;
+            const int64_t info = d[7];
+            const int rows = (int)d[2];
+            const int cols = (int)d[3];
+            const int mode = (int)d[4];
+            const int in_off = (int)d[5];
+            const int out_off = (int)d[6];
             const bool direct = (info & kPiDirect) != 0;
             const bool xg = (info & kPiXGlobal) != 0;
             const double2* tile = nullptr;
@@ -260,8 +304,8 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 for (int j = j0; j < cols; j += kConsumers) {
                     double ar = 0.0, ai = 0.0;
                     if (mode == kModeS) {
-                        const int64_t ld = __ldg(d + 1);
-                        const double2* W = p.work + __ldg(d + 0) + j;
+                        const int64_t ld = d[1];
+                        const double2* W = p.work + d[0] + j;
 #pragma unroll 4
                         for (int r = 0; r < rows; ++r) {
                             const double2 m = __ldcg(W + (int64_t)r * ld);
@@ -330,6 +374,7 @@ __global__ void __launch_bounds__(kThreads) uhmv_bulk_kernel(const Params p) {
     unsigned char* stages = smem + L.stage_off;
     double2* xin = reinterpret_cast<double2*>(smem + L.xin_off);
     double2* outv = reinterpret_cast<double2*>(smem + L.out_off);
+    int64_t* pdesc = reinterpret_cast<int64_t*>(smem + L.desc_off);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
     uint64_t* empty = full + p.nstage;
     uint64_t* opfull = empty + p.nstage;
@@ -349,9 +394,9 @@ __global__ void __launch_bounds__(kThreads) uhmv_bulk_kernel(const Params p) {
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     if (warp == kConsumerWarps) {
-        if ((threadIdx.x & 31) == 0) producer(p, stages, full, empty, opfull, opempty, slots);
+        producer(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer(p, stages, xin, outv, full, empty, opfull, opempty, slots);
+        consumer(p, stages, xin, outv, pdesc, full, empty, opfull, opempty, slots);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch

@@ -66,7 +66,7 @@ KIND_NAMES = ["P1", "NEAR", "RED", "U", "Z", "FAR", "ZERO"]
 
 ALIGN = 8  # complex128 elements per 128 B
 HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
-ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op
+ROWS_PER_CHUNK = 40  # output rows per NEAR/FAR op (a whole leaf at configs 1-2, half at 3-4)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1024  # complex128 per shared-memory stage (16 KiB) of the bulk-copy kernel
 
@@ -164,8 +164,12 @@ def _chunks(lo, hi, step):
     return out
 
 
-def pack(u, *, rows_per_chunk: int = ROWS_PER_CHUNK, near_interleave=(0.4, 0.3, 0.3)) -> PackedOperator:
+def pack(u, *, rows_per_chunk: int | None = None, near_interleave=(0.4, 0.3, 0.3)) -> PackedOperator:
     """Pack a UniformHMatrix (reference object or mirror) into arena + programs."""
+    if rows_per_chunk is None:
+        import os
+
+        rows_per_chunk = int(os.environ.get("UHMV_ROWS_PER_CHUNK", ROWS_PER_CHUNK))
     bct = u.bct
     n_rows, n_cols = bct.shape
     rnodes, cnodes = bct.row_tree.nodes, bct.col_tree.nodes
