@@ -37,6 +37,7 @@ def parse():
     ap.add_argument("--mode", default="bulk", choices=["bulk", "fused", "phased"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--adjoint", action="store_true")
+    ap.add_argument("--view", default="full", choices=["full", "far", "near"], help="diagnostics: parity view")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     return ap.parse_args()
@@ -185,6 +186,12 @@ def main():
 
     t_build = time.perf_counter()
     u = workloads.build_operator(args.config)
+    if args.view != "full":
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from matvec_oracle import farfield_only, nearfield_only
+
+        u = farfield_only(u) if args.view == "far" else nearfield_only(u)
+        config["view"] = args.view
     x_np = workloads.seeded_vector(u.shape[1], 0)
     from paper_2405_15573_b200.packer import pack
 

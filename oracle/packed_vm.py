@@ -43,8 +43,6 @@ def run_op(prog, i, bufs, engine="segs"):
     out_b, out_e = (int(v) for v in prog.ops[i, 6:8])
     xin = np.zeros(n_in, dtype=np.complex128)
     for buf, off, ln, dst, _ in prog.runs[in_b:in_e]:
-        if engine == "pieces" and buf == BUF_X:
-            continue  # the bulk kernel reads x in place
         xin[dst : dst + ln] = bufs[buf][off : off + ln]
     out = np.zeros(n_out, dtype=np.complex128)
     for m_off, buf, rows, cols, ld, mode, in_off, out_off, xg in _segments(prog, i, engine):

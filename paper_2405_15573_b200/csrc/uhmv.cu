@@ -419,6 +419,7 @@ struct uhmv_plan {
     int bulk_smem[2];
     int bulk_nstage[2];
     int sm_count;
+    int debug_skip_waits;  // diagnostics only (UHMV_DEBUG_SKIP_WAITS): results are wrong
 };
 
 extern "C" {
@@ -500,8 +501,8 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     // bulk engine: as many 16-KiB stages as fit with the requested CTAs per SM
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, desc->device);
-    int want_ctas = 2;
-    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 2;
+    int want_ctas = 3;
+    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 3;
     int want_stages = 0;
     if (const char* ev = getenv("UHMV_NSTAGE")) want_stages = atoi(ev);
     int bulk_need = 0;
@@ -541,6 +542,7 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         if (grid > progs[k]->n_ops) grid = progs[k]->n_ops > 0 ? progs[k]->n_ops : 1;
         p->bulk_grid[k] = grid;
     }
+    if (const char* ev = getenv("UHMV_DEBUG_SKIP_WAITS")) p->debug_skip_waits = atoi(ev);
     *out = p;
     return UHMV_OK;
 }
@@ -566,7 +568,7 @@ static bulk::Params make_bulk_params(const uhmv_plan* plan, const uhmv_program& 
     bp.n_counters = pr.n_counters;
     bp.xin_max = pr.xin_max;
     bp.out_max = pr.out_max;
-    bp.skip_waits = 0;
+    bp.skip_waits = plan->debug_skip_waits;
     return bp;
 }
 

@@ -229,14 +229,18 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             }
         }
         consumer_sync();
-        // gather work-buffer inputs (x is read in place by the pieces)
+        // gather the op's input vector: x windows (read-only) and y/u/z (coherent ld.cg)
         for (int r = in_b; r < in_e; ++r) {
             const int64_t* rd = p.runs + (int64_t)r * kRunFields;
-            if ((int)__ldg(rd + 0) != kBufWork) continue;
+            const int buf = (int)__ldg(rd + 0);
             const int64_t off = __ldg(rd + 1);
             const int len = (int)__ldg(rd + 2);
             const int dst = (int)__ldg(rd + 3);
-            for (int i = tid; i < len; i += kConsumers) xin[dst + i] = __ldcg(p.work + off + i);
+            if (buf == kBufX) {
+                for (int i = tid; i < len; i += kConsumers) xin[dst + i] = __ldg(p.x + off + i);
+            } else {
+                for (int i = tid; i < len; i += kConsumers) xin[dst + i] = __ldcg(p.work + off + i);
+            }
         }
         for (int i = tid; i < n_out; i += kConsumers) outv[i] = make_double2(0.0, 0.0);
         {
@@ -274,14 +278,19 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 if (r0 < 0) r0 += kRowGroups;
                 for (int r = r0; r < rows; r += kRowGroups) {
                     const double2* T = tile + r * cols;
-                    double ar = 0.0, ai = 0.0;
+                    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+                    int j = g;
                     if (xg) {
-#pragma unroll 4
-                        for (int j = g; j < cols; j += kLanesPerRow) cmac(ar, ai, T[j], __ldg(xv + j));
+                        for (; j < cols; j += kLanesPerRow) cmac(ar, ai, T[j], __ldg(xv + j));
                     } else {
-#pragma unroll 4
-                        for (int j = g; j < cols; j += kLanesPerRow) cmac(ar, ai, T[j], xv[j]);
+                        for (; j + kLanesPerRow < cols; j += 2 * kLanesPerRow) {  // two chains
+                            cmac(ar, ai, T[j], xv[j]);
+                            cmac(br, bi, T[j + kLanesPerRow], xv[j + kLanesPerRow]);
+                        }
+                        if (j < cols) cmac(ar, ai, T[j], xv[j]);
                     }
+                    ar += br;
+                    ai += bi;
 #pragma unroll
                     for (int o = 1; o < kLanesPerRow; o <<= 1) {
                         ar += __shfl_xor_sync(gmask, ar, o);
@@ -299,32 +308,50 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     consumer_sync();
                     hsync = true;
                 }
-                int j0 = (tid - (out_off % kConsumers)) % kConsumers;
-                if (j0 < 0) j0 += kConsumers;
-                for (int j = j0; j < cols; j += kConsumers) {
-                    double ar = 0.0, ai = 0.0;
-                    if (mode == kModeS) {
-                        const int64_t ld = d[1];
-                        const double2* W = p.work + d[0] + j;
+                // P lanes per column (adjacent lanes), rows split r = p, p+P, ...; combined with
+                // an xor-shuffle tree (fixed order).  Column o = out_off + j is owned by the lane
+                // group (o % nJ), so every add to outv[o] comes from one thread.
+                const int P = cols <= 32 ? 4 : (cols <= 64 ? 2 : 1);
+                const int nJ = kConsumers / P;
+                const int pp = tid % P;
+                int j0 = (tid / P - (out_off % nJ)) % nJ;
+                if (j0 < 0) j0 += nJ;
+                const int jend = ((cols + nJ - 1) / nJ) * nJ;  // uniform trip count per warp
+                for (int j = j0; j < jend; j += nJ) {
+                    const bool live = j < cols;
+                    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+                    if (live) {
+                        if (mode == kModeS) {
+                            const int64_t ld = d[1];
+                            const double2* W = p.work + d[0] + j;
 #pragma unroll 4
-                        for (int r = 0; r < rows; ++r) {
-                            const double2 m = __ldcg(W + (int64_t)r * ld);
-                            ar += m.x;
-                            ai += m.y;
+                            for (int r = pp; r < rows; r += P) {
+                                const double2 m = __ldcg(W + (int64_t)r * ld);
+                                ar += m.x;
+                                ai += m.y;
+                            }
+                        } else {
+                            const double2* xv = xin + in_off;
+                            int r = pp;
+                            for (; r + P < rows; r += 2 * P) {  // two independent chains
+                                cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
+                                cmac_conj(br, bi, tile[(r + P) * cols + j], xv[r + P]);
+                            }
+                            if (r < rows) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
+                            ar += br;
+                            ai += bi;
                         }
-                    } else if (xg) {
-                        const double2* xv = p.x + in_off;
-#pragma unroll 4
-                        for (int r = 0; r < rows; ++r) cmac_conj(ar, ai, tile[r * cols + j], __ldg(xv + r));
-                    } else {
-                        const double2* xv = xin + in_off;
-#pragma unroll 4
-                        for (int r = 0; r < rows; ++r) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
                     }
-                    double2 v = outv[out_off + j];
-                    v.x += ar;
-                    v.y += ai;
-                    outv[out_off + j] = v;
+                    for (int o = 1; o < P; o <<= 1) {
+                        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+                    }
+                    if (live && pp == 0) {
+                        double2 v = outv[out_off + j];
+                        v.x += ar;
+                        v.y += ai;
+                        outv[out_off + j] = v;
+                    }
                 }
             }
             if (!direct && (info & kPiEnd)) {

@@ -660,7 +660,7 @@ def _finish(phased, fused, n_ctr):
             segs.extend(_panel_split(s))
         seg_e = len(segs)
         pc_b = len(pieces)
-        pieces.extend(_pieces(ordered, has_x))
+        pieces.extend(_pieces(ordered, False))  # x windows are staged in smem (L1 is carved out)
         pc_e = len(pieces)
         w_b = len(waits)
         waits.extend(wt)
@@ -668,7 +668,7 @@ def _finish(phased, fused, n_ctr):
         s_b = len(sigs)
         sigs.extend(sgn)
         s_e = len(sigs)
-        xin_len = 0 if has_x else n_in
+        xin_len = n_in
         ops[i] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind, pc_b, pc_e, xin_len)
         in_max = max(in_max, n_in)
         xin_max = max(xin_max, xin_len)
