@@ -21,6 +21,7 @@ from paper_2405_15573_b200.packer import (
     PI_DIRECT,
     PI_XGLOBAL,
     RUN_ADD,
+    RUN_ATOMIC,
 )
 
 __all__ = ["run_program", "vm_matvec"]
@@ -59,7 +60,7 @@ def run_op(prog, i, bufs, engine="segs"):
         else:
             raise ValueError(mode)
     for buf, off, ln, dst, flags in prog.runs[out_b:out_e]:
-        if flags & RUN_ADD:
+        if flags & (RUN_ADD | RUN_ATOMIC):
             bufs[buf][off : off + ln] += out[dst : dst + ln]
         else:
             bufs[buf][off : off + ln] = out[dst : dst + ln]
@@ -88,7 +89,7 @@ def vm_matvec(packed, v, adjoint=False, order="phased", engine="segs"):
     n_in, n_out = (packed.n_rows, packed.n_cols) if adjoint else (packed.n_cols, packed.n_rows)
     x = np.asarray(v, dtype=np.complex128)
     assert x.shape == (n_in,)
-    w = np.full(n_out, np.nan + 1j * np.nan)  # every entry must be written
+    w = np.zeros(n_out, dtype=np.complex128)  # the launcher zeroes w (NEAR/FAR add atomically)
     work = np.zeros(packed.work_len, dtype=np.complex128)
     run_program(prog, packed.arena, work, x, w, order=order, engine=engine)
     return w

@@ -306,8 +306,17 @@ __device__ void run_op(const ExecParams& p, int op, double2* xin, double2* outv,
         const int64_t off = __ldg(rd + 1);
         const int len = (int)__ldg(rd + 2);
         const int dst = (int)__ldg(rd + 3);
-        const int add = (int)(__ldg(rd + 4) & 1);
+        const int flags = (int)__ldg(rd + 4);
+        const int add = flags & 1;
         double2* dp = (buf == kBufW ? p.w : p.work) + off;
+        if (flags & 2) {  // fp64 red.add into the pre-zeroed output (<= 2 addends per entry)
+            for (int i = tid; i < len; i += kThreads) {
+                const double2 v = outv[dst + i];
+                atomicAdd(&dp[i].x, v.x);
+                atomicAdd(&dp[i].y, v.y);
+            }
+            continue;
+        }
         for (int i = tid; i < len; i += kThreads) {
             double2 v = outv[dst + i];
             if (add) {
@@ -477,10 +486,12 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         return fail(UHMV_EINVAL, "op vectors exceed shared memory (" + std::to_string(need) +
                                      " > " + std::to_string(smem_optin) + " bytes)");
     }
-    e = cudaFuncSetAttribute(uhmv_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, need);
+    // the attribute is per function, shared by every plan: always allow the opt-in maximum
+    e = cudaFuncSetAttribute(uhmv_phase_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             smem_optin);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(uhmv_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 need);
+                                 smem_optin);
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaFuncSetAttribute");
@@ -524,7 +535,7 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         return fail(UHMV_EINVAL, "bulk engine shared memory exceeds the opt-in limit");
     }
     e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             bulk_need);
+                             smem_optin);
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaFuncSetAttribute(bulk)");
@@ -605,6 +616,11 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
         return fail(UHMV_EINVAL, "uhmv_execute_phases: bad phase range");
     if (pr.n_ops > 0 && (!x || !w)) return fail(UHMV_EINVAL, "null vector pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
+    if (phase_lo == 0 && n_out > 0) {  // NEAR/FAR add into a zeroed output
+        cudaError_t e0 = cudaMemsetAsync(w, 0, (size_t)n_out * 16, st);
+        if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
+    }
     ExecParams ep = make_params(plan, pr, x, w);
     for (int ph = phase_lo; ph < phase_hi; ++ph) {
         const int n = pr.phase_hi[ph] - pr.phase_lo[ph];
@@ -624,6 +640,12 @@ int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode,
         return uhmv_execute_phases(plan, x, w, adjoint, 0, pr.n_phases, stream);
     if (mode != UHMV_MODE_FUSED && mode != UHMV_MODE_BULK)
         return fail(UHMV_EINVAL, "uhmv_execute: unknown mode");
+    const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
+    if (n_out > 0) {  // NEAR/FAR add into a zeroed output
+        if (!w) return fail(UHMV_EINVAL, "null output pointer");
+        cudaError_t e0 = cudaMemsetAsync(w, 0, (size_t)n_out * 16, static_cast<cudaStream_t>(stream));
+        if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
+    }
     if (pr.n_ops == 0) return UHMV_OK;
     if (!x || !w) return fail(UHMV_EINVAL, "null vector pointer");
     const int k = adjoint ? 1 : 0;

@@ -370,8 +370,17 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             const int64_t off = __ldg(rd + 1);
             const int len = (int)__ldg(rd + 2);
             const int dst = (int)__ldg(rd + 3);
-            const int add = (int)(__ldg(rd + 4) & 1);
+            const int flags = (int)__ldg(rd + 4);
+            const int add = flags & 1;
             double2* dp = (buf == kBufW ? p.w : p.work) + off;
+            if (flags & 2) {  // fp64 red.add into the pre-zeroed output (<= 2 addends per entry)
+                for (int i = tid; i < len; i += kConsumers) {
+                    const double2 v = outv[dst + i];
+                    atomicAdd(&dp[i].x, v.x);
+                    atomicAdd(&dp[i].y, v.y);
+                }
+                continue;
+            }
             for (int i = tid; i < len; i += kConsumers) {
                 double2 v = outv[dst + i];
                 if (add) {

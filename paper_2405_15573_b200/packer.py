@@ -48,7 +48,8 @@ __all__ = ["PackedOperator", "Program", "pack", "MODE_N", "MODE_H", "MODE_S"]
 
 MODE_N, MODE_H, MODE_S = 0, 1, 2
 BUF_ARENA, BUF_WORK, BUF_X, BUF_W = 0, 1, 2, 3
-RUN_ADD = 1
+RUN_ADD = 1  # out run: read-modify-write add (single writer)
+RUN_ATOMIC = 2  # out run: fp64 red.add -- w is zeroed first; <= 2 addends per entry
 
 OP_FIELDS = 16  # int32 per op
 # op layout: n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, wait_b, wait_e,
@@ -164,7 +165,7 @@ def _chunks(lo, hi, step):
     return out
 
 
-def pack(u, *, rows_per_chunk: int | None = None, near_interleave=(0.4, 0.3, 0.3)) -> PackedOperator:
+def pack(u, *, rows_per_chunk: int | None = None, near_interleave=(0.35, 0.1, 0.2, 0.35)) -> PackedOperator:
     """Pack a UniformHMatrix (reference object or mirror) into arena + programs."""
     if rows_per_chunk is None:
         import os
@@ -487,7 +488,9 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
         )
 
     # NEAR + FAR per output-leaf chunk
-    near_ctr = {}  # leaf -> [(a, b, counter)]
+    # The output w is zeroed by the launcher and every entry receives at most one NEAR and one
+    # FAR contribution through fp64 atomic adds: with two addends onto zero the sum is
+    # order-independent (fl(a+b) = fl(b+a)), so NEAR and FAR need no ordering between them.
     for p, leaf in enumerate(out_leaves):
         n = out_nodes[leaf]
         dlist = dense_by_outleaf.get(leaf, [])
@@ -515,30 +518,23 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
                     segs.append(_seg(offs[("D", bid)], BUF_ARENA, r.size, n.size, n.size, MODE_H, pos, 0, r.lo))
                     pos += r.size
                     nbytes += r.size * n.size
-            cid = ctr()
-            near_ctr.setdefault(leaf, []).append((a, b, cid))
-            ops[KIND_NEAR].append((KIND_NEAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, 0)], [], [cid], nbytes))
+            ops[KIND_NEAR].append((KIND_NEAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], [], [], nbytes))
+        anc = out_anc[p]
+        if not anc:
+            continue
         for a, b in _chunks(n.lo, n.hi, rows_per_chunk):
             rows = b - a
-            near_key = next((c for (na, nb, c) in near_ctr.get(leaf, []) if na <= a and b <= nb), None)
-            anc = out_anc[p]
-            if anc:
-                in_runs, segs, waits = [], [], []
-                pos = 0
-                for s in anc:
-                    ls = out_rank[s]
-                    in_runs.append((BUF_WORK, z_off[s], ls, pos, 0))
-                    segs.append(_seg(offs[(out_basis_key, s)] + (a - out_nodes[s].lo) * ls, BUF_ARENA, rows, ls, ls, MODE_N, pos, 0))
-                    waits.append((c_z[s], 1))
-                    pos += ls
-                if near_key is not None:
-                    waits.append((near_key, 1))
-                ops[KIND_FAR].append(
-                    (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ADD if near_key is not None else 0)],
-                     waits, [], rows * pos)
-                )
-            elif near_key is None:
-                ops[KIND_ZERO].append((KIND_ZERO, 0, rows, [], [], [(BUF_W, a, rows, 0, 0)], [], [], 0))
+            in_runs, segs, waits = [], [], []
+            pos = 0
+            for s in anc:
+                ls = out_rank[s]
+                in_runs.append((BUF_WORK, z_off[s], ls, pos, 0))
+                segs.append(_seg(offs[(out_basis_key, s)] + (a - out_nodes[s].lo) * ls, BUF_ARENA, rows, ls, ls, MODE_N, pos, 0))
+                waits.append((c_z[s], 1))
+                pos += ls
+            ops[KIND_FAR].append(
+                (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], waits, [], rows * pos)
+            )
 
     # ---- order: largest first inside each kind (reference uniform.py:505-506) ----
     for k in ops:
@@ -548,15 +544,16 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     f = f / f[-1]
     cut = [int(round(x * len(near))) for x in f]
     near_parts = [near[cut[i] : cut[i + 1]] for i in range(len(near_interleave))]
-    while len(near_parts) < 3:
+    while len(near_parts) < 4:
         near_parts.append([])
-    # phased launches (multi-launch mode): [P1 + NEAR + ZERO] [RED] [U] [Z] [FAR]
-    phased = [ops[KIND_P1] + near + ops[KIND_ZERO]]
+    # phased launches (multi-launch mode): [P1 + NEAR] [RED] [U] [Z] [FAR]
+    phased = [ops[KIND_P1] + near]
     phased += [ops[k] for k in (KIND_RED, KIND_U, KIND_Z, KIND_FAR)]
-    # fused persistent order: every op waits only on ops that come earlier
+    # fused persistent order: every op waits only on ops that come earlier; nearfield ops (no
+    # dependencies) are spread between the dependent farfield phases to cover their latency
     fused = (
-        ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + ops[KIND_U] + near_parts[1]
-        + ops[KIND_Z] + near_parts[2] + ops[KIND_ZERO] + ops[KIND_FAR]
+        ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
+        + ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
     )
     return _finish(phased, fused, n_ctr), work
 
