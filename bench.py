@@ -325,7 +325,10 @@ def main():
         "gpu_launches": args.steps * op.kernel_launches(args.adjoint, args.mode),
         "clocks": clk,
         "build_s": t_build,
+        "launch": op.launch_info(args.adjoint, args.mode) if world == 1 else None,
     }
+    if os.environ.get("UHMV_PROFILE") and world == 1 and args.mode == "bulk":
+        line["engine_cycles"] = op.profile(args.adjoint, args.mode)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(u, x_np, args.cpu_sample_s) if not args.adjoint else None
     print(json.dumps(line), flush=True)

@@ -107,6 +107,11 @@ int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjo
 int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int* smem_bytes,
                    int* threads_per_cta, int* stages);
 
+/* Diagnostics: per-CTA cycle counters of the bulk engine ([grid][8] uint64 device buffer, or
+ * NULL to disable): consumer waiting for data / dependencies / computing / op overhead,
+ * producer waiting for a free stage / an op slot, ops, pieces. */
+int uhmv_plan_set_profile(uhmv_plan* plan, void* counters);
+
 int uhmv_plan_destroy(uhmv_plan* plan);
 
 /* Thread-local text of the last failure ("" if none). */

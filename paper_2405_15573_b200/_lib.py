@@ -66,6 +66,7 @@ EXPORTS = (
     "uhmv_execute_phases",
     "uhmv_matvec_host",
     "uhmv_plan_info",
+    "uhmv_plan_set_profile",
     "uhmv_plan_destroy",
     "uhmv_last_error",
 )
@@ -95,6 +96,8 @@ def lib():
     pi = ctypes.POINTER(i32)
     L.uhmv_plan_info.argtypes = [vp, i32, i32, pi, pi, pi, pi]
     L.uhmv_plan_info.restype = i32
+    L.uhmv_plan_set_profile.argtypes = [vp, vp]
+    L.uhmv_plan_set_profile.restype = i32
     L.uhmv_plan_destroy.argtypes = [vp]
     L.uhmv_plan_destroy.restype = i32
     L.uhmv_last_error.restype = ctypes.c_char_p

@@ -429,6 +429,7 @@ struct uhmv_plan {
     int bulk_nstage[2];
     int sm_count;
     int debug_skip_waits;  // diagnostics only (UHMV_DEBUG_SKIP_WAITS): results are wrong
+    unsigned long long* prof;  // diagnostics only (uhmv_plan_set_profile)
 };
 
 extern "C" {
@@ -580,6 +581,7 @@ static bulk::Params make_bulk_params(const uhmv_plan* plan, const uhmv_program& 
     bp.xin_max = pr.xin_max;
     bp.out_max = pr.out_max;
     bp.skip_waits = plan->debug_skip_waits;
+    bp.prof = plan->prof;
     return bp;
 }
 
@@ -697,6 +699,12 @@ int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int*
     if (smem_bytes) *smem_bytes = b ? plan->bulk_smem[k] : plan->smem[k];
     if (threads_per_cta) *threads_per_cta = b ? bulk::kThreads : kThreads;
     if (stages) *stages = b ? plan->bulk_nstage[k] : 0;
+    return UHMV_OK;
+}
+
+int uhmv_plan_set_profile(uhmv_plan* plan, void* counters) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_set_profile: null plan");
+    plan->prof = static_cast<unsigned long long*>(counters);
     return UHMV_OK;
 }
 

@@ -53,7 +53,12 @@ struct Params {
     int32_t xin_max;
     int32_t out_max;
     int32_t skip_waits;  // phased launches: dependencies are ordered by the stream
+    unsigned long long* prof;  // optional [grid][8] cycle counters (UHMV_PROFILE), else null
 };
+
+// prof slots: 0 consumer wait for data, 1 consumer dependency wait, 2 consumer compute,
+// 3 consumer op overhead (gather/scatter/barriers), 4 producer wait for a free stage,
+// 5 producer wait for an op slot, 6 ops, 7 pieces
 
 constexpr int kDescCache = 64;  // piece descriptors cached in shared memory per batch
 
@@ -123,6 +128,8 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
     uint32_t sphase = 0;
     int q = 0;
     uint32_t qphase = 0;
+    unsigned long long c_empty = 0, c_slot = 0;
+    const bool prof = p.prof != nullptr && lane == 0;
     unsigned long long t_next = 0;
     if (lane == 0) t_next = atomicAdd(p.ticket, 1ull);
     t_next = __shfl_sync(0xffffffffu, t_next, 0);
@@ -136,7 +143,9 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
             if (lane == 0) t = atomicAdd(p.ticket, 1ull);  // next op, overlapped with this one
             t_next = __shfl_sync(0xffffffffu, t, 0);
         }
+        long long tq = prof ? clock64() : 0;
         mbar_wait(&opempty[q], qphase ^ 1u);
+        if (prof) c_slot += clock64() - tq;
         if (lane == 0) {
             slots[q] = op;
             mbar_arrive(&opfull[q]);
@@ -145,7 +154,13 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
             q = 0;
             qphase ^= 1u;
         }
-        if (op < 0) break;
+        if (op < 0) {
+            if (prof) {
+                p.prof[(size_t)blockIdx.x * 8 + 4] = c_empty;
+                p.prof[(size_t)blockIdx.x * 8 + 5] = c_slot;
+            }
+            break;
+        }
         for (int base = pc_b; base < pc_e; base += 32) {
             const int nb = min(32, pc_e - base);
             int64_t f0 = 0, f1 = 0, f7 = kPiDirect;
@@ -165,7 +180,9 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 const int rcv = __shfl_sync(0xffffffffu, rc, k);
                 const int rows = rcv >> 16, cols = rcv & 0xFFFF;
                 if (info & kPiBegin) {
+                    const long long te = prof ? clock64() : 0;
                     mbar_wait(&empty[stage], sphase ^ 1u);
+                    if (prof) c_empty += clock64() - te;
                     if (lane == 0)
                         mbar_arrive_expect_tx(&full[stage], (uint32_t)(((info >> 32) & 0xFFFFFF) * 16));
                 }
@@ -205,7 +222,10 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     uint32_t sphase = 0;
     int q = 0;
     uint32_t qphase = 0;
+    const bool prof = p.prof != nullptr && tid == 0;
+    unsigned long long c_data = 0, c_dep = 0, c_comp = 0, c_ovh = 0, n_ops = 0, n_pcs = 0;
     for (;;) {
+        long long t0 = prof ? clock64() : 0;
         mbar_wait(&opfull[q], qphase);
         const int op = slots[q];
         __syncwarp();
@@ -214,12 +234,29 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             q = 0;
             qphase ^= 1u;
         }
-        if (op < 0) break;
+        if (op < 0) {
+            if (prof) {
+                unsigned long long* pr = p.prof + (size_t)blockIdx.x * 8;
+                pr[0] = c_data;
+                pr[1] = c_dep;
+                pr[2] = c_comp;
+                pr[3] = c_ovh;
+                pr[6] = n_ops;
+                pr[7] = n_pcs;
+            }
+            break;
+        }
         const int32_t* hp = p.ops + (int64_t)op * 16;
         const int n_out = __ldg(hp + 1);
         const int in_b = __ldg(hp + 2), in_e = __ldg(hp + 3);
         const int out_b = __ldg(hp + 6), out_e = __ldg(hp + 7);
         const int pc_b = __ldg(hp + 13), pc_e = __ldg(hp + 14);
+        if (prof) {
+            const long long t1 = clock64();
+            c_ovh += t1 - t0;
+            t0 = t1;
+            ++n_ops;
+        }
         if (tid == 0 && !p.skip_waits) {
             const int wb = __ldg(hp + 8), we = __ldg(hp + 9);
             for (int i = wb; i < we; ++i) {
@@ -229,6 +266,11 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             }
         }
         consumer_sync();
+        if (prof) {
+            const long long t1 = clock64();
+            c_dep += t1 - t0;
+            t0 = t1;
+        }
         // gather the op's input vector: x windows (read-only) and y/u/z (coherent ld.cg)
         for (int r = in_b; r < in_e; ++r) {
             const int64_t* rd = p.runs + (int64_t)r * kRunFields;
@@ -267,8 +309,19 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             const bool direct = (info & kPiDirect) != 0;
             const bool xg = (info & kPiXGlobal) != 0;
             const double2* tile = nullptr;
+            if (prof) {
+                const long long t1 = clock64();
+                c_ovh += t1 - t0;
+                t0 = t1;
+                ++n_pcs;
+            }
             if (!direct) {
                 if (info & kPiBegin) mbar_wait(&full[stage], sphase);
+                if (prof) {
+                    const long long t1 = clock64();
+                    c_data += t1 - t0;
+                    t0 = t1;
+                }
                 tile = reinterpret_cast<const double2*>(stages + (size_t)stage * kStageBytes) +
                        (info & 0xFFFFFF);
             }
@@ -354,6 +407,11 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     }
                 }
             }
+            if (prof) {
+                const long long t1 = clock64();
+                c_comp += t1 - t0;
+                t0 = t1;
+            }
             if (!direct && (info & kPiEnd)) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
@@ -391,6 +449,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 __stcg(dp + i, v);
             }
         }
+        if (prof) c_ovh += clock64() - t0;
         if (!p.skip_waits) {
             consumer_sync();
             if (tid == 0) {

@@ -140,6 +140,23 @@ class DeviceOperator:
             return 0
         return len(prog.phases) if mode == "phased" else 1
 
+    def profile(self, adjoint=False, mode="bulk"):
+        """Diagnostics: run one matvec with the bulk engine's per-CTA cycle counters on and
+        return them summed over CTAs (see include/uhmv.h uhmv_plan_set_profile)."""
+        torch = self.torch
+        grid = self.launch_info(adjoint, mode)["grid"]
+        buf = torch.zeros((grid, 8), dtype=torch.int64, device=self.device)
+        _lib.check(_lib.lib().uhmv_plan_set_profile(self._plan, ctypes.c_void_p(buf.data_ptr())), "set_profile")
+        p = self.packed
+        n_in = p.n_rows if adjoint else p.n_cols
+        x = torch.ones(n_in, dtype=torch.complex128, device=self.device)
+        self.matvec(x, adjoint=adjoint, mode=mode)
+        torch.cuda.synchronize(self.device)
+        _lib.check(_lib.lib().uhmv_plan_set_profile(self._plan, None), "set_profile")
+        names = ["c_wait_data", "c_wait_dep", "c_compute", "c_overhead", "p_wait_stage", "p_wait_slot", "ops", "pieces"]
+        tot = buf.sum(dim=0).tolist()
+        return {"grid": grid, **{k: v for k, v in zip(names, tot)}}
+
     # ---- execution ----
     def _stream(self, stream):
         torch = self.torch

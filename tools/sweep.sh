@@ -1,9 +1,23 @@
 #!/bin/bash
-# quick perf sweep on the GPU box: prints ms/step and roofline frac per setting
+# quick perf sweep on the GPU box: prints ms/step, roofline frac, launch geometry and (with
+# UHMV_PROFILE=1) the bulk engine's cycle accounting, one line per setting
 mkdir -p gpurun_out
-run() {  # label, env..., args...
+run() {  # label; uses $ENVV and $ARGS
   local label=$1; shift
-  env "$@" > /dev/null
   out=$(env $ENVV timeout 300 python bench.py $ARGS --steps 20 --warmup 5 --no-cpu-baseline 2>&1 | tail -1)
-  echo "$label $(python -c "import json,sys; d=json.loads(sys.argv[1]); print('%.4f ms frac %.3f e2e %.1f' % (d['ms_per_step'], d['roofline']['frac'], d['e2e']['value']))" "$out" 2>/dev/null || echo "FAIL: $out" | tail -c 600)"
+  echo "$label $(python - "$out" <<'PY' 2>/dev/null || echo "FAIL: $(echo "$out" | tail -c 400)"
+import json, sys
+d = json.loads(sys.argv[1])
+s = '%.4f ms frac %.3f e2e %.1f' % (d['ms_per_step'], d['roofline']['frac'], d['e2e']['value'])
+L = d.get('launch') or {}
+s += ' grid %s st %s smem %s' % (L.get('grid'), L.get('stages'), L.get('smem_bytes'))
+c = d.get('engine_cycles')
+if c:
+    tot = c['c_wait_data'] + c['c_wait_dep'] + c['c_compute'] + c['c_overhead']
+    s += ' | cons data %.2f dep %.2f comp %.2f ovh %.2f | prod stage %.2f slot %.2f | ops %d pcs %d' % (
+        c['c_wait_data'] / tot, c['c_wait_dep'] / tot, c['c_compute'] / tot, c['c_overhead'] / tot,
+        c['p_wait_stage'] / tot, c['p_wait_slot'] / tot, c['ops'], c['pieces'])
+print(s)
+PY
+)"
 }
