@@ -61,6 +61,7 @@ struct Params {
 // 5 producer wait for an op slot, 6 ops, 7 pieces
 
 constexpr int kDescCache = 64;  // piece descriptors cached in shared memory per batch
+constexpr int kSlots = 8;       // register accumulator slots per thread (segment groups)
 
 struct Layout {
     int stage_off, xin_off, out_off, desc_off, bar_off, slot_off, total;
@@ -290,7 +291,63 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             for (int i = tid; i < nb; i += kConsumers) pdesc[i] = __ldg(p.pieces + (int64_t)pc_b * kPieceFields + i);
         }
         consumer_sync();
-        bool hsync = false;
+        // Segment groups accumulate in registers across all their pieces and are reduced once:
+        //   N group (all N pieces of the op): output row o is owned by row-group o % 16, register
+        //     slot o / 16 (n_out <= 128), partial over the lane's columns j = g (mod 8);
+        //   H/S group (pieces of one segment): output column j owned by lane group (j mod nJ),
+        //     slot = j / nJ, partial over the lane's rows r = pp (mod P).
+        double accr[kSlots], acci[kSlots];
+#pragma unroll
+        for (int k = 0; k < kSlots; ++k) accr[k] = acci[k] = 0.0;
+        const bool nreg = n_out <= kSlots * kRowGroups;
+        int g_mode = -1, g_out = 0, g_cols = 0;
+        auto flush = [&]() {
+            if (g_mode == kModeN) {
+                if (nreg) {
+#pragma unroll
+                    for (int k = 0; k < kSlots; ++k) {
+                        if (k * kRowGroups >= n_out) break;
+                        double ar = accr[k], ai = acci[k];
+#pragma unroll
+                        for (int o = 1; o < kLanesPerRow; o <<= 1) {
+                            ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                            ai += __shfl_xor_sync(0xffffffffu, ai, o);
+                        }
+                        const int o = k * kRowGroups + rg;
+                        if (g == 0 && o < n_out) {
+                            double2 v = outv[o];
+                            v.x += ar;
+                            v.y += ai;
+                            outv[o] = v;
+                        }
+                    }
+                }
+            } else if (g_mode >= 0) {
+                const int P = g_cols <= 32 ? 4 : (g_cols <= 64 ? 2 : 1);
+                const int nJ = kConsumers / P;
+                const int pp = tid % P;
+                int j0 = (tid / P - (g_out % nJ)) % nJ;
+                if (j0 < 0) j0 += nJ;
+#pragma unroll
+                for (int k = 0; k < kSlots; ++k) {
+                    if (k * nJ >= g_cols) break;
+                    double ar = accr[k], ai = acci[k];
+                    for (int o = 1; o < P; o <<= 1) {
+                        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+                    }
+                    const int j = j0 + k * nJ;
+                    if (pp == 0 && j < g_cols) {
+                        double2 v = outv[g_out + j];
+                        v.x += ar;
+                        v.y += ai;
+                        outv[g_out + j] = v;
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kSlots; ++k) accr[k] = acci[k] = 0.0;
+        };
         for (int pc = pc_b; pc < pc_e; ++pc) {
             const int slot = (pc - pc_b) & (kDescCache - 1);
             if (slot == 0 && pc > pc_b) {  // refill the descriptor cache (ops with > 64 pieces)
@@ -307,7 +364,16 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             const int in_off = (int)d[5];
             const int out_off = (int)d[6];
             const bool direct = (info & kPiDirect) != 0;
-            const bool xg = (info & kPiXGlobal) != 0;
+            // group change?
+            if (mode == kModeN ? (g_mode != kModeN)
+                               : (g_mode != mode || g_out != out_off || g_cols != cols)) {
+                const bool to_h = (g_mode == kModeN) && mode != kModeN;
+                flush();
+                if (to_h) consumer_sync();  // N owners and H owners differ: order their outv adds
+                g_mode = mode;
+                g_out = out_off;
+                g_cols = cols;
+            }
             const double2* tile = nullptr;
             if (prof) {
                 const long long t1 = clock64();
@@ -326,85 +392,75 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                        (info & 0xFFFFFF);
             }
             if (mode == kModeN) {
-                const double2* xv = xg ? (p.x + in_off) : (xin + in_off);
+                const double2* xv = xin + in_off;
                 int r0 = (rg - (out_off % kRowGroups)) % kRowGroups;
                 if (r0 < 0) r0 += kRowGroups;
                 for (int r = r0; r < rows; r += kRowGroups) {
                     const double2* T = tile + r * cols;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
                     int j = g;
-                    if (xg) {
-                        for (; j < cols; j += kLanesPerRow) cmac(ar, ai, T[j], __ldg(xv + j));
-                    } else {
-                        for (; j + kLanesPerRow < cols; j += 2 * kLanesPerRow) {  // two chains
-                            cmac(ar, ai, T[j], xv[j]);
-                            cmac(br, bi, T[j + kLanesPerRow], xv[j + kLanesPerRow]);
-                        }
-                        if (j < cols) cmac(ar, ai, T[j], xv[j]);
+                    for (; j + kLanesPerRow < cols; j += 2 * kLanesPerRow) {  // two chains
+                        cmac(ar, ai, T[j], xv[j]);
+                        cmac(br, bi, T[j + kLanesPerRow], xv[j + kLanesPerRow]);
                     }
+                    if (j < cols) cmac(ar, ai, T[j], xv[j]);
                     ar += br;
                     ai += bi;
+                    const int o = out_off + r;
+                    if (nreg) {
+                        const int k = o / kRowGroups;
 #pragma unroll
-                    for (int o = 1; o < kLanesPerRow; o <<= 1) {
-                        ar += __shfl_xor_sync(gmask, ar, o);
-                        ai += __shfl_xor_sync(gmask, ai, o);
-                    }
-                    if (g == 0) {
-                        double2 v = outv[out_off + r];
-                        v.x += ar;
-                        v.y += ai;
-                        outv[out_off + r] = v;
+                        for (int q = 0; q < kSlots; ++q)
+                            if (q == k) {
+                                accr[q] += ar;
+                                acci[q] += ai;
+                            }
+                    } else {  // wide N op: reduce and add per row
+#pragma unroll
+                        for (int s2 = 1; s2 < kLanesPerRow; s2 <<= 1) {
+                            ar += __shfl_xor_sync(gmask, ar, s2);
+                            ai += __shfl_xor_sync(gmask, ai, s2);
+                        }
+                        if (g == 0) {
+                            double2 v = outv[o];
+                            v.x += ar;
+                            v.y += ai;
+                            outv[o] = v;
+                        }
                     }
                 }
             } else {
-                if (!hsync) {  // N owners (8*rg) and H owners (o % 128) differ: order them
-                    consumer_sync();
-                    hsync = true;
-                }
-                // P lanes per column (adjacent lanes), rows split r = p, p+P, ...; combined with
-                // an xor-shuffle tree (fixed order).  Column o = out_off + j is owned by the lane
-                // group (o % nJ), so every add to outv[o] comes from one thread.
                 const int P = cols <= 32 ? 4 : (cols <= 64 ? 2 : 1);
                 const int nJ = kConsumers / P;
                 const int pp = tid % P;
                 int j0 = (tid / P - (out_off % nJ)) % nJ;
                 if (j0 < 0) j0 += nJ;
-                const int jend = ((cols + nJ - 1) / nJ) * nJ;  // uniform trip count per warp
-                for (int j = j0; j < jend; j += nJ) {
-                    const bool live = j < cols;
+#pragma unroll
+                for (int k = 0; k < kSlots; ++k) {
+                    if (k * nJ >= cols) break;
+                    const int j = j0 + k * nJ;
+                    if (j >= cols) continue;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
-                    if (live) {
-                        if (mode == kModeS) {
-                            const int64_t ld = d[1];
-                            const double2* W = p.work + d[0] + j;
+                    if (mode == kModeS) {
+                        const int64_t ld = d[1];
+                        const double2* W = p.work + d[0] + j;
 #pragma unroll 4
-                            for (int r = pp; r < rows; r += P) {
-                                const double2 m = __ldcg(W + (int64_t)r * ld);
-                                ar += m.x;
-                                ai += m.y;
-                            }
-                        } else {
-                            const double2* xv = xin + in_off;
-                            int r = pp;
-                            for (; r + P < rows; r += 2 * P) {  // two independent chains
-                                cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
-                                cmac_conj(br, bi, tile[(r + P) * cols + j], xv[r + P]);
-                            }
-                            if (r < rows) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
-                            ar += br;
-                            ai += bi;
+                        for (int r = pp; r < rows; r += P) {
+                            const double2 m = __ldcg(W + (int64_t)r * ld);
+                            ar += m.x;
+                            ai += m.y;
                         }
+                    } else {
+                        const double2* xv = xin + in_off;
+                        int r = pp;
+                        for (; r + P < rows; r += 2 * P) {  // two independent chains
+                            cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
+                            cmac_conj(br, bi, tile[(r + P) * cols + j], xv[r + P]);
+                        }
+                        if (r < rows) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
                     }
-                    for (int o = 1; o < P; o <<= 1) {
-                        ar += __shfl_xor_sync(0xffffffffu, ar, o);
-                        ai += __shfl_xor_sync(0xffffffffu, ai, o);
-                    }
-                    if (live && pp == 0) {
-                        double2 v = outv[out_off + j];
-                        v.x += ar;
-                        v.y += ai;
-                        outv[out_off + j] = v;
-                    }
+                    accr[k] += ar + br;
+                    acci[k] += ai + bi;
                 }
             }
             if (prof) {
@@ -421,6 +477,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 }
             }
         }
+        flush();
         consumer_sync();
         for (int r = out_b; r < out_e; ++r) {
             const int64_t* rd = p.runs + (int64_t)r * kRunFields;
