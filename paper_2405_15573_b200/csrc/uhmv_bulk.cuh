@@ -1,21 +1,28 @@
 // uhmv_bulk.cuh -- warp-specialised bulk-copy engine for the uniform-H op programs (sm_100a).
 //
-// Same op semantics as the register kernel in uhmv.cu, different data path: every arena slab
-// an op streams is cut on the host into "pieces" (row ranges, packer._pieces) packed into
-// 16-KiB shared-memory stages.  One producer lane per CTA claims ops from the fused ticket
-// order, publishes them to the consumer warps through an op-slot ring, and streams their
-// pieces with cp.async.bulk (the TMA engine, SASS UBLKCP) into an mbarrier-guarded stage
-// ring -- WITHOUT waiting for the op's dependencies: arena data never depends on anything, so
-// HBM streaming runs ahead across ops while the consumers wait for y/u/z.  Four consumer warps
-// gather the op's work-buffer inputs, compute the GEMV pieces out of shared memory, and write
-// the op's outputs.  Bytes in flight per SM are set by the ring (stages x 16 KiB x CTAs/SM),
-// not by registers or warp count.
+// Same op semantics as the register kernel in uhmv.cu, different data path.  Every arena slab an
+// op streams is cut on the host into "pieces" (row ranges, packer._pieces) packed into 16-KiB
+// shared-memory stages.  Per CTA:
 //
-//   N piece: out[r] += sum_j T[r,j] in[j]     8 lanes per row (128 B of smem per row-group
-//            load, conflict-free), rows owned by row-group (out_off+r) % 16 -> no atomics.
-//   H piece: out[j] += sum_r conj(T[r,j]) in[r]   column j owned by thread (out_off+j) % 128.
-//   S piece: out[j] += sum_r W[r,j] read directly (ld.cg) from the work buffer (partials).
-// "in" is the op's shared-memory gather of y/u/z, or x read in place (ld.global.nc, L1/L2).
+//   producer warp  claims ops from the fused ticket order (one ticket ahead), prefetches each
+//                  op's header, run table and compressed piece descriptors into an op slot in
+//                  shared memory (one coalesced round trip), publishes the slot, then streams the
+//                  op's pieces with cp.async.bulk (TMA engine, SASS UBLKCP) into an mbarrier-
+//                  guarded stage ring.  It never waits for an op's dependencies -- arena data
+//                  depends on nothing -- so HBM streaming runs ahead across ops.
+//   4 consumer     wait for the op's dependency counters (ld.acquire.gpu), gather the op's input
+//   warps          vector into shared memory (one batched round trip), compute the GEMV pieces
+//                  out of the stage ring accumulating each segment group in registers, reduce
+//                  once per group, scatter the outputs (st.cg / fp64 red.add) and signal
+//                  (red.release.gpu).
+//
+//   N group: out[o] += sum_j T[r,j] in[j]   row o owned by row-group o % 16 (8 lanes per row,
+//            128 contiguous smem bytes per row-group load), register slot o / 16.
+//   H group: out[j] += sum_r conj(T[r,j]) in[r]   column j owned by a P-lane group (rows split
+//            over the P lanes), register slot j / nJ.
+//   S group: out[j] += sum_r W[r,j] over the partial vectors, read directly (ld.cg) from work.
+// Every output entry has exactly one owner thread and a fixed summation order: results are
+// bit-reproducible run to run.
 
 #pragma once
 
@@ -26,12 +33,31 @@ constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
 constexpr int kStageElems = 1024;                // = packer.STAGE_ELEMS (16 KiB of complex128)
 constexpr int kStageBytes = kStageElems * 16;
-constexpr int kOpSlots = 4;
+constexpr int kOpSlots = 2;
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
 constexpr int kPieceFields = 8;
-constexpr int64_t kPiBegin = 1ll << 24, kPiEnd = 1ll << 25, kPiDirect = 1ll << 26,
-                  kPiXGlobal = 1ll << 27;
+constexpr int kSlots = 8;         // register accumulator slots per thread
+constexpr int kSlotRuns = 48;     // run descriptors cached per op slot
+constexpr int kSlotPieces = 128;  // piece descriptors cached per op slot
+constexpr int kGatherBatch = 8;   // loads in flight per thread in the gather
+constexpr int64_t kPiBegin = 1ll << 24, kPiEnd = 1ll << 25, kPiDirect = 1ll << 26;
+
+// compressed consumer-side piece descriptor (int4):
+//   x = rows << 16 | cols, y = in_off, z = out_off,
+//   w = smem_off | mode << 16 | begin << 20 | end << 21 | direct << 22
+constexpr int kCBegin = 1 << 20, kCEnd = 1 << 21, kCDirect = 1 << 22;
+
+struct OpSlot {
+    int hdr[16];
+    int64_t roff[kSlotRuns];
+    int rlen[kSlotRuns];
+    int rdst[kSlotRuns];
+    int rbf[kSlotRuns];  // buf | flags << 8
+    int4 pc[kSlotPieces];
+    int op;
+    int pad[3];
+};
 
 struct Params {
     const double2* arena;
@@ -52,19 +78,16 @@ struct Params {
     int32_t n_counters;
     int32_t xin_max;
     int32_t out_max;
-    int32_t skip_waits;  // phased launches: dependencies are ordered by the stream
-    unsigned long long* prof;  // optional [grid][8] cycle counters (UHMV_PROFILE), else null
+    int32_t skip_waits;        // diagnostics: ignore dependencies (results are wrong)
+    unsigned long long* prof;  // optional [grid][64] cycle counters, else null
 };
 
-// prof slots: 0 consumer wait for data, 1 consumer dependency wait, 2 consumer compute,
-// 3 consumer op overhead (gather/scatter/barriers), 4 producer wait for a free stage,
-// 5 producer wait for an op slot, 6 ops, 7 pieces
-
-constexpr int kDescCache = 64;  // piece descriptors cached in shared memory per batch
-constexpr int kSlots = 8;       // register accumulator slots per thread (segment groups)
+// prof layout per CTA (64 x u64): [kind * 8 + c] for op kinds 0..6 with c = 0 consumer waiting
+// for stage data, 1 dependency wait, 2 compute, 3 op prologue/epilogue, 4 pieces, 5 ops;
+// [56] producer waiting for a free stage, [57] producer waiting for a free op slot.
 
 struct Layout {
-    int stage_off, xin_off, out_off, desc_off, bar_off, slot_off, total;
+    int stage_off, xin_off, out_off, slot_off, bar_off, total;
 };
 
 __host__ __device__ inline Layout layout(int nstage, int xin_max, int out_max) {
@@ -72,10 +95,9 @@ __host__ __device__ inline Layout layout(int nstage, int xin_max, int out_max) {
     L.stage_off = 0;
     L.xin_off = nstage * kStageBytes;
     L.out_off = L.xin_off + ((xin_max * 16 + 127) & ~127);
-    L.desc_off = L.out_off + ((out_max * 16 + 127) & ~127);
-    L.bar_off = L.desc_off + kDescCache * kPieceFields * 8;
-    L.slot_off = L.bar_off + (2 * nstage + 2 * kOpSlots) * 8;
-    L.total = L.slot_off + 16 * 4;
+    L.slot_off = L.out_off + ((out_max * 16 + 127) & ~127);
+    L.bar_off = L.slot_off + kOpSlots * (int)sizeof(OpSlot);
+    L.total = L.bar_off + (2 * nstage + 2 * kOpSlots) * 8 + 16;
     return L;
 }
 
@@ -112,16 +134,27 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(su32(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
 
-// Whole producer warp runs this loop in lock-step; lane 0 issues barriers and copies, the 32
-// lanes fetch piece descriptors 32 at a time (one coalesced round trip per batch instead of one
-// per piece), and the next ticket is claimed while the current op's pieces are issued.
+__device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64_t mode,
+                                               int64_t in_off, int64_t out_off, int64_t info) {
+    int4 c;
+    c.x = (int)((rows << 16) | cols);
+    c.y = (int)in_off;
+    c.z = (int)out_off;
+    c.w = (int)((info & 0xFFFF) | (mode << 16) | ((info & kPiBegin) ? kCBegin : 0) |
+                ((info & kPiEnd) ? kCEnd : 0) | ((info & kPiDirect) ? kCDirect : 0));
+    return c;
+}
+
 __device__ __forceinline__ void producer(const Params& p, unsigned char* stages, uint64_t* full,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
-                                         int* slots) {
+                                         OpSlot* slots) {
     const int lane = threadIdx.x & 31;
     uint64_t policy;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
@@ -136,29 +169,74 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
     t_next = __shfl_sync(0xffffffffu, t_next, 0);
     for (;;) {
         const int op = (t_next < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t_next) : -1;
-        int pc_b = 0, pc_e = 0;
+        int hv = 0;
         if (op >= 0) {
-            pc_b = __ldg(p.ops + (int64_t)op * 16 + 13);
-            pc_e = __ldg(p.ops + (int64_t)op * 16 + 14);
+            if (lane < 16) hv = __ldg(p.ops + (int64_t)op * 16 + lane);
             unsigned long long t = 0;
             if (lane == 0) t = atomicAdd(p.ticket, 1ull);  // next op, overlapped with this one
             t_next = __shfl_sync(0xffffffffu, t, 0);
         }
-        long long tq = prof ? clock64() : 0;
+        const int in_b = __shfl_sync(0xffffffffu, hv, 2);
+        const int out_e = __shfl_sync(0xffffffffu, hv, 7);
+        const int pc_b = __shfl_sync(0xffffffffu, hv, 13);
+        const int pc_e = __shfl_sync(0xffffffffu, hv, 14);
+        // prefetch the run table and the first kSlotPieces piece descriptors
+        int64_t roff[2];
+        int rlen[2], rdst[2], rbf[2];
+        const int n_runs = op >= 0 ? out_e - in_b : 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int r = lane + 32 * k;
+            if (r < n_runs && r < kSlotRuns) {
+                const int64_t* rd = p.runs + (int64_t)(in_b + r) * kRunFields;
+                roff[k] = __ldg(rd + 1);
+                rlen[k] = (int)__ldg(rd + 2);
+                rdst[k] = (int)__ldg(rd + 3);
+                rbf[k] = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
+            }
+        }
+        int4 cp[kSlotPieces / 32];
+        const int n_pc = op >= 0 ? pc_e - pc_b : 0;
+#pragma unroll
+        for (int k = 0; k < kSlotPieces / 32; ++k) {
+            const int i = lane + 32 * k;
+            if (i < n_pc) {
+                const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
+                cp[k] = compress_piece(__ldg(d + 2), __ldg(d + 3), __ldg(d + 4), __ldg(d + 5),
+                                       __ldg(d + 6), __ldg(d + 7));
+            }
+        }
+        const long long tq = prof ? clock64() : 0;
         mbar_wait(&opempty[q], qphase ^ 1u);
         if (prof) c_slot += clock64() - tq;
-        if (lane == 0) {
-            slots[q] = op;
-            mbar_arrive(&opfull[q]);
+        OpSlot* S = slots + q;
+        if (lane < 16) S->hdr[lane] = hv;
+        if (lane == 0) S->op = op;
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int r = lane + 32 * k;
+            if (r < n_runs && r < kSlotRuns) {
+                S->roff[r] = roff[k];
+                S->rlen[r] = rlen[k];
+                S->rdst[r] = rdst[k];
+                S->rbf[r] = rbf[k];
+            }
         }
+#pragma unroll
+        for (int k = 0; k < kSlotPieces / 32; ++k) {
+            const int i = lane + 32 * k;
+            if (i < n_pc) S->pc[i] = cp[k];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&opfull[q]);  // release: the slot writes above are visible
         if (++q == kOpSlots) {
             q = 0;
             qphase ^= 1u;
         }
         if (op < 0) {
             if (prof) {
-                p.prof[(size_t)blockIdx.x * 8 + 4] = c_empty;
-                p.prof[(size_t)blockIdx.x * 8 + 5] = c_slot;
+                p.prof[(size_t)blockIdx.x * 64 + 56] = c_empty;
+                p.prof[(size_t)blockIdx.x * 64 + 57] = c_slot;
             }
             break;
         }
@@ -170,7 +248,7 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 const int64_t* d = p.pieces + (int64_t)(base + lane) * kPieceFields;
                 f0 = __ldg(d + 0);
                 f1 = __ldg(d + 1);
-                rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));  // rows <= 2^15, cols <= 2^16
+                rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));
                 f7 = __ldg(d + 7);
             }
             for (int k = 0; k < nb; ++k) {
@@ -210,10 +288,50 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
     }
 }
 
+struct RunRef {
+    int64_t off;
+    int len, dst, bf;
+};
+
+__device__ __forceinline__ RunRef get_run(const Params& p, const OpSlot* S, int base, int r) {
+    RunRef R;
+    if (r < kSlotRuns) {
+        R.off = S->roff[r];
+        R.len = S->rlen[r];
+        R.dst = S->rdst[r];
+        R.bf = S->rbf[r];
+    } else {
+        const int64_t* rd = p.runs + (int64_t)(base + r) * kRunFields;
+        R.off = __ldg(rd + 1);
+        R.len = (int)__ldg(rd + 2);
+        R.dst = (int)__ldg(rd + 3);
+        R.bf = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
+    }
+    return R;
+}
+
+// run containing vector position pos among runs [lo, hi) (sorted by dst, contiguous cover)
+__device__ __forceinline__ int find_run(const Params& p, const OpSlot* S, int base, int lo, int hi,
+                                        int pos) {
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        const int d = (mid < kSlotRuns) ? S->rdst[mid] : (int)__ldg(p.runs + (int64_t)(base + mid) * kRunFields + 3);
+        if (d <= pos) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int4 get_piece(const Params& p, const OpSlot* S, int pc_b, int i) {
+    if (i < kSlotPieces) return S->pc[i];
+    const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
+    return compress_piece(__ldg(d + 2), __ldg(d + 3), __ldg(d + 4), __ldg(d + 5), __ldg(d + 6),
+                          __ldg(d + 7));
+}
+
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
-                                         double2* outv, int64_t* pdesc, uint64_t* full,
-                                         uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
-                                         int* slots) {
+                                         double2* outv, uint64_t* full, uint64_t* empty,
+                                         uint64_t* opfull, uint64_t* opempty, OpSlot* slots) {
     const int tid = threadIdx.x;  // 0..127
     const int lane = tid & 31;
     const int g = tid & (kLanesPerRow - 1);
@@ -224,42 +342,22 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     int q = 0;
     uint32_t qphase = 0;
     const bool prof = p.prof != nullptr && tid == 0;
-    unsigned long long c_data = 0, c_dep = 0, c_comp = 0, c_ovh = 0, n_ops = 0, n_pcs = 0;
+    unsigned long long* pr = prof ? p.prof + (size_t)blockIdx.x * 64 : nullptr;
     for (;;) {
         long long t0 = prof ? clock64() : 0;
         mbar_wait(&opfull[q], qphase);
-        const int op = slots[q];
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&opempty[q]);
-        if (++q == kOpSlots) {
-            q = 0;
-            qphase ^= 1u;
-        }
-        if (op < 0) {
-            if (prof) {
-                unsigned long long* pr = p.prof + (size_t)blockIdx.x * 8;
-                pr[0] = c_data;
-                pr[1] = c_dep;
-                pr[2] = c_comp;
-                pr[3] = c_ovh;
-                pr[6] = n_ops;
-                pr[7] = n_pcs;
-            }
-            break;
-        }
-        const int32_t* hp = p.ops + (int64_t)op * 16;
-        const int n_out = __ldg(hp + 1);
-        const int in_b = __ldg(hp + 2), in_e = __ldg(hp + 3);
-        const int out_b = __ldg(hp + 6), out_e = __ldg(hp + 7);
-        const int pc_b = __ldg(hp + 13), pc_e = __ldg(hp + 14);
-        if (prof) {
-            const long long t1 = clock64();
-            c_ovh += t1 - t0;
-            t0 = t1;
-            ++n_ops;
-        }
+        const OpSlot* S = slots + q;
+        const int op = S->op;
+        if (op < 0) break;
+        const int n_out = S->hdr[1];
+        const int in_b = S->hdr[2], in_e = S->hdr[3];
+        const int out_e = S->hdr[7];
+        const int pc_b = S->hdr[13], pc_e = S->hdr[14];
+        const int kind = S->hdr[12] & 7;
+        const int n_in_runs = in_e - in_b;
+        const int n_runs = out_e - in_b;
         if (tid == 0 && !p.skip_waits) {
-            const int wb = __ldg(hp + 8), we = __ldg(hp + 9);
+            const int wb = S->hdr[8], we = S->hdr[9];
             for (int i = wb; i < we; ++i) {
                 const int c = __ldg(p.waits + 2 * i);
                 const uint32_t need = (uint32_t)__ldg(p.waits + 2 * i + 1);
@@ -269,33 +367,32 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         consumer_sync();
         if (prof) {
             const long long t1 = clock64();
-            c_dep += t1 - t0;
+            pr[kind * 8 + 1] += t1 - t0;
             t0 = t1;
+            pr[kind * 8 + 5] += 1;
         }
-        // gather the op's input vector: x windows (read-only) and y/u/z (coherent ld.cg)
-        for (int r = in_b; r < in_e; ++r) {
-            const int64_t* rd = p.runs + (int64_t)r * kRunFields;
-            const int buf = (int)__ldg(rd + 0);
-            const int64_t off = __ldg(rd + 1);
-            const int len = (int)__ldg(rd + 2);
-            const int dst = (int)__ldg(rd + 3);
-            if (buf == kBufX) {
-                for (int i = tid; i < len; i += kConsumers) xin[dst + i] = __ldg(p.x + off + i);
-            } else {
-                for (int i = tid; i < len; i += kConsumers) xin[dst + i] = __ldcg(p.work + off + i);
+        // gather the input vector: all loads of a batch issued before any smem store
+        const int n_in = S->hdr[0];
+        for (int base = 0; base < n_in; base += kGatherBatch * kConsumers) {
+            double2 v[kGatherBatch];
+#pragma unroll
+            for (int k = 0; k < kGatherBatch; ++k) {
+                const int pos = base + tid + k * kConsumers;
+                if (pos < n_in) {
+                    const RunRef R = get_run(p, S, in_b, find_run(p, S, in_b, 0, n_in_runs, pos));
+                    const int64_t src = R.off + (pos - R.dst);
+                    v[k] = ((R.bf & 0xFF) == kBufX) ? __ldg(p.x + src) : __ldcg(p.work + src);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < kGatherBatch; ++k) {
+                const int pos = base + tid + k * kConsumers;
+                if (pos < n_in) xin[pos] = v[k];
             }
         }
         for (int i = tid; i < n_out; i += kConsumers) outv[i] = make_double2(0.0, 0.0);
-        {
-            const int nb = min(kDescCache, pc_e - pc_b) * kPieceFields;
-            for (int i = tid; i < nb; i += kConsumers) pdesc[i] = __ldg(p.pieces + (int64_t)pc_b * kPieceFields + i);
-        }
         consumer_sync();
-        // Segment groups accumulate in registers across all their pieces and are reduced once:
-        //   N group (all N pieces of the op): output row o is owned by row-group o % 16, register
-        //     slot o / 16 (n_out <= 128), partial over the lane's columns j = g (mod 8);
-        //   H/S group (pieces of one segment): output column j owned by lane group (j mod nJ),
-        //     slot = j / nJ, partial over the lane's rows r = pp (mod P).
+
         double accr[kSlots], acci[kSlots];
 #pragma unroll
         for (int k = 0; k < kSlots; ++k) accr[k] = acci[k] = 0.0;
@@ -348,23 +445,17 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
 #pragma unroll
             for (int k = 0; k < kSlots; ++k) accr[k] = acci[k] = 0.0;
         };
-        for (int pc = pc_b; pc < pc_e; ++pc) {
-            const int slot = (pc - pc_b) & (kDescCache - 1);
-            if (slot == 0 && pc > pc_b) {  // refill the descriptor cache (ops with > 64 pieces)
-                consumer_sync();
-                const int nb = min(kDescCache, pc_e - pc) * kPieceFields;
-                for (int i = tid; i < nb; i += kConsumers) pdesc[i] = __ldg(p.pieces + (int64_t)pc * kPieceFields + i);
-                consumer_sync();
-            }
-            const int64_t* d = pdesc + slot * kPieceFields;
-            const int64_t info = d[7];
-            const int rows = (int)d[2];
-            const int cols = (int)d[3];
-            const int mode = (int)d[4];
-            const int in_off = (int)d[5];
-            const int out_off = (int)d[6];
-            const bool direct = (info & kPiDirect) != 0;
-            // group change?
+        if (prof) {
+            const long long t1 = clock64();
+            pr[kind * 8 + 3] += t1 - t0;
+            t0 = t1;
+        }
+        for (int i = 0; i < pc_e - pc_b; ++i) {
+            const int4 c = get_piece(p, S, pc_b, i);
+            const int rows = c.x >> 16, cols = c.x & 0xFFFF;
+            const int in_off = c.y, out_off = c.z;
+            const int mode = (c.w >> 16) & 0xF;
+            const bool direct = (c.w & kCDirect) != 0;
             if (mode == kModeN ? (g_mode != kModeN)
                                : (g_mode != mode || g_out != out_off || g_cols != cols)) {
                 const bool to_h = (g_mode == kModeN) && mode != kModeN;
@@ -375,22 +466,24 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 g_cols = cols;
             }
             const double2* tile = nullptr;
-            if (prof) {
-                const long long t1 = clock64();
-                c_ovh += t1 - t0;
-                t0 = t1;
-                ++n_pcs;
-            }
             if (!direct) {
-                if (info & kPiBegin) mbar_wait(&full[stage], sphase);
-                if (prof) {
-                    const long long t1 = clock64();
-                    c_data += t1 - t0;
-                    t0 = t1;
+                if (c.w & kCBegin) {
+                    if (prof) {
+                        const long long t1 = clock64();
+                        pr[kind * 8 + 2] += t1 - t0;
+                        t0 = t1;
+                    }
+                    mbar_wait(&full[stage], sphase);
+                    if (prof) {
+                        const long long t1 = clock64();
+                        pr[kind * 8 + 0] += t1 - t0;
+                        t0 = t1;
+                    }
                 }
                 tile = reinterpret_cast<const double2*>(stages + (size_t)stage * kStageBytes) +
-                       (info & 0xFFFFFF);
+                       (c.w & 0xFFFF);
             }
+            if (prof) pr[kind * 8 + 4] += 1;
             if (mode == kModeN) {
                 const double2* xv = xin + in_off;
                 int r0 = (rg - (out_off % kRowGroups)) % kRowGroups;
@@ -410,16 +503,16 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     if (nreg) {
                         const int k = o / kRowGroups;
 #pragma unroll
-                        for (int q = 0; q < kSlots; ++q)
-                            if (q == k) {
-                                accr[q] += ar;
-                                acci[q] += ai;
+                        for (int s = 0; s < kSlots; ++s)
+                            if (s == k) {
+                                accr[s] += ar;
+                                acci[s] += ai;
                             }
                     } else {  // wide N op: reduce and add per row
 #pragma unroll
-                        for (int s2 = 1; s2 < kLanesPerRow; s2 <<= 1) {
-                            ar += __shfl_xor_sync(gmask, ar, s2);
-                            ai += __shfl_xor_sync(gmask, ai, s2);
+                        for (int s = 1; s < kLanesPerRow; s <<= 1) {
+                            ar += __shfl_xor_sync(gmask, ar, s);
+                            ai += __shfl_xor_sync(gmask, ai, s);
                         }
                         if (g == 0) {
                             double2 v = outv[o];
@@ -435,6 +528,12 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 const int pp = tid % P;
                 int j0 = (tid / P - (out_off % nJ)) % nJ;
                 if (j0 < 0) j0 += nJ;
+                int64_t dm = 0, dld = 0;
+                if (direct) {
+                    const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
+                    dm = __ldg(d + 0);
+                    dld = __ldg(d + 1);
+                }
 #pragma unroll
                 for (int k = 0; k < kSlots; ++k) {
                     if (k * nJ >= cols) break;
@@ -442,11 +541,10 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     if (j >= cols) continue;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
                     if (mode == kModeS) {
-                        const int64_t ld = d[1];
-                        const double2* W = p.work + d[0] + j;
+                        const double2* W = p.work + dm + j;
 #pragma unroll 4
                         for (int r = pp; r < rows; r += P) {
-                            const double2 m = __ldcg(W + (int64_t)r * ld);
+                            const double2 m = __ldcg(W + (int64_t)r * dld);
                             ar += m.x;
                             ai += m.y;
                         }
@@ -463,12 +561,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     acci[k] += ai + bi;
                 }
             }
-            if (prof) {
-                const long long t1 = clock64();
-                c_comp += t1 - t0;
-                t0 = t1;
-            }
-            if (!direct && (info & kPiEnd)) {
+            if (!direct && (c.w & kCEnd)) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
                 if (++stage == p.nstage) {
@@ -479,59 +572,54 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         }
         flush();
         consumer_sync();
-        for (int r = out_b; r < out_e; ++r) {
-            const int64_t* rd = p.runs + (int64_t)r * kRunFields;
-            const int buf = (int)__ldg(rd + 0);
-            const int64_t off = __ldg(rd + 1);
-            const int len = (int)__ldg(rd + 2);
-            const int dst = (int)__ldg(rd + 3);
-            const int flags = (int)__ldg(rd + 4);
-            const int add = flags & 1;
-            double2* dp = (buf == kBufW ? p.w : p.work) + off;
+        if (prof) {
+            const long long t1 = clock64();
+            pr[kind * 8 + 2] += t1 - t0;
+            t0 = t1;
+        }
+        // scatter the output vector
+        for (int pos = tid; pos < n_out; pos += kConsumers) {
+            const RunRef R = get_run(p, S, in_b, find_run(p, S, in_b, n_in_runs, n_runs, pos));
+            const int buf = R.bf & 0xFF, flags = R.bf >> 8;
+            double2* dp = (buf == kBufW ? p.w : p.work) + R.off + (pos - R.dst);
+            const double2 v = outv[pos];
             if (flags & 2) {  // fp64 red.add into the pre-zeroed output (<= 2 addends per entry)
-                for (int i = tid; i < len; i += kConsumers) {
-                    const double2 v = outv[dst + i];
-                    atomicAdd(&dp[i].x, v.x);
-                    atomicAdd(&dp[i].y, v.y);
-                }
-                continue;
-            }
-            for (int i = tid; i < len; i += kConsumers) {
-                double2 v = outv[dst + i];
-                if (add) {
-                    const double2 o = __ldcg(dp + i);
-                    v.x += o.x;
-                    v.y += o.y;
-                }
-                __stcg(dp + i, v);
+                atomicAdd(&dp->x, v.x);
+                atomicAdd(&dp->y, v.y);
+            } else if (flags & 1) {
+                const double2 o = __ldcg(dp);
+                __stcg(dp, make_double2(v.x + o.x, v.y + o.y));
+            } else {
+                __stcg(dp, v);
             }
         }
-        if (prof) c_ovh += clock64() - t0;
-        if (!p.skip_waits) {
-            consumer_sync();
-            if (tid == 0) {
-                const int sb = __ldg(hp + 10), se = __ldg(hp + 11);
-                if (se > sb) {
-                    __threadfence();
-                    for (int i = sb; i < se; ++i) atomicAdd(p.counters + __ldg(p.sigs + i), 1u);
-                }
-            }
+        const int sb = S->hdr[10], se = S->hdr[11];
+        consumer_sync();  // all outputs issued; the slot is no longer read
+        if (lane == 0) mbar_arrive(&opempty[q]);
+        if (tid == 0 && !p.skip_waits && se > sb) {
+            __threadfence();
+            for (int i2 = sb; i2 < se; ++i2) red_release_add(p.counters + __ldg(p.sigs + i2), 1u);
         }
+        if (++q == kOpSlots) {
+            q = 0;
+            qphase ^= 1u;
+        }
+        if (prof) pr[kind * 8 + 3] += clock64() - t0;
     }
 }
 
-__global__ void __launch_bounds__(kThreads) uhmv_bulk_kernel(const Params p) {
+__global__ void __launch_bounds__(kThreads, 3) uhmv_bulk_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.xin_max, p.out_max);
     unsigned char* stages = smem + L.stage_off;
     double2* xin = reinterpret_cast<double2*>(smem + L.xin_off);
     double2* outv = reinterpret_cast<double2*>(smem + L.out_off);
-    int64_t* pdesc = reinterpret_cast<int64_t*>(smem + L.desc_off);
+    OpSlot* slots = reinterpret_cast<OpSlot*>(smem + L.slot_off);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bar_off);
     uint64_t* empty = full + p.nstage;
     uint64_t* opfull = empty + p.nstage;
     uint64_t* opempty = opfull + kOpSlots;
-    int* slots = reinterpret_cast<int*>(smem + L.slot_off);
+    int* flag = reinterpret_cast<int*>(opempty + kOpSlots);
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.nstage; ++s) {
             mbar_init(&full[s], 1);
@@ -548,17 +636,17 @@ __global__ void __launch_bounds__(kThreads) uhmv_bulk_kernel(const Params p) {
     if (warp == kConsumerWarps) {
         producer(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer(p, stages, xin, outv, pdesc, full, empty, opfull, opempty, slots);
+        consumer(p, stages, xin, outv, full, empty, opfull, opempty, slots);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch
     if (threadIdx.x == 0) {
         __threadfence();
         const uint32_t prev = atomicAdd(p.exit_count, 1u);
-        slots[8] = (prev == gridDim.x - 1) ? 1 : 0;
+        flag[0] = (prev == gridDim.x - 1) ? 1 : 0;
     }
     __syncthreads();
-    if (slots[8]) {
+    if (flag[0]) {
         __threadfence();
         for (int i = threadIdx.x; i < p.n_counters; i += kThreads) p.counters[i] = 0u;
         if (threadIdx.x == 0) {

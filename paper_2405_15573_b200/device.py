@@ -145,7 +145,7 @@ class DeviceOperator:
         return them summed over CTAs (see include/uhmv.h uhmv_plan_set_profile)."""
         torch = self.torch
         grid = self.launch_info(adjoint, mode)["grid"]
-        buf = torch.zeros((grid, 8), dtype=torch.int64, device=self.device)
+        buf = torch.zeros((grid, 64), dtype=torch.int64, device=self.device)
         _lib.check(_lib.lib().uhmv_plan_set_profile(self._plan, ctypes.c_void_p(buf.data_ptr())), "set_profile")
         p = self.packed
         n_in = p.n_rows if adjoint else p.n_cols
@@ -153,9 +153,16 @@ class DeviceOperator:
         self.matvec(x, adjoint=adjoint, mode=mode)
         torch.cuda.synchronize(self.device)
         _lib.check(_lib.lib().uhmv_plan_set_profile(self._plan, None), "set_profile")
-        names = ["c_wait_data", "c_wait_dep", "c_compute", "c_overhead", "p_wait_stage", "p_wait_slot", "ops", "pieces"]
+        from .packer import KIND_NAMES
+
         tot = buf.sum(dim=0).tolist()
-        return {"grid": grid, **{k: v for k, v in zip(names, tot)}}
+        out = {"grid": grid, "p_wait_stage": tot[56], "p_wait_slot": tot[57], "kinds": {}}
+        cats = ["wait_data", "wait_dep", "compute", "overhead", "pieces", "ops"]
+        for k, name in enumerate(KIND_NAMES):
+            row = tot[k * 8 : k * 8 + 6]
+            if row[5]:
+                out["kinds"][name] = dict(zip(cats, row))
+        return out
 
     # ---- execution ----
     def _stream(self, stream):

@@ -13,10 +13,14 @@ L = d.get('launch') or {}
 s += ' grid %s st %s smem %s' % (L.get('grid'), L.get('stages'), L.get('smem_bytes'))
 c = d.get('engine_cycles')
 if c:
-    tot = c['c_wait_data'] + c['c_wait_dep'] + c['c_compute'] + c['c_overhead']
-    s += ' | cons data %.2f dep %.2f comp %.2f ovh %.2f | prod stage %.2f slot %.2f | ops %d pcs %d' % (
-        c['c_wait_data'] / tot, c['c_wait_dep'] / tot, c['c_compute'] / tot, c['c_overhead'] / tot,
-        c['p_wait_stage'] / tot, c['p_wait_slot'] / tot, c['ops'], c['pieces'])
+    ks = c['kinds']
+    tot = sum(v['wait_data'] + v['wait_dep'] + v['compute'] + v['overhead'] for v in ks.values())
+    s += ' | prod stage %.2f slot %.2f' % (c['p_wait_stage'] / tot, c['p_wait_slot'] / tot)
+    for name, v in ks.items():
+        t = v['wait_data'] + v['wait_dep'] + v['compute'] + v['overhead']
+        s += ' | %s %.2f: data %.2f dep %.2f comp %.2f ovh %.2f cyc/op %.0f' % (
+            name, t / tot, v['wait_data'] / t, v['wait_dep'] / t, v['compute'] / t, v['overhead'] / t,
+            t / max(v['ops'], 1) / (d['launch']['grid'] and 1))
 print(s)
 PY
 )"
