@@ -430,6 +430,7 @@ struct uhmv_plan {
     int sm_count;
     int debug_skip_waits;  // diagnostics only (UHMV_DEBUG_SKIP_WAITS): results are wrong
     unsigned long long* prof;  // diagnostics only (uhmv_plan_set_profile)
+    int debug_flags;           // diagnostics only (UHMV_DEBUG_FLAGS): results are wrong
 };
 
 extern "C" {
@@ -555,6 +556,7 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         p->bulk_grid[k] = grid;
     }
     if (const char* ev = getenv("UHMV_DEBUG_SKIP_WAITS")) p->debug_skip_waits = atoi(ev);
+    if (const char* ev = getenv("UHMV_DEBUG_FLAGS")) p->debug_flags = atoi(ev);
     *out = p;
     return UHMV_OK;
 }
@@ -582,6 +584,7 @@ static bulk::Params make_bulk_params(const uhmv_plan* plan, const uhmv_program& 
     bp.out_max = pr.out_max;
     bp.skip_waits = plan->debug_skip_waits;
     bp.prof = plan->prof;
+    bp.dbg = plan->debug_flags;
     return bp;
 }
 

@@ -79,6 +79,7 @@ struct Params {
     int32_t xin_max;
     int32_t out_max;
     int32_t skip_waits;        // diagnostics: ignore dependencies (results are wrong)
+    int32_t dbg;               // diagnostics: 1 skip compute, 2 skip gather/scatter (wrong results)
     unsigned long long* prof;  // optional [grid][64] cycle counters, else null
 };
 
@@ -87,7 +88,7 @@ struct Params {
 // [56] producer waiting for a free stage, [57] producer waiting for a free op slot.
 
 struct Layout {
-    int stage_off, xin_off, out_off, slot_off, bar_off, total;
+    int stage_off, xin_off, out_off, slot_off, bar_off, prof_off, total;
 };
 
 __host__ __device__ inline Layout layout(int nstage, int xin_max, int out_max) {
@@ -97,7 +98,8 @@ __host__ __device__ inline Layout layout(int nstage, int xin_max, int out_max) {
     L.out_off = L.xin_off + ((xin_max * 16 + 127) & ~127);
     L.slot_off = L.out_off + ((out_max * 16 + 127) & ~127);
     L.bar_off = L.slot_off + kOpSlots * (int)sizeof(OpSlot);
-    L.total = L.bar_off + (2 * nstage + 2 * kOpSlots) * 8 + 16;
+    L.prof_off = L.bar_off + (2 * nstage + 2 * kOpSlots) * 8 + 16;
+    L.total = L.prof_off + 64 * 8;
     return L;
 }
 
@@ -331,7 +333,8 @@ __device__ __forceinline__ int4 get_piece(const Params& p, const OpSlot* S, int 
 
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
                                          double2* outv, uint64_t* full, uint64_t* empty,
-                                         uint64_t* opfull, uint64_t* opempty, OpSlot* slots) {
+                                         uint64_t* opfull, uint64_t* opempty, OpSlot* slots,
+                                         unsigned long long* sprof) {
     const int tid = threadIdx.x;  // 0..127
     const int lane = tid & 31;
     const int g = tid & (kLanesPerRow - 1);
@@ -342,13 +345,17 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     int q = 0;
     uint32_t qphase = 0;
     const bool prof = p.prof != nullptr && tid == 0;
-    unsigned long long* pr = prof ? p.prof + (size_t)blockIdx.x * 64 : nullptr;
+    unsigned long long* pr = prof ? sprof : nullptr;
     for (;;) {
         long long t0 = prof ? clock64() : 0;
         mbar_wait(&opfull[q], qphase);
         const OpSlot* S = slots + q;
         const int op = S->op;
-        if (op < 0) break;
+        if (op < 0) {
+            if (prof)
+                for (int i = 0; i < 56; ++i) p.prof[(size_t)blockIdx.x * 64 + i] = sprof[i];
+            break;
+        }
         const int n_out = S->hdr[1];
         const int in_b = S->hdr[2], in_e = S->hdr[3];
         const int out_e = S->hdr[7];
@@ -372,7 +379,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             pr[kind * 8 + 5] += 1;
         }
         // gather the input vector: all loads of a batch issued before any smem store
-        const int n_in = S->hdr[0];
+        const int n_in = (p.dbg & 2) ? 0 : S->hdr[0];
         for (int base = 0; base < n_in; base += kGatherBatch * kConsumers) {
             double2 v[kGatherBatch];
 #pragma unroll
@@ -484,7 +491,9 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                        (c.w & 0xFFFF);
             }
             if (prof) pr[kind * 8 + 4] += 1;
-            if (mode == kModeN) {
+            if (p.dbg & 1) {
+                // diagnostics: no compute
+            } else if (mode == kModeN) {
                 const double2* xv = xin + in_off;
                 int r0 = (rg - (out_off % kRowGroups)) % kRowGroups;
                 if (r0 < 0) r0 += kRowGroups;
@@ -578,7 +587,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             t0 = t1;
         }
         // scatter the output vector
-        for (int pos = tid; pos < n_out; pos += kConsumers) {
+        for (int pos = tid; pos < ((p.dbg & 2) ? 0 : n_out); pos += kConsumers) {
             const RunRef R = get_run(p, S, in_b, find_run(p, S, in_b, n_in_runs, n_runs, pos));
             const int buf = R.bf & 0xFF, flags = R.bf >> 8;
             double2* dp = (buf == kBufW ? p.w : p.work) + R.off + (pos - R.dst);
@@ -620,6 +629,8 @@ __global__ void __launch_bounds__(kThreads, 3) uhmv_bulk_kernel(const Params p) 
     uint64_t* opfull = empty + p.nstage;
     uint64_t* opempty = opfull + kOpSlots;
     int* flag = reinterpret_cast<int*>(opempty + kOpSlots);
+    unsigned long long* sprof = reinterpret_cast<unsigned long long*>(smem + L.prof_off);
+    if (threadIdx.x < 64) sprof[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.nstage; ++s) {
             mbar_init(&full[s], 1);
@@ -636,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 3) uhmv_bulk_kernel(const Params p) 
     if (warp == kConsumerWarps) {
         producer(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer(p, stages, xin, outv, full, empty, opfull, opempty, slots);
+        consumer(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch
