@@ -514,8 +514,8 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     // bulk engine: as many 16-KiB stages as fit with the requested CTAs per SM
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, desc->device);
-    int want_ctas = 3;
-    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 3;
+    int want_ctas = 2;
+    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 2;
     int want_stages = 0;
     if (const char* ev = getenv("UHMV_NSTAGE")) want_stages = atoi(ev);
     int bulk_need = 0;
@@ -536,15 +536,18 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         delete p;
         return fail(UHMV_EINVAL, "bulk engine shared memory exceeds the opt-in limit");
     }
-    e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem_optin);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel<true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaFuncSetAttribute(bulk)");
     }
     for (int k = 0; k < 2; ++k) {
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk::uhmv_bulk_kernel,
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk::uhmv_bulk_kernel<false>,
                                                           bulk::kThreads, p->bulk_smem[k]);
         if (e != cudaSuccess) {
             delete p;
@@ -657,8 +660,12 @@ int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode,
     if (mode == UHMV_MODE_BULK) {
         if (!pr.pieces) return fail(UHMV_EINVAL, "bulk mode needs the piece table");
         bulk::Params bp = make_bulk_params(plan, pr, k, x, w);
-        bulk::uhmv_bulk_kernel<<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k],
-                                 static_cast<cudaStream_t>(stream)>>>(bp);
+        if (bp.prof)
+            bulk::uhmv_bulk_kernel<true><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k],
+                                           static_cast<cudaStream_t>(stream)>>>(bp);
+        else
+            bulk::uhmv_bulk_kernel<false><<<plan->bulk_grid[k], bulk::kThreads,
+                                            plan->bulk_smem[k], static_cast<cudaStream_t>(stream)>>>(bp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "uhmv_bulk_kernel launch");
         return UHMV_OK;

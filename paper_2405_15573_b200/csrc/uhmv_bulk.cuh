@@ -31,7 +31,7 @@ namespace bulk {
 constexpr int kConsumerWarps = 4;
 constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
-constexpr int kStageElems = 1024;                // = packer.STAGE_ELEMS (16 KiB of complex128)
+constexpr int kStageElems = 1280;                // = packer.STAGE_ELEMS (20 KiB of complex128)
 constexpr int kStageBytes = kStageElems * 16;
 constexpr int kOpSlots = 2;
 constexpr int kLanesPerRow = 8;
@@ -154,6 +154,7 @@ __device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64
     return c;
 }
 
+template <bool PROF>
 __device__ __forceinline__ void producer(const Params& p, unsigned char* stages, uint64_t* full,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
                                          OpSlot* slots) {
@@ -165,7 +166,7 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
     int q = 0;
     uint32_t qphase = 0;
     unsigned long long c_empty = 0, c_slot = 0;
-    const bool prof = p.prof != nullptr && lane == 0;
+    const bool prof = PROF && lane == 0;
     unsigned long long t_next = 0;
     if (lane == 0) t_next = atomicAdd(p.ticket, 1ull);
     t_next = __shfl_sync(0xffffffffu, t_next, 0);
@@ -331,6 +332,7 @@ __device__ __forceinline__ int4 get_piece(const Params& p, const OpSlot* S, int 
                           __ldg(d + 7));
 }
 
+template <bool PROF>
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
                                          double2* outv, uint64_t* full, uint64_t* empty,
                                          uint64_t* opfull, uint64_t* opempty, OpSlot* slots,
@@ -344,7 +346,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     uint32_t sphase = 0;
     int q = 0;
     uint32_t qphase = 0;
-    const bool prof = p.prof != nullptr && tid == 0;
+    const bool prof = PROF && tid == 0;
     unsigned long long* pr = prof ? sprof : nullptr;
     for (;;) {
         long long t0 = prof ? clock64() : 0;
@@ -498,25 +500,41 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 int r0 = (rg - (out_off % kRowGroups)) % kRowGroups;
                 if (r0 < 0) r0 += kRowGroups;
                 for (int r = r0; r < rows; r += kRowGroups) {
-                    const double2* T = tile + r * cols;
+                    const double2* T = tile + r * cols + g;
+                    const double2* X = xv + g;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
                     int j = g;
-                    for (; j + kLanesPerRow < cols; j += 2 * kLanesPerRow) {  // two chains
-                        cmac(ar, ai, T[j], xv[j]);
-                        cmac(br, bi, T[j + kLanesPerRow], xv[j + kLanesPerRow]);
+                    for (; j + 3 * kLanesPerRow < cols; j += 4 * kLanesPerRow) {  // 4 loads in flight
+                        const double2 t0 = T[0], t1 = T[8], t2 = T[16], t3 = T[24];
+                        const double2 x0 = X[0], x1 = X[8], x2 = X[16], x3 = X[24];
+                        cmac(ar, ai, t0, x0);
+                        cmac(br, bi, t1, x1);
+                        cmac(ar, ai, t2, x2);
+                        cmac(br, bi, t3, x3);
+                        T += 32;
+                        X += 32;
                     }
-                    if (j < cols) cmac(ar, ai, T[j], xv[j]);
+                    for (; j < cols; j += kLanesPerRow) {
+                        cmac(ar, ai, T[0], X[0]);
+                        T += 8;
+                        X += 8;
+                    }
                     ar += br;
                     ai += bi;
                     const int o = out_off + r;
                     if (nreg) {
                         const int k = o / kRowGroups;
+                        if (k == 0) {
+                            accr[0] += ar;
+                            acci[0] += ai;
+                        } else {
 #pragma unroll
-                        for (int s = 0; s < kSlots; ++s)
-                            if (s == k) {
-                                accr[s] += ar;
-                                acci[s] += ai;
-                            }
+                            for (int s = 1; s < kSlots; ++s)
+                                if (s == k) {
+                                    accr[s] += ar;
+                                    acci[s] += ai;
+                                }
+                        }
                     } else {  // wide N op: reduce and add per row
 #pragma unroll
                         for (int s = 1; s < kLanesPerRow; s <<= 1) {
@@ -617,7 +635,8 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) uhmv_bulk_kernel(const Params p) {
+template <bool PROF>
+__global__ void __launch_bounds__(kThreads, 2) uhmv_bulk_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.xin_max, p.out_max);
     unsigned char* stages = smem + L.stage_off;
@@ -645,9 +664,9 @@ __global__ void __launch_bounds__(kThreads, 3) uhmv_bulk_kernel(const Params p) 
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     if (warp == kConsumerWarps) {
-        producer(p, stages, full, empty, opfull, opempty, slots);
+        producer<PROF>(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
+        consumer<PROF>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch
