@@ -28,7 +28,7 @@
 
 namespace bulk {
 
-constexpr int kConsumerWarps = 4;
+constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
 constexpr int kStageElems = 1280;                // = packer.STAGE_ELEMS (20 KiB of complex128)
@@ -37,7 +37,7 @@ constexpr int kOpSlots = 2;
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
 constexpr int kPieceFields = 8;
-constexpr int kSlots = 8;         // register accumulator slots per thread
+constexpr int kSlots = 4;         // register accumulator slots per thread
 constexpr int kSlotRuns = 48;     // run descriptors cached per op slot
 constexpr int kSlotPieces = 128;  // piece descriptors cached per op slot
 constexpr int kGatherBatch = 8;   // loads in flight per thread in the gather
@@ -183,52 +183,26 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
         const int out_e = __shfl_sync(0xffffffffu, hv, 7);
         const int pc_b = __shfl_sync(0xffffffffu, hv, 13);
         const int pc_e = __shfl_sync(0xffffffffu, hv, 14);
-        // prefetch the run table and the first kSlotPieces piece descriptors
-        int64_t roff[2];
-        int rlen[2], rdst[2], rbf[2];
-        const int n_runs = op >= 0 ? out_e - in_b : 0;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int r = lane + 32 * k;
-            if (r < n_runs && r < kSlotRuns) {
-                const int64_t* rd = p.runs + (int64_t)(in_b + r) * kRunFields;
-                roff[k] = __ldg(rd + 1);
-                rlen[k] = (int)__ldg(rd + 2);
-                rdst[k] = (int)__ldg(rd + 3);
-                rbf[k] = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
-            }
-        }
-        int4 cp[kSlotPieces / 32];
-        const int n_pc = op >= 0 ? pc_e - pc_b : 0;
-#pragma unroll
-        for (int k = 0; k < kSlotPieces / 32; ++k) {
-            const int i = lane + 32 * k;
-            if (i < n_pc) {
-                const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
-                cp[k] = compress_piece(__ldg(d + 2), __ldg(d + 3), __ldg(d + 4), __ldg(d + 5),
-                                       __ldg(d + 6), __ldg(d + 7));
-            }
-        }
         const long long tq = prof ? clock64() : 0;
         mbar_wait(&opempty[q], qphase ^ 1u);
         if (prof) c_slot += clock64() - tq;
+        // fill the op slot: header, run table, first kSlotPieces compressed piece descriptors
         OpSlot* S = slots + q;
         if (lane < 16) S->hdr[lane] = hv;
         if (lane == 0) S->op = op;
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int r = lane + 32 * k;
-            if (r < n_runs && r < kSlotRuns) {
-                S->roff[r] = roff[k];
-                S->rlen[r] = rlen[k];
-                S->rdst[r] = rdst[k];
-                S->rbf[r] = rbf[k];
-            }
+        const int n_runs = op >= 0 ? out_e - in_b : 0;
+        for (int r = lane; r < n_runs && r < kSlotRuns; r += 32) {
+            const int64_t* rd = p.runs + (int64_t)(in_b + r) * kRunFields;
+            S->roff[r] = __ldg(rd + 1);
+            S->rlen[r] = (int)__ldg(rd + 2);
+            S->rdst[r] = (int)__ldg(rd + 3);
+            S->rbf[r] = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
         }
-#pragma unroll
-        for (int k = 0; k < kSlotPieces / 32; ++k) {
-            const int i = lane + 32 * k;
-            if (i < n_pc) S->pc[i] = cp[k];
+        const int n_pc = op >= 0 ? pc_e - pc_b : 0;
+        for (int i = lane; i < n_pc && i < kSlotPieces; i += 32) {
+            const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
+            S->pc[i] = compress_piece(__ldg(d + 2), __ldg(d + 3), __ldg(d + 4), __ldg(d + 5),
+                                      __ldg(d + 6), __ldg(d + 7));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&opfull[q]);  // release: the slot writes above are visible
@@ -636,7 +610,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
 }
 
 template <bool PROF>
-__global__ void __launch_bounds__(kThreads, 2) uhmv_bulk_kernel(const Params p) {
+__global__ void __maxnreg__(112) uhmv_bulk_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.xin_max, p.out_max);
     unsigned char* stages = smem + L.stage_off;

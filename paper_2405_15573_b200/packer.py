@@ -67,7 +67,7 @@ KIND_NAMES = ["P1", "NEAR", "RED", "U", "Z", "FAR", "ZERO"]
 
 ALIGN = 8  # complex128 elements per 128 B
 HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
-ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op (= consumer row-groups: one row each)
+ROWS_PER_CHUNK = 32  # output rows per NEAR/FAR op (= consumer row-groups: one row each)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1280  # complex128 per shared-memory stage (20 KiB: one 16 x 80 dense chunk)
 
