@@ -20,6 +20,7 @@ from paper_2405_15573_b200.packer import (
     MODE_S,
     PI_DIRECT,
     PI_XGLOBAL,
+    PI_XSTAGE,
     RUN_ADD,
     RUN_ATOMIC,
 )
@@ -36,7 +37,7 @@ def _segments(prog, i, engine):
     else:
         for m_off, ld, rows, cols, mode, in_off, out_off, info in prog.pieces[prog.ops[i, 13] : prog.ops[i, 14]]:
             buf = BUF_WORK if info & PI_DIRECT else BUF_ARENA
-            yield (m_off, buf, rows, cols, ld, mode, in_off, out_off, bool(info & PI_XGLOBAL))
+            yield (m_off, buf, rows, cols, ld, mode, in_off, out_off, bool(info & (PI_XGLOBAL | PI_XSTAGE)))
 
 
 def run_op(prog, i, bufs, engine="segs"):

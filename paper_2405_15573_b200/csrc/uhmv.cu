@@ -514,8 +514,8 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     // bulk engine: as many 16-KiB stages as fit with the requested CTAs per SM
     int smem_sm = 0;
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, desc->device);
-    int want_ctas = 2;
-    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 2;
+    int want_ctas = 3;
+    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 3;
     int want_stages = 0;
     if (const char* ev = getenv("UHMV_NSTAGE")) want_stages = atoi(ev);
     int bulk_need = 0;

@@ -28,10 +28,10 @@
 
 namespace bulk {
 
-constexpr int kConsumerWarps = 8;
+constexpr int kConsumerWarps = 4;
 constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
-constexpr int kStageElems = 1280;                // = packer.STAGE_ELEMS (20 KiB of complex128)
+constexpr int kStageElems = 1408;                // = packer.STAGE_ELEMS (22 KiB of complex128)
 constexpr int kStageBytes = kStageElems * 16;
 constexpr int kOpSlots = 2;
 constexpr int kLanesPerRow = 8;
@@ -41,12 +41,13 @@ constexpr int kSlots = 4;         // register accumulator slots per thread
 constexpr int kSlotRuns = 48;     // run descriptors cached per op slot
 constexpr int kSlotPieces = 128;  // piece descriptors cached per op slot
 constexpr int kGatherBatch = 8;   // loads in flight per thread in the gather
-constexpr int64_t kPiBegin = 1ll << 24, kPiEnd = 1ll << 25, kPiDirect = 1ll << 26;
+constexpr int64_t kPiBegin = 1ll << 24, kPiEnd = 1ll << 25, kPiDirect = 1ll << 26,
+                  kPiXStage = 1ll << 28;
 
 // compressed consumer-side piece descriptor (int4):
 //   x = rows << 16 | cols, y = in_off, z = out_off,
-//   w = smem_off | mode << 16 | begin << 20 | end << 21 | direct << 22
-constexpr int kCBegin = 1 << 20, kCEnd = 1 << 21, kCDirect = 1 << 22;
+//   w = smem_off | mode << 16 | begin << 20 | end << 21 | direct << 22 | xstage << 23
+constexpr int kCBegin = 1 << 20, kCEnd = 1 << 21, kCDirect = 1 << 22, kCXStage = 1 << 23;
 
 struct OpSlot {
     int hdr[16];
@@ -150,7 +151,8 @@ __device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64
     c.y = (int)in_off;
     c.z = (int)out_off;
     c.w = (int)((info & 0xFFFF) | (mode << 16) | ((info & kPiBegin) ? kCBegin : 0) |
-                ((info & kPiEnd) ? kCEnd : 0) | ((info & kPiDirect) ? kCDirect : 0));
+                ((info & kPiEnd) ? kCEnd : 0) | ((info & kPiDirect) ? kCDirect : 0) |
+                ((info & kPiXStage) ? kCXStage : 0));
     return c;
 }
 
@@ -159,8 +161,9 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
                                          OpSlot* slots) {
     const int lane = threadIdx.x & 31;
-    uint64_t policy;
+    uint64_t policy, policy_keep;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(policy_keep));
     int stage = 0;
     uint32_t sphase = 0;
     int q = 0;
@@ -219,13 +222,15 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
         }
         for (int base = pc_b; base < pc_e; base += 32) {
             const int nb = min(32, pc_e - base);
-            int64_t f0 = 0, f1 = 0, f7 = kPiDirect;
-            int rc = 0;
+            int64_t f0 = 0, f1 = 0, f7 = kPiDirect, f5 = 0;
+            int rc = 0, md = 0;
             if (lane < nb) {
                 const int64_t* d = p.pieces + (int64_t)(base + lane) * kPieceFields;
                 f0 = __ldg(d + 0);
                 f1 = __ldg(d + 1);
                 rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));
+                md = (int)__ldg(d + 4);
+                f5 = __ldg(d + 5);
                 f7 = __ldg(d + 7);
             }
             for (int k = 0; k < nb; ++k) {
@@ -235,6 +240,8 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 const int64_t ld = __shfl_sync(0xffffffffu, f1, k);
                 const int rcv = __shfl_sync(0xffffffffu, rc, k);
                 const int rows = rcv >> 16, cols = rcv & 0xFFFF;
+                const int pmode = __shfl_sync(0xffffffffu, md, k);
+                const int64_t xo = __shfl_sync(0xffffffffu, f5, k);
                 if (info & kPiBegin) {
                     const long long te = prof ? clock64() : 0;
                     mbar_wait(&empty[stage], sphase ^ 1u);
@@ -252,6 +259,11 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                         for (int r = 0; r < rows; ++r)
                             bulk_g2s(dst + (size_t)r * cols * 16, src + (int64_t)r * ld,
                                      (uint32_t)cols * 16, &full[stage], policy);
+                    }
+                    if (info & kPiXStage) {  // the piece's x window, right behind its rows
+                        const int w = (pmode == kModeN) ? cols : rows;
+                        bulk_g2s(dst + (size_t)rows * cols * 16, p.x + xo, (uint32_t)w * 16,
+                                 &full[stage], policy_keep);
                     }
                 }
                 if (info & kPiEnd) {
@@ -355,7 +367,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             pr[kind * 8 + 5] += 1;
         }
         // gather the input vector: all loads of a batch issued before any smem store
-        const int n_in = (p.dbg & 2) ? 0 : S->hdr[0];
+        const int n_in = (p.dbg & 2) ? 0 : S->hdr[15];  // work inputs only (x rides in stages)
         for (int base = 0; base < n_in; base += kGatherBatch * kConsumers) {
             double2 v[kGatherBatch];
 #pragma unroll
@@ -470,21 +482,22 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             if (p.dbg & 1) {
                 // diagnostics: no compute
             } else if (mode == kModeN) {
-                const double2* xv = xin + in_off;
+                const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
                 int r0 = (rg - (out_off % kRowGroups)) % kRowGroups;
                 if (r0 < 0) r0 += kRowGroups;
                 for (int r = r0; r < rows; r += kRowGroups) {
                     const double2* T = tile + r * cols + g;
                     const double2* X = xv + g;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+                    double cr = 0.0, ci = 0.0, dr = 0.0, di = 0.0;
                     int j = g;
-                    for (; j + 3 * kLanesPerRow < cols; j += 4 * kLanesPerRow) {  // 4 loads in flight
+                    for (; j + 3 * kLanesPerRow < cols; j += 4 * kLanesPerRow) {  // 4 chains
                         const double2 t0 = T[0], t1 = T[8], t2 = T[16], t3 = T[24];
                         const double2 x0 = X[0], x1 = X[8], x2 = X[16], x3 = X[24];
                         cmac(ar, ai, t0, x0);
                         cmac(br, bi, t1, x1);
-                        cmac(ar, ai, t2, x2);
-                        cmac(br, bi, t3, x3);
+                        cmac(cr, ci, t2, x2);
+                        cmac(dr, di, t3, x3);
                         T += 32;
                         X += 32;
                     }
@@ -493,8 +506,8 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                         T += 8;
                         X += 8;
                     }
-                    ar += br;
-                    ai += bi;
+                    ar += br + (cr + dr);
+                    ai += bi + (ci + di);
                     const int o = out_off + r;
                     if (nreg) {
                         const int k = o / kRowGroups;
@@ -550,7 +563,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                             ai += m.y;
                         }
                     } else {
-                        const double2* xv = xin + in_off;
+                        const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
                         int r = pp;
                         for (; r + P < rows; r += 2 * P) {  // two independent chains
                             cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
@@ -610,7 +623,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
 }
 
 template <bool PROF>
-__global__ void __maxnreg__(112) uhmv_bulk_kernel(const Params p) {
+__global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.xin_max, p.out_max);
     unsigned char* stages = smem + L.stage_off;

@@ -59,17 +59,18 @@ RUN_FIELDS = 5  # int64: buf, off, len, dst, flags
 PIECE_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_off, out_off, info
 # piece info bits: [0,24) smem element offset in its stage, 24 stage_begin, 25 stage_end,
 # 26 direct (no stage: coherent loads from the work buffer), 27 input read from x directly,
+# 28 x window carried in the stage behind the matrix rows (in_off = its x index),
 # [32,56) elements of the stage (on stage_begin pieces)
-PI_BEGIN, PI_END, PI_DIRECT, PI_XGLOBAL = 1 << 24, 1 << 25, 1 << 26, 1 << 27
+PI_BEGIN, PI_END, PI_DIRECT, PI_XGLOBAL, PI_XSTAGE = 1 << 24, 1 << 25, 1 << 26, 1 << 27, 1 << 28
 
 KIND_P1, KIND_NEAR, KIND_RED, KIND_U, KIND_Z, KIND_FAR, KIND_ZERO = range(7)
 KIND_NAMES = ["P1", "NEAR", "RED", "U", "Z", "FAR", "ZERO"]
 
 ALIGN = 8  # complex128 elements per 128 B
 HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
-ROWS_PER_CHUNK = 32  # output rows per NEAR/FAR op (= consumer row-groups: one row each)
+ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op (= consumer row-groups: one row each)
 P1_CHUNK = 256  # max input rows per P1 op
-STAGE_ELEMS = 1280  # complex128 per shared-memory stage (20 KiB: one 16 x 80 dense chunk)
+STAGE_ELEMS = 1408  # complex128 per shared-memory stage (22 KiB: a 16 x 80 dense chunk + x window)
 
 
 def _align(n: int) -> int:
@@ -579,7 +580,11 @@ def _order_segments(segs):
 
 
 def _pieces(segs, has_x):
-    """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages."""
+    """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages.
+
+    Pieces whose input is a window of x (P1 and NEAR ops) carry that window inside the stage,
+    right behind their matrix rows (PI_XSTAGE): the producer bulk-copies it from x (L2-resident)
+    so the consumers never gather x.  Their ``in_off`` is then the x index of the window."""
     out = []
     fill = 0  # elements used in the open stage
     open_idx = None  # index in ``out`` of the open stage's first piece
@@ -593,31 +598,32 @@ def _pieces(segs, has_x):
         open_idx = None
 
     for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in segs:
-        xin = x_off if (x_off >= 0 and has_x) else in_off
-        xflag = PI_XGLOBAL if (x_off >= 0 and has_x) else 0
+        xs = x_off >= 0 and has_x
         if buf == BUF_WORK:  # coherent in-kernel data: no bulk copy, no stage
-            out.append([m_off, ld, rows, cols, mode, xin, out_off, PI_DIRECT | xflag])
+            out.append([m_off, ld, rows, cols, mode, in_off, out_off, PI_DIRECT])
             continue
-        if cols > STAGE_ELEMS:
+        # elements a piece of n rows occupies in a stage (matrix + its x window)
+        per_row = cols + (1 if (xs and mode != MODE_N) else 0)
+        extra = cols if (xs and mode == MODE_N) else 0
+        if per_row + extra > STAGE_ELEMS:
             raise ValueError(f"segment row of {cols} elements exceeds a {STAGE_ELEMS}-element stage")
         r = 0
         while r < rows:
-            room = (STAGE_ELEMS - fill) // cols
-            if room == 0:
+            room = (STAGE_ELEMS - fill - extra) // per_row
+            if room <= 0:
                 close()
-                room = STAGE_ELEMS // cols
+                room = (STAGE_ELEMS - extra) // per_row
             n = min(room, rows - r)
-            info = fill | xflag
+            info = fill | (PI_XSTAGE if xs else 0)
             if open_idx is None:
                 info |= PI_BEGIN
                 open_idx = len(out)
-            out.append([
-                m_off + r * ld, ld, n, cols, mode,
-                xin + (r if mode != MODE_N else 0),
-                out_off + (r if mode == MODE_N else 0),
-                info,
-            ])
-            fill += n * cols
+            if xs:
+                in_v = x_off + (r if mode != MODE_N else 0)
+            else:
+                in_v = in_off + (r if mode != MODE_N else 0)
+            out.append([m_off + r * ld, ld, n, cols, mode, in_v, out_off + (r if mode == MODE_N else 0), info])
+            fill += n * per_row + extra
             r += n
     close()
     return out
@@ -657,7 +663,7 @@ def _finish(phased, fused, n_ctr):
             segs.extend(_panel_split(s))
         seg_e = len(segs)
         pc_b = len(pieces)
-        pieces.extend(_pieces(ordered, False))  # x windows are staged in smem (L1 is carved out)
+        pieces.extend(_pieces(ordered, has_x))
         pc_e = len(pieces)
         w_b = len(waits)
         waits.extend(wt)
@@ -665,7 +671,7 @@ def _finish(phased, fused, n_ctr):
         s_b = len(sigs)
         sigs.extend(sgn)
         s_e = len(sigs)
-        xin_len = n_in
+        xin_len = 0 if has_x else n_in  # x windows travel in the stages (bulk kernel)
         ops[i] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind, pc_b, pc_e, xin_len)
         in_max = max(in_max, n_in)
         xin_max = max(xin_max, xin_len)

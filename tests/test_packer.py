@@ -41,7 +41,7 @@ def test_vm_matches_reference(golden, order, engine):
 def test_pieces_tile_stages(golden):
     """Bulk-kernel pieces: stages never overflow, begin/end flags pair up, every arena
     element of every segment is covered exactly once."""
-    from paper_2405_15573_b200.packer import PI_BEGIN, PI_DIRECT, PI_END, STAGE_ELEMS
+    from paper_2405_15573_b200.packer import PI_BEGIN, PI_DIRECT, PI_END, PI_XSTAGE, STAGE_ELEMS
 
     name, u, ex = golden
     p = pack(u)
@@ -53,6 +53,7 @@ def test_pieces_tile_stages(golden):
             for m_off, ld, rows, cols, mode, in_off, out_off, info in pcs:
                 if info & PI_DIRECT:
                     continue
+                xw = (cols if mode == 0 else rows) if info & PI_XSTAGE else 0
                 if info & PI_BEGIN:
                     assert not open_
                     open_ = True
@@ -61,7 +62,7 @@ def test_pieces_tile_stages(golden):
                     fill = 0
                 assert open_
                 assert (int(info) & 0xFFFFFF) == fill
-                fill += rows * cols
+                fill += rows * cols + xw
                 assert fill <= STAGE_ELEMS
                 if info & PI_END:
                     assert fill == stage
