@@ -71,6 +71,7 @@ HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
 ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op (= consumer row-groups: one row each)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # complex128 per shared-memory stage (22 KiB: a 16 x 80 dense chunk + x window)
+BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 
 
 def _align(n: int) -> int:
@@ -597,7 +598,15 @@ def _pieces(segs, has_x):
         fill = 0
         open_idx = None
 
-    for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in segs:
+    split = []
+    for sg in segs:  # H/S groups own at most BULK_HCOLS_MAX output columns: cut wider ones
+        m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off = sg
+        if mode != MODE_N and cols > BULK_HCOLS_MAX:
+            for c0, c1 in _chunks(0, cols, BULK_HCOLS_MAX):
+                split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off))
+        else:
+            split.append(sg)
+    for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in split:
         xs = x_off >= 0 and has_x
         if buf == BUF_WORK:  # coherent in-kernel data: no bulk copy, no stage
             out.append([m_off, ld, rows, cols, mode, in_off, out_off, PI_DIRECT])

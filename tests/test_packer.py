@@ -41,7 +41,7 @@ def test_vm_matches_reference(golden, order, engine):
 def test_pieces_tile_stages(golden):
     """Bulk-kernel pieces: stages never overflow, begin/end flags pair up, every arena
     element of every segment is covered exactly once."""
-    from paper_2405_15573_b200.packer import PI_BEGIN, PI_DIRECT, PI_END, PI_XSTAGE, STAGE_ELEMS
+    from paper_2405_15573_b200.packer import BULK_HCOLS_MAX, PI_BEGIN, PI_DIRECT, PI_END, PI_XSTAGE, STAGE_ELEMS
 
     name, u, ex = golden
     p = pack(u)
@@ -51,6 +51,8 @@ def test_pieces_tile_stages(golden):
             open_ = False
             fill = 0
             for m_off, ld, rows, cols, mode, in_off, out_off, info in pcs:
+                if mode != 0:
+                    assert cols <= BULK_HCOLS_MAX  # register slots of an H/S group
                 if info & PI_DIRECT:
                     continue
                 xw = (cols if mode == 0 else rows) if info & PI_XSTAGE else 0
