@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 2
+#define UHMV_ABI_VERSION 3
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -57,6 +57,8 @@ typedef struct uhmv_program {
     int32_t out_max;    /* largest output vector of any op (complex elements)          */
     int32_t n_counters; /* dependency counters used by the fused mode                  */
     int32_t xin_max;    /* largest work-buffer input of any op (bulk engine)           */
+    int32_t zero_output; /* zero w before the launch (0 for the post-exchange program of a
+                            multi-GPU rank, which adds into w)                          */
 } uhmv_program;
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */

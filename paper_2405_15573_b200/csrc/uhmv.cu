@@ -625,7 +625,7 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
     if (pr.n_ops > 0 && (!x || !w)) return fail(UHMV_EINVAL, "null vector pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
-    if (phase_lo == 0 && n_out > 0) {  // NEAR/FAR add into a zeroed output
+    if (phase_lo == 0 && n_out > 0 && pr.zero_output) {  // NEAR/FAR add into a zeroed output
         cudaError_t e0 = cudaMemsetAsync(w, 0, (size_t)n_out * 16, st);
         if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
     }
@@ -649,7 +649,7 @@ int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode,
     if (mode != UHMV_MODE_FUSED && mode != UHMV_MODE_BULK)
         return fail(UHMV_EINVAL, "uhmv_execute: unknown mode");
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
-    if (n_out > 0) {  // NEAR/FAR add into a zeroed output
+    if (n_out > 0 && pr.zero_output) {  // NEAR/FAR add into a zeroed output
         if (!w) return fail(UHMV_EINVAL, "null output pointer");
         cudaError_t e0 = cudaMemsetAsync(w, 0, (size_t)n_out * 16, static_cast<cudaStream_t>(stream));
         if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");

@@ -72,13 +72,16 @@ class _DeviceProgram:
         s.out_max = p.out_max
         s.n_counters = p.n_counters
         s.xin_max = p.xin_max
+        s.zero_output = int(p.zero_output)
         return s
 
 
 class DeviceOperator:
     """A packed uniform H-matrix resident in HBM, with its C-ABI plan."""
 
-    def __init__(self, packed: PackedOperator, device=None):
+    def __init__(self, packed: PackedOperator, device=None, programs=None, share_with=None):
+        """``programs=(fwd, adj)`` overrides the packed programs; ``share_with`` reuses another
+        DeviceOperator's arena / work / counter buffers (multi-GPU launch B)."""
         torch = _torch()
         L = _lib.lib()
         self.torch = torch
@@ -87,17 +90,23 @@ class DeviceOperator:
         if dev.index is None:
             dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
-        self.arena = torch.from_numpy(packed.arena).to(dev)
-        self.work = torch.zeros(packed.work_len, dtype=torch.complex128, device=dev)
-        n_ctr = max(packed.fwd.n_counters, packed.adj.n_counters, 1)
-        self.counters = torch.zeros(n_ctr, dtype=torch.int32, device=dev)
-        self.ticket = torch.zeros(1, dtype=torch.int64, device=dev)
-        self.exit_count = torch.zeros(1, dtype=torch.int32, device=dev)
-        nmax = max(packed.n_rows, packed.n_cols, 1)
-        self.x_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
-        self.w_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
-        self.fwd = _DeviceProgram(torch, packed.fwd, dev)
-        self.adj = _DeviceProgram(torch, packed.adj, dev)
+        fwd_p, adj_p = programs if programs is not None else (packed.fwd, packed.adj)
+        self.progs = (fwd_p, adj_p)
+        if share_with is not None:
+            for name in ("arena", "work", "counters", "ticket", "exit_count", "x_scratch", "w_scratch"):
+                setattr(self, name, getattr(share_with, name))
+        else:
+            self.arena = torch.from_numpy(packed.arena).to(dev)
+            self.work = torch.zeros(packed.work_len, dtype=torch.complex128, device=dev)
+            n_ctr = max(packed.fwd.n_counters, packed.adj.n_counters, 1)
+            self.counters = torch.zeros(n_ctr, dtype=torch.int32, device=dev)
+            self.ticket = torch.zeros(1, dtype=torch.int64, device=dev)
+            self.exit_count = torch.zeros(1, dtype=torch.int32, device=dev)
+            nmax = max(packed.n_rows, packed.n_cols, 1)
+            self.x_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
+            self.w_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
+        self.fwd = _DeviceProgram(torch, fwd_p, dev)
+        self.adj = _DeviceProgram(torch, adj_p, dev)
         d = _lib.UhmvDesc()
         d.abi_version = _lib.ABI_VERSION
         d.device = dev.index
@@ -135,7 +144,7 @@ class DeviceOperator:
     def kernel_launches(self, adjoint=False, mode=None) -> int:
         """Number of our kernel launches one matvec issues."""
         mode = mode or default_mode()
-        prog = self.packed.adj if adjoint else self.packed.fwd
+        prog = self.progs[1] if adjoint else self.progs[0]
         if prog.n_ops == 0:
             return 0
         return len(prog.phases) if mode == "phased" else 1

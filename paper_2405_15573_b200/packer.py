@@ -95,6 +95,9 @@ class Program:
     out_max: int
     n_counters: int
     kinds: np.ndarray  # (n_ops,) op kind
+    zero_output: bool = True  # the launcher zeroes w before this program (NEAR/FAR add into it)
+    arena_elems: int = 0  # complex128 arena elements the program streams (roofline bytes / 16)
+    part_b: "Program | None" = None  # multi-GPU: the program launched after the y/u exchange
 
     @property
     def n_ops(self) -> int:
@@ -115,6 +118,10 @@ class PackedOperator:
     bytes_alg: int  # SURVEY.md §8d operator bytes (cheapest stored form), without vectors
     bytes_arena: int
     storage: dict = field(default_factory=dict)
+    rank: int = 0
+    world: int = 1
+    part: dict | None = None
+    exchange: dict = field(default_factory=dict)  # per direction: (ex_off, ex_len) block layout
 
 
 def _leaves_under(tree):
@@ -167,8 +174,23 @@ def _chunks(lo, hi, step):
     return out
 
 
-def pack(u, *, rows_per_chunk: int | None = None, near_interleave=(0.35, 0.1, 0.2, 0.35)) -> PackedOperator:
-    """Pack a UniformHMatrix (reference object or mirror) into arena + programs."""
+def pack(
+    u,
+    *,
+    rows_per_chunk: int | None = None,
+    near_interleave=(0.35, 0.1, 0.2, 0.35),
+    rank: int = 0,
+    world: int = 1,
+) -> PackedOperator:
+    """Pack a UniformHMatrix (reference object or mirror) into arena + programs.
+
+    ``world > 1``: the programs of one rank of the row-cluster partition.
+    Output leaves are cut into ``world`` contiguous slices (``partition_bounds``); this rank
+    runs P1/RED/U for the input clusters it owns (first index inside its input slice),
+    NEAR/FAR for its output rows and Z for every output cluster touching its rows.  y/u live
+    in an exchange region of the work buffer, one block per rank padded to ``ex_len``, filled
+    for everyone by one in-place all-gather between launch A (P1, RED, U, NEAR) and launch B
+    (Z, NEAR, FAR)."""
     if rows_per_chunk is None:
         import os
 
@@ -287,8 +309,15 @@ def pack(u, *, rows_per_chunk: int | None = None, near_interleave=(0.35, 0.1, 0.
         bct=bct, rank_r=rank_r, rank_c=rank_c, kb=kb, factorized=factorized,
         fcols=fcols, ycols=ycols, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
     )
-    fwd, work_f = _build_program(geo, adjoint=False, rows_per_chunk=rows_per_chunk, near_interleave=near_interleave)
-    adj, work_a = _build_program(geo, adjoint=True, rows_per_chunk=rows_per_chunk, near_interleave=near_interleave)
+    if world > 1:
+        rb = partition_bounds(bct.row_tree, world)
+        cb = rb if bct.col_tree is bct.row_tree else partition_bounds(bct.col_tree, world)
+        part = dict(rank=rank, world=world, row_bounds=rb, col_bounds=cb)
+    else:
+        part = None
+    kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part)
+    fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
+    adj, work_a, ex_a = _build_program(geo, adjoint=True, **kw)
     elems_alg = bytes_bases + bytes_coupling + bytes_dense
     return PackedOperator(
         n_rows=n_rows,
@@ -302,6 +331,10 @@ def pack(u, *, rows_per_chunk: int | None = None, near_interleave=(0.35, 0.1, 0.
         n_dense=len(dense_ids),
         bytes_alg=16 * elems_alg,
         bytes_arena=16 * int(arena.size),
+        rank=rank,
+        world=world,
+        part=part,
+        exchange={"fwd": ex_f, "adj": ex_a},
         storage=dict(
             bases=16 * bytes_bases,
             coupling=16 * bytes_coupling,
@@ -312,13 +345,33 @@ def pack(u, *, rows_per_chunk: int | None = None, near_interleave=(0.35, 0.1, 0.
     )
 
 
+def partition_bounds(tree, world: int):
+    """Cut the tree's index range into ``world`` contiguous slices on leaf boundaries.
+
+    Cuts at tree level log2(world) when that is a power of two and the tree is balanced
+    (subtree-aligned), otherwise leaf-balanced by index count."""
+    leaves, _ = _leaves_under(tree)
+    nodes = tree.nodes
+    lo = nodes[getattr(tree, "root", 0)].lo
+    hi = nodes[getattr(tree, "root", 0)].hi
+    ends = [nodes[l].hi for l in leaves]
+    bounds = [lo]
+    for r in range(1, world):
+        target = lo + (hi - lo) * r / world
+        # leaf end closest to the target, strictly after the previous cut
+        best = min((e for e in ends if e > bounds[-1]), key=lambda e: abs(e - target), default=hi)
+        bounds.append(best)
+    bounds.append(hi)
+    return bounds
+
+
 def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
     """Logical segment; ``x_off`` >= 0 means the input vector is x[x_off : ...] (read in place
     by the bulk kernel, staged into xin at ``in_off`` by the register kernel)."""
     return (int(m_off), int(buf), int(rows), int(cols), int(ld), int(mode), int(in_off), int(out_off), int(x_off))
 
 
-def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
+def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None):
     bct = geo["bct"]
     offs = geo["offs"]
     fcols, ycols = geo["fcols"], geo["ycols"]
@@ -336,6 +389,31 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
         in_basis_key, out_basis_key = "V", "U"
         dense_by_outleaf = geo["dense_by_rleaf"]
     in_nodes, out_nodes = in_tree.nodes, out_tree.nodes
+    if part is not None:
+        rank, world = part["rank"], part["world"]
+        in_b = part["row_bounds"] if adjoint else part["col_bounds"]
+        out_b = part["col_bounds"] if adjoint else part["row_bounds"]
+        out_lo, out_hi = out_b[rank], out_b[rank + 1]
+
+        def owner_in(t):
+            lo = in_nodes[t].lo
+            for r in range(world):
+                if in_b[r] <= lo < in_b[r + 1]:
+                    return r
+            return world - 1
+
+        def out_needed(s_):
+            n_ = out_nodes[s_]
+            return n_.lo < out_hi and n_.hi > out_lo
+    else:
+        rank, world = 0, 1
+        out_lo, out_hi = 0, out_tree.nodes[getattr(out_tree, "root", 0)].hi
+
+        def owner_in(t):
+            return 0
+
+        def out_needed(s_):
+            return True
 
     # ---- work-buffer layout ----
     work = 0
@@ -348,7 +426,7 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
 
     in_leaves, in_span = _leaves_under(in_tree)
     out_leaves, out_span = _leaves_under(out_tree)
-    in_anc = _ancestors_in(in_tree, in_leaves, in_span, [t for t in in_map if in_rank[t] > 0])
+    in_anc = _ancestors_in(in_tree, in_leaves, in_span, [t for t in in_map if in_rank[t] > 0 and owner_in(t) == rank])
     out_anc = _ancestors_in(out_tree, out_leaves, out_span, [s for s in out_map if out_rank[s] > 0])
 
     p1_items = []  # (leafpos, lo, hi): every in-leaf split in <= P1_CHUNK rows
@@ -362,18 +440,26 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     for idx, (p, a, b) in enumerate(p1_items):
         for t in in_anc[p]:
             chunks_of[t].append(idx)
-    y_off, part_off = {}, {}
+    # exchange region: per owner rank, its input clusters' [y_t | u_t] in position order, every
+    # rank block padded to the same length (in-place all-gather target)
+    u_len = {t: (ycols[t][1] if not adjoint else fcols[t][1]) for t in in_map}
+    by_rank = [[] for _ in range(world)]
     for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
-        y_off[t] = walloc(in_rank[t])
+        by_rank[owner_in(t)].append(t)
+    ex_len = max([sum(in_rank[t] + u_len[t] for t in ts) for ts in by_rank] + [0])
+    y_off, u_off = {}, {}
+    for r, ts in enumerate(by_rank):
+        cur = r * ex_len
+        for t in ts:
+            y_off[t] = cur
+            cur += in_rank[t]
+            u_off[t] = cur
+            cur += u_len[t]
+    walloc(world * ex_len)
+    part_off = {}
     for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
-        if in_rank[t]:
+        if in_rank[t] and owner_in(t) == rank:
             part_off[t] = y_off[t] if len(chunks_of[t]) == 1 else walloc(len(chunks_of[t]) * in_rank[t])
-    # staging vectors u: forward per column cluster t (columns of Y_t), adjoint per row
-    # cluster s (columns of F_s)
-    u_off, u_len = {}, {}
-    for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
-        u_len[t] = ycols[t][1] if not adjoint else fcols[t][1]
-        u_off[t] = walloc(u_len[t])
     z_off = {}
     for s in sorted(out_map, key=lambda s: out_nodes[s].lo):
         z_off[s] = walloc(out_rank[s])
@@ -410,7 +496,7 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     # RED: y_t = sum of chunk partials (skipped when the single partial is y_t itself)
     for t in in_map:
         lt, nchunk = in_rank[t], len(chunks_of[t])
-        if lt == 0 or nchunk <= 1:
+        if lt == 0 or nchunk <= 1 or owner_in(t) != rank:
             continue
         segs = [_seg(part_off[t], BUF_WORK, nchunk, lt, lt, MODE_S, 0, 0)]
         ops[KIND_RED].append(
@@ -418,8 +504,8 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
         )
     y_wait = {}
     for t in in_map:
-        if in_rank[t] == 0:
-            y_wait[t] = []
+        if in_rank[t] == 0 or owner_in(t) != rank:
+            y_wait[t] = []  # zero-width, or produced by another rank (ordered by the exchange)
         elif len(chunks_of[t]) <= 1:
             y_wait[t] = [(c_part[t], len(chunks_of[t]))]
         else:
@@ -430,7 +516,7 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     for t in in_map:
         n, lt = u_len[t], in_rank[t]
         u_wait[t] = []
-        if n == 0 or lt == 0:
+        if n == 0 or lt == 0 or owner_in(t) != rank:
             continue
         u_wait[t] = [(c_u[t], 1)]
         base = offs[("Y", t)] if not adjoint else offs[("F", t)]
@@ -442,7 +528,7 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     # Z: coupling, owned by the output cluster (row cluster forward, column cluster adjoint)
     for s in out_map:
         ls = out_rank[s]
-        if ls == 0:
+        if ls == 0 or not out_needed(s):
             continue
         in_runs, segs, waits = [], [], []
         if not adjoint:
@@ -495,6 +581,8 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     # order-independent (fl(a+b) = fl(b+a)), so NEAR and FAR need no ordering between them.
     for p, leaf in enumerate(out_leaves):
         n = out_nodes[leaf]
+        if not (out_lo <= n.lo and n.hi <= out_hi):
+            continue  # another rank's output rows
         dlist = dense_by_outleaf.get(leaf, [])
         # forward: row chunks of the leaf; adjoint: the whole column leaf (H segments reduce
         # over the block rows, so the op owns all |c| output entries of the leaf)
@@ -551,13 +639,25 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave):
     # phased launches (multi-launch mode): [P1 + NEAR] [RED] [U] [Z] [FAR]
     phased = [ops[KIND_P1] + near]
     phased += [ops[k] for k in (KIND_RED, KIND_U, KIND_Z, KIND_FAR)]
-    # fused persistent order: every op waits only on ops that come earlier; nearfield ops (no
-    # dependencies) are spread between the dependent farfield phases to cover their latency
-    fused = (
-        ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
-        + ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
-    )
-    return _finish(phased, fused, n_ctr), work
+    ex = (0, ex_len)
+    if world == 1:
+        # fused persistent order: every op waits only on ops that come earlier; nearfield ops
+        # (no dependencies) are spread between the dependent farfield phases to cover latency
+        fused = (
+            ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
+            + ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
+        )
+        return _finish(phased, fused, n_ctr), work, ex
+    # multi-GPU: launch A produces this rank's y/u (+ nearfield), the exchange fills every
+    # rank's y/u, launch B consumes them.  Waits on ops outside a launch are dropped: they are
+    # ordered by the launch boundary and the all-gather.
+    a_ops = ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
+    b_ops = ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
+    prog_a = _finish([a_ops], a_ops, n_ctr)
+    prog_b = _finish([b_ops], b_ops, n_ctr, keep_waits_on=KIND_Z)
+    prog_b.zero_output = False
+    prog_a.part_b = prog_b
+    return prog_a, work, ex
 
 
 def _panel_split(s):
@@ -638,9 +738,10 @@ def _pieces(segs, has_x):
     return out
 
 
-def _finish(phased, fused, n_ctr):
+def _finish(phased, fused, n_ctr, keep_waits_on=None):
     """Flatten op tuples into arrays in the phased order; the fused order is a
-    permutation (``fused_order[ticket] = op index``)."""
+    permutation (``fused_order[ticket] = op index``).  ``keep_waits_on``: in a partial program
+    keep only waits on counters signalled by ops of this kind inside the program."""
     order = [o for ph in phased for o in ph]
     bounds = []
     a = 0
@@ -656,7 +757,14 @@ def _finish(phased, fused, n_ctr):
     ops = np.zeros((n, OP_FIELDS), dtype=np.int32)
     segs, pieces, runs, waits, sigs = [], [], [], [], []
     in_max = xin_max = out_max = 0
+    arena_elems = 0
+    local_ctr = None
+    if keep_waits_on is not None:
+        local_ctr = {c for o in order if o[0] == keep_waits_on for c in o[7]}
     for i, (kind, n_in, n_out, in_runs, sg, out_runs, wt, sgn, _) in enumerate(order):
+        if local_ctr is not None:
+            wt = [w for w in wt if w[0] in local_ctr]
+        arena_elems += sum(q[2] * q[3] for q in sg if q[1] == BUF_ARENA)
         has_x = any(r[0] == BUF_X for r in in_runs)
         has_w = any(r[0] == BUF_WORK for r in in_runs)
         assert not (has_x and has_w), "an op reads x or work inputs, never both"
@@ -699,4 +807,5 @@ def _finish(phased, fused, n_ctr):
         out_max=out_max,
         n_counters=n_ctr,
         kinds=ops[:, 12].copy(),
+        arena_elems=arena_elems,
     )
