@@ -53,10 +53,15 @@ def views():
 
 
 def ensure_built():
+    """Build libuhmv.so if it is missing or stale (ABI mismatch), then load it."""
     from paper_2405_15573_b200 import _lib
 
-    if not os.path.exists(_lib.LIB_PATH):
-        import __graft_entry__
+    if os.path.exists(_lib.LIB_PATH):
+        try:
+            return _lib.lib()
+        except RuntimeError:
+            pass
+    import __graft_entry__
 
-        __graft_entry__.build()
+    __graft_entry__.build()
     return _lib.lib()
