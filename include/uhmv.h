@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 3
+#define UHMV_ABI_VERSION 4
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -59,6 +59,7 @@ typedef struct uhmv_program {
     int32_t xin_max;    /* largest work-buffer input of any op (bulk engine)           */
     int32_t zero_output; /* zero w before the launch (0 for the post-exchange program of a
                             multi-GPU rank, which adds into w)                          */
+    int32_t stage_elems; /* complex128 elements per shared-memory stage (bulk engine)  */
 } uhmv_program;
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */

@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "check", "LIB_PATH", "MAX_PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 3
+ABI_VERSION = 4
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -36,6 +36,7 @@ class UhmvProgram(ctypes.Structure):
         ("n_counters", ctypes.c_int32),
         ("xin_max", ctypes.c_int32),
         ("zero_output", ctypes.c_int32),
+        ("stage_elems", ctypes.c_int32),
     ]
 
 

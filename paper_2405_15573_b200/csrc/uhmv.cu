@@ -523,13 +523,14 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         const uhmv_program* pr = progs[k];
         int budget = smem_sm / want_ctas - 1024;
         if (budget > smem_optin) budget = smem_optin;
-        const int fixed = bulk::layout(0, pr->xin_max, pr->out_max).total;
-        int ns = (budget - fixed) / bulk::kStageBytes;
+        const int sbytes = (pr->stage_elems > 0 ? pr->stage_elems : 1408) * 16;
+        const int fixed = bulk::layout(0, sbytes, pr->xin_max, pr->out_max).total;
+        int ns = (budget - fixed) / sbytes;
         if (want_stages > 0) ns = want_stages;
         if (ns > 12) ns = 12;
         if (ns < 2) ns = 2;
         p->bulk_nstage[k] = ns;
-        p->bulk_smem[k] = bulk::layout(ns, pr->xin_max, pr->out_max).total;
+        p->bulk_smem[k] = bulk::layout(ns, sbytes, pr->xin_max, pr->out_max).total;
         if (p->bulk_smem[k] > bulk_need) bulk_need = p->bulk_smem[k];
     }
     if (bulk_need > smem_optin) {
@@ -579,6 +580,7 @@ static bulk::Params make_bulk_params(const uhmv_plan* plan, const uhmv_program& 
     bp.fused_order = pr.fused_order;
     bp.op_count = pr.n_ops;
     bp.nstage = plan->bulk_nstage[k];
+    bp.stage_bytes = (pr.stage_elems > 0 ? pr.stage_elems : 1408) * 16;
     bp.counters = plan->d.counters;
     bp.ticket = plan->d.ticket;
     bp.exit_count = plan->d.exit_count;

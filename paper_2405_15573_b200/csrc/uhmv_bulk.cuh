@@ -31,8 +31,7 @@ namespace bulk {
 constexpr int kConsumerWarps = 4;
 constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
-constexpr int kStageElems = 1408;                // = packer.STAGE_ELEMS (22 KiB of complex128)
-constexpr int kStageBytes = kStageElems * 16;
+
 constexpr int kOpSlots = 2;
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
@@ -73,6 +72,7 @@ struct Params {
     const int32_t* fused_order;
     int32_t op_count;
     int32_t nstage;
+    int32_t stage_bytes;  // 16 x program.stage_elems
     uint32_t* counters;
     unsigned long long* ticket;
     uint32_t* exit_count;
@@ -92,10 +92,10 @@ struct Layout {
     int stage_off, xin_off, out_off, slot_off, bar_off, prof_off, total;
 };
 
-__host__ __device__ inline Layout layout(int nstage, int xin_max, int out_max) {
+__host__ __device__ inline Layout layout(int nstage, int stage_bytes, int xin_max, int out_max) {
     Layout L;
     L.stage_off = 0;
-    L.xin_off = nstage * kStageBytes;
+    L.xin_off = nstage * stage_bytes;
     L.out_off = L.xin_off + ((xin_max * 16 + 127) & ~127);
     L.slot_off = L.out_off + ((out_max * 16 + 127) & ~127);
     L.bar_off = L.slot_off + kOpSlots * (int)sizeof(OpSlot);
@@ -251,7 +251,7 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 }
                 if (lane == 0) {
                     unsigned char* dst =
-                        stages + (size_t)stage * kStageBytes + (size_t)(info & 0xFFFFFF) * 16;
+                        stages + (size_t)stage * p.stage_bytes + (size_t)(info & 0xFFFFFF) * 16;
                     const double2* src = p.arena + m_off;
                     if (ld == cols) {
                         bulk_g2s(dst, src, (uint32_t)rows * cols * 16, &full[stage], policy);
@@ -475,7 +475,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                         t0 = t1;
                     }
                 }
-                tile = reinterpret_cast<const double2*>(stages + (size_t)stage * kStageBytes) +
+                tile = reinterpret_cast<const double2*>(stages + (size_t)stage * p.stage_bytes) +
                        (c.w & 0xFFFF);
             }
             if (prof) pr[kind * 8 + 4] += 1;
@@ -625,7 +625,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
 template <bool PROF>
 __global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const Layout L = layout(p.nstage, p.xin_max, p.out_max);
+    const Layout L = layout(p.nstage, p.stage_bytes, p.xin_max, p.out_max);
     unsigned char* stages = smem + L.stage_off;
     double2* xin = reinterpret_cast<double2*>(smem + L.xin_off);
     double2* outv = reinterpret_cast<double2*>(smem + L.out_off);

@@ -73,6 +73,7 @@ class _DeviceProgram:
         s.n_counters = p.n_counters
         s.xin_max = p.xin_max
         s.zero_output = int(p.zero_output)
+        s.stage_elems = int(p.stage_elems)
         return s
 
 

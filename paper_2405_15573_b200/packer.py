@@ -70,7 +70,7 @@ ALIGN = 8  # complex128 elements per 128 B
 HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
 ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op (= consumer row-groups: one row each)
 P1_CHUNK = 256  # max input rows per P1 op
-STAGE_ELEMS = 1408  # complex128 per shared-memory stage (22 KiB: a 16 x 80 dense chunk + x window)
+STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 
 
@@ -98,6 +98,7 @@ class Program:
     zero_output: bool = True  # the launcher zeroes w before this program (NEAR/FAR add into it)
     arena_elems: int = 0  # complex128 arena elements the program streams (roofline bytes / 16)
     part_b: "Program | None" = None  # multi-GPU: the program launched after the y/u exchange
+    stage_elems: int = STAGE_ELEMS  # bulk kernel stage size the pieces were packed for
 
     @property
     def n_ops(self) -> int:
@@ -181,6 +182,7 @@ def pack(
     near_interleave=(0.35, 0.1, 0.2, 0.35),
     rank: int = 0,
     world: int = 1,
+    stage_elems: int | None = None,
 ) -> PackedOperator:
     """Pack a UniformHMatrix (reference object or mirror) into arena + programs.
 
@@ -191,10 +193,12 @@ def pack(
     in an exchange region of the work buffer, one block per rank padded to ``ex_len``, filled
     for everyone by one in-place all-gather between launch A (P1, RED, U, NEAR) and launch B
     (Z, NEAR, FAR)."""
-    if rows_per_chunk is None:
-        import os
+    import os
 
+    if rows_per_chunk is None:
         rows_per_chunk = int(os.environ.get("UHMV_ROWS_PER_CHUNK", ROWS_PER_CHUNK))
+    if stage_elems is None:
+        stage_elems = int(os.environ.get("UHMV_STAGE_ELEMS", STAGE_ELEMS))
     bct = u.bct
     n_rows, n_cols = bct.shape
     rnodes, cnodes = bct.row_tree.nodes, bct.col_tree.nodes
@@ -315,7 +319,7 @@ def pack(
         part = dict(rank=rank, world=world, row_bounds=rb, col_bounds=cb)
     else:
         part = None
-    kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part)
+    kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems)
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
     adj, work_a, ex_a = _build_program(geo, adjoint=True, **kw)
     elems_alg = bytes_bases + bytes_coupling + bytes_dense
@@ -371,7 +375,7 @@ def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
     return (int(m_off), int(buf), int(rows), int(cols), int(ld), int(mode), int(in_off), int(out_off), int(x_off))
 
 
-def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None):
+def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS):
     bct = geo["bct"]
     offs = geo["offs"]
     fcols, ycols = geo["fcols"], geo["ycols"]
@@ -647,14 +651,14 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, 
             ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
             + ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
         )
-        return _finish(phased, fused, n_ctr), work, ex
+        return _finish(phased, fused, n_ctr, stage_elems=stage_elems), work, ex
     # multi-GPU: launch A produces this rank's y/u (+ nearfield), the exchange fills every
     # rank's y/u, launch B consumes them.  Waits on ops outside a launch are dropped: they are
     # ordered by the launch boundary and the all-gather.
     a_ops = ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
     b_ops = ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
-    prog_a = _finish([a_ops], a_ops, n_ctr)
-    prog_b = _finish([b_ops], b_ops, n_ctr, keep_waits_on=KIND_Z)
+    prog_a = _finish([a_ops], a_ops, n_ctr, stage_elems=stage_elems)
+    prog_b = _finish([b_ops], b_ops, n_ctr, keep_waits_on=KIND_Z, stage_elems=stage_elems)
     prog_b.zero_output = False
     prog_a.part_b = prog_b
     return prog_a, work, ex
@@ -680,7 +684,7 @@ def _order_segments(segs):
     return n + h
 
 
-def _pieces(segs, has_x):
+def _pieces(segs, has_x, stage_elems=STAGE_ELEMS):
     """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages.
 
     Pieces whose input is a window of x (P1 and NEAR ops) carry that window inside the stage,
@@ -714,14 +718,14 @@ def _pieces(segs, has_x):
         # elements a piece of n rows occupies in a stage (matrix + its x window)
         per_row = cols + (1 if (xs and mode != MODE_N) else 0)
         extra = cols if (xs and mode == MODE_N) else 0
-        if per_row + extra > STAGE_ELEMS:
-            raise ValueError(f"segment row of {cols} elements exceeds a {STAGE_ELEMS}-element stage")
+        if per_row + extra > stage_elems:
+            raise ValueError(f"segment row of {cols} elements exceeds a {stage_elems}-element stage")
         r = 0
         while r < rows:
-            room = (STAGE_ELEMS - fill - extra) // per_row
+            room = (stage_elems - fill - extra) // per_row
             if room <= 0:
                 close()
-                room = (STAGE_ELEMS - extra) // per_row
+                room = (stage_elems - extra) // per_row
             n = min(room, rows - r)
             info = fill | (PI_XSTAGE if xs else 0)
             if open_idx is None:
@@ -738,7 +742,7 @@ def _pieces(segs, has_x):
     return out
 
 
-def _finish(phased, fused, n_ctr, keep_waits_on=None):
+def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
     """Flatten op tuples into arrays in the phased order; the fused order is a
     permutation (``fused_order[ticket] = op index``).  ``keep_waits_on``: in a partial program
     keep only waits on counters signalled by ops of this kind inside the program."""
@@ -780,7 +784,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None):
             segs.extend(_panel_split(s))
         seg_e = len(segs)
         pc_b = len(pieces)
-        pieces.extend(_pieces(ordered, has_x))
+        pieces.extend(_pieces(ordered, has_x, stage_elems))
         pc_e = len(pieces)
         w_b = len(waits)
         waits.extend(wt)
@@ -808,4 +812,5 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None):
         n_counters=n_ctr,
         kinds=ops[:, 12].copy(),
         arena_elems=arena_elems,
+        stage_elems=stage_elems,
     )

@@ -60,12 +60,12 @@ def test_pieces_tile_stages(golden):
                     assert not open_
                     open_ = True
                     stage = (int(info) >> 32) & 0xFFFFFF
-                    assert 0 < stage <= STAGE_ELEMS
+                    assert 0 < stage <= prog.stage_elems
                     fill = 0
                 assert open_
                 assert (int(info) & 0xFFFFFF) == fill
                 fill += rows * cols + xw
-                assert fill <= STAGE_ELEMS
+                assert fill <= prog.stage_elems
                 if info & PI_END:
                     assert fill == stage
                     open_ = False
