@@ -351,9 +351,9 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         const int kind = S->hdr[12] & 7;
         const int n_in_runs = in_e - in_b;
         const int n_runs = out_e - in_b;
-        if (tid == 0 && !p.skip_waits) {
+        if (!p.skip_waits) {  // every consumer thread polls one dependency counter in parallel
             const int wb = S->hdr[8], we = S->hdr[9];
-            for (int i = wb; i < we; ++i) {
+            for (int i = wb + tid; i < we; i += kConsumers) {
                 const int c = __ldg(p.waits + 2 * i);
                 const uint32_t need = (uint32_t)__ldg(p.waits + 2 * i + 1);
                 while (ld_acquire(p.counters + c) < need) __nanosleep(20);
