@@ -490,21 +490,26 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     const double2* X = xv + g;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
                     double cr = 0.0, ci = 0.0, dr = 0.0, di = 0.0;
-                    int j = g;
-                    for (; j + 3 * kLanesPerRow < cols; j += 4 * kLanesPerRow) {  // 4 chains
-                        const double2 t0 = T[0], t1 = T[8], t2 = T[16], t3 = T[24];
-                        const double2 x0 = X[0], x1 = X[8], x2 = X[16], x3 = X[24];
+                    // warp-uniform trip count (cols is uniform per piece); ragged tails are
+                    // predicated instead of diverging inside the row-group
+                    const int nk = (cols + kLanesPerRow - 1) / kLanesPerRow;
+                    for (int k = 0; k < nk; k += 4) {
+                        const int j = g + k * kLanesPerRow;
+                        const double2 z = make_double2(0.0, 0.0);
+                        const double2 t0 = (j < cols) ? T[0] : z;
+                        const double2 x0 = (j < cols) ? X[0] : z;
+                        const double2 t1 = (j + 8 < cols) ? T[8] : z;
+                        const double2 x1 = (j + 8 < cols) ? X[8] : z;
+                        const double2 t2 = (j + 16 < cols) ? T[16] : z;
+                        const double2 x2 = (j + 16 < cols) ? X[16] : z;
+                        const double2 t3 = (j + 24 < cols) ? T[24] : z;
+                        const double2 x3 = (j + 24 < cols) ? X[24] : z;
                         cmac(ar, ai, t0, x0);
                         cmac(br, bi, t1, x1);
                         cmac(cr, ci, t2, x2);
                         cmac(dr, di, t3, x3);
                         T += 32;
                         X += 32;
-                    }
-                    for (; j < cols; j += kLanesPerRow) {
-                        cmac(ar, ai, T[0], X[0]);
-                        T += 8;
-                        X += 8;
                     }
                     ar += br + (cr + dr);
                     ai += bi + (ci + di);
