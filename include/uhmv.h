@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 4
+#define UHMV_ABI_VERSION 5
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -60,6 +60,8 @@ typedef struct uhmv_program {
     int32_t zero_output; /* zero w before the launch (0 for the post-exchange program of a
                             multi-GPU rank, which adds into w)                          */
     int32_t stage_elems; /* complex128 elements per shared-memory stage (bulk engine)  */
+    const int64_t* mr_segs;   /* multi-RHS segments, n x 8 int64 (one input source each)   */
+    const int32_t* mr_ranges; /* n_ops x 2 int32: mr_segs range of every op                 */
 } uhmv_program;
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */
@@ -104,6 +106,13 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
  * Replaces: the whole matvec_uh call as a caller sees it (uniform.py:476-556). */
 int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
                      void* stream);
+
+/* Multi-RHS product on FP64 tensor cores (DMMA): W = A X or A^H X, X (n_in x nrhs), W
+ * (n_out x nrhs) and work_mr (work_len x nrhs) device complex128, row-major, nrhs a
+ * multiple of 16.  Replaces the reference's column loop over matvec_uh (uniform.py:493-494
+ * rejects 2-D input).  Asynchronous. */
+int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs,
+                      int adjoint, void* stream);
 
 /* Launch geometry chosen for a mode (grid CTAs, dynamic shared memory bytes, threads per CTA,
  * shared-memory stages of the bulk engine). */

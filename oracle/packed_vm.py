@@ -94,3 +94,44 @@ def vm_matvec(packed, v, adjoint=False, order="phased", engine="segs"):
     work = np.zeros(packed.work_len, dtype=np.complex128)
     run_program(prog, packed.arena, work, x, w, order=order, engine=engine)
     return w
+
+
+def run_op_mr(prog, i, bufs, R):
+    """Multi-RHS op: vectors are (len, R) blocks; uses the resolved ``mr_segs``."""
+    n_out = int(prog.ops[i, 1])
+    out_b, out_e = (int(v) for v in prog.ops[i, 6:8])
+    a, b = (int(v) for v in prog.mr_ranges[i])
+    out = np.zeros((n_out, R), dtype=np.complex128)
+    for m_off, ld, rows, cols, mode, in_buf, in_abs, out_off in prog.mr_segs[a:b]:
+        if mode == MODE_S:
+            src = bufs[BUF_WORK]
+            for k in range(rows):
+                out[out_off : out_off + cols] += src[m_off + k * ld : m_off + k * ld + cols]
+            continue
+        idx = m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]
+        m = bufs[BUF_ARENA][idx]
+        vin = bufs[int(in_buf)]
+        if mode == MODE_N:
+            out[out_off : out_off + rows] += m @ vin[in_abs : in_abs + cols]
+        else:
+            out[out_off : out_off + cols] += np.conj(m).T @ vin[in_abs : in_abs + rows]
+    for buf, off, ln, dst, flags in prog.runs[out_b:out_e]:
+        if flags & (RUN_ADD | RUN_ATOMIC):
+            bufs[buf][off : off + ln] += out[dst : dst + ln]
+        else:
+            bufs[buf][off : off + ln] = out[dst : dst + ln]
+
+
+def vm_matmat(packed, V, adjoint=False):
+    """Multi-RHS program interpreter: V (n_in, R) -> W (n_out, R)."""
+    prog = packed.adj if adjoint else packed.fwd
+    n_in, n_out = (packed.n_rows, packed.n_cols) if adjoint else (packed.n_cols, packed.n_rows)
+    X = np.asarray(V, dtype=np.complex128)
+    R = X.shape[1]
+    assert X.shape[0] == n_in
+    W = np.zeros((n_out, R), dtype=np.complex128)
+    work = np.zeros((packed.work_len, R), dtype=np.complex128)
+    bufs = {BUF_ARENA: packed.arena, BUF_WORK: work, BUF_X: X, BUF_W: W}
+    for i in prog.fused_order.tolist():
+        run_op_mr(prog, i, bufs, R)
+    return W

@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "check", "LIB_PATH", "MAX_PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 4
+ABI_VERSION = 5
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -37,6 +37,8 @@ class UhmvProgram(ctypes.Structure):
         ("xin_max", ctypes.c_int32),
         ("zero_output", ctypes.c_int32),
         ("stage_elems", ctypes.c_int32),
+        ("mr_segs", ctypes.c_void_p),
+        ("mr_ranges", ctypes.c_void_p),
     ]
 
 
@@ -67,6 +69,7 @@ EXPORTS = (
     "uhmv_execute",
     "uhmv_execute_phases",
     "uhmv_matvec_host",
+    "uhmv_execute_mrhs",
     "uhmv_plan_info",
     "uhmv_plan_set_profile",
     "uhmv_plan_destroy",
@@ -94,6 +97,8 @@ def lib():
     L.uhmv_execute_phases.argtypes = [vp, vp, vp, i32, i32, i32, vp]
     L.uhmv_execute_phases.restype = i32
     L.uhmv_matvec_host.argtypes = [vp, vp, vp, i32, i32, vp]
+    L.uhmv_execute_mrhs.argtypes = [vp, vp, vp, vp, i32, i32, vp]
+    L.uhmv_execute_mrhs.restype = i32
     L.uhmv_matvec_host.restype = i32
     pi = ctypes.POINTER(i32)
     L.uhmv_plan_info.argtypes = [vp, i32, i32, pi, pi, pi, pi]

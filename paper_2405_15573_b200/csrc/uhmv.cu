@@ -343,6 +343,7 @@ __device__ void run_op(const ExecParams& p, int op, double2* xin, double2* outv,
 }  // namespace
 
 #include "uhmv_bulk.cuh"
+#include "uhmv_mrhs.cuh"
 
 namespace {
 
@@ -431,6 +432,7 @@ struct uhmv_plan {
     int debug_skip_waits;  // diagnostics only (UHMV_DEBUG_SKIP_WAITS): results are wrong
     unsigned long long* prof;  // diagnostics only (uhmv_plan_set_profile)
     int debug_flags;           // diagnostics only (UHMV_DEBUG_FLAGS): results are wrong
+    int mrhs_grid;
 };
 
 extern "C" {
@@ -559,6 +561,16 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         if (grid > progs[k]->n_ops) grid = progs[k]->n_ops > 0 ? progs[k]->n_ops : 1;
         p->bulk_grid[k] = grid;
     }
+    {
+        int per_sm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrhs::uhmv_mrhs_kernel,
+                                                          mrhs::kThreads, 0);
+        if (e != cudaSuccess) {
+            delete p;
+            return cuda_fail(e, "occupancy(mrhs)");
+        }
+        p->mrhs_grid = (per_sm < 1 ? 1 : per_sm) * p->sm_count;
+    }
     if (const char* ev = getenv("UHMV_DEBUG_SKIP_WAITS")) p->debug_skip_waits = atoi(ev);
     if (const char* ev = getenv("UHMV_DEBUG_FLAGS")) p->debug_flags = atoi(ev);
     *out = p;
@@ -677,6 +689,45 @@ int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode,
                         static_cast<cudaStream_t>(stream)>>>(ep);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "uhmv_fused_kernel launch");
+    return UHMV_OK;
+}
+
+int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs,
+                      int adjoint, void* stream) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_execute_mrhs: null plan");
+    if (nrhs <= 0 || nrhs % mrhs::kRC) return fail(UHMV_EINVAL, "nrhs must be a multiple of 16");
+    const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
+    if (!pr.mr_segs || !pr.mr_ranges) return fail(UHMV_EINVAL, "program has no multi-RHS tables");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
+    if (n_out > 0 && pr.zero_output) {
+        cudaError_t e0 = cudaMemsetAsync(w, 0, (size_t)n_out * nrhs * 16, st);
+        if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(W)");
+    }
+    if (pr.n_ops == 0) return UHMV_OK;
+    if (!x || !w || !work_mr) return fail(UHMV_EINVAL, "null matrix pointer");
+    mrhs::Params mp;
+    mp.arena = static_cast<const double2*>(plan->d.arena);
+    mp.work = static_cast<double2*>(work_mr);
+    mp.x = static_cast<const double2*>(x);
+    mp.w = static_cast<double2*>(w);
+    mp.ops = pr.ops;
+    mp.runs = pr.runs;
+    mp.waits = pr.waits;
+    mp.sigs = pr.sigs;
+    mp.fused_order = pr.fused_order;
+    mp.mr_segs = pr.mr_segs;
+    mp.mr_ranges = pr.mr_ranges;
+    mp.op_count = pr.n_ops;
+    mp.nrhs = nrhs;
+    mp.counters = plan->d.counters;
+    mp.ticket = plan->d.ticket;
+    mp.exit_count = plan->d.exit_count;
+    mp.n_counters = pr.n_counters;
+    int grid = plan->mrhs_grid < pr.n_ops ? plan->mrhs_grid : pr.n_ops;
+    mrhs::uhmv_mrhs_kernel<<<grid, mrhs::kThreads, 0, st>>>(mp);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "uhmv_mrhs_kernel launch");
     return UHMV_OK;
 }
 

@@ -50,6 +50,8 @@ class _DeviceProgram:
         self.sigs = up(prog.sigs, torch.int32)
         self.fused_order = up(prog.fused_order, torch.int32)
         self.pieces = up(prog.pieces, torch.int64)
+        self.mr_segs = up(prog.mr_segs, torch.int64)
+        self.mr_ranges = up(prog.mr_ranges, torch.int32)
 
     def struct(self) -> _lib.UhmvProgram:
         p = self.prog
@@ -74,6 +76,8 @@ class _DeviceProgram:
         s.xin_max = p.xin_max
         s.zero_output = int(p.zero_output)
         s.stage_elems = int(p.stage_elems)
+        s.mr_segs = self.mr_segs.data_ptr()
+        s.mr_ranges = self.mr_ranges.data_ptr()
         return s
 
 
@@ -197,6 +201,36 @@ class DeviceOperator:
         )
         _lib.check(rc, "uhmv_execute")
         return out
+
+    def matmat(self, X, adjoint=False, out=None, stream=None):
+        """Multi-RHS device API on FP64 tensor cores: X (n_in, R) complex128 CUDA tensor ->
+        (n_out, R).  R is padded to a multiple of 16 internally."""
+        torch = self.torch
+        p = self.packed
+        n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
+        if X.dim() != 2 or X.shape[0] != n_in or X.dtype != torch.complex128:
+            raise ValueError(f"X must be complex128 of shape ({n_in}, R)")
+        R = X.shape[1]
+        Rp = max(16, (R + 15) // 16 * 16)
+        if Rp != R:
+            Xp = torch.zeros((n_in, Rp), dtype=torch.complex128, device=self.device)
+            Xp[:, :R] = X
+        else:
+            Xp = X.contiguous()
+        W = torch.empty((n_out, Rp), dtype=torch.complex128, device=self.device)
+        need = p.work_len * Rp
+        if getattr(self, "_work_mr", None) is None or self._work_mr.numel() < need:
+            self._work_mr = torch.zeros(need, dtype=torch.complex128, device=self.device)
+        rc = _lib.lib().uhmv_execute_mrhs(
+            self._plan, ctypes.c_void_p(Xp.data_ptr()), ctypes.c_void_p(W.data_ptr()),
+            ctypes.c_void_p(self._work_mr.data_ptr()), int(Rp), int(adjoint), self._stream(stream),
+        )
+        _lib.check(rc, "uhmv_execute_mrhs")
+        res = W[:, :R] if Rp != R else W
+        if out is not None:
+            out.copy_(res)
+            return out
+        return res
 
     def execute_phases(self, x, out, adjoint, lo, hi, stream=None):
         rc = _lib.lib().uhmv_execute_phases(

@@ -57,6 +57,7 @@ OP_FIELDS = 16  # int32 per op
 SEG_FIELDS = 8  # int64: m_off, buf, rows, cols, ld, mode, in_off, out_off
 RUN_FIELDS = 5  # int64: buf, off, len, dst, flags
 PIECE_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_off, out_off, info
+MR_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_buf, in_abs (element index), out_off
 # piece info bits: [0,24) smem element offset in its stage, 24 stage_begin, 25 stage_end,
 # 26 direct (no stage: coherent loads from the work buffer), 27 input read from x directly,
 # 28 x window carried in the stage behind the matrix rows (in_off = its x index),
@@ -99,6 +100,8 @@ class Program:
     arena_elems: int = 0  # complex128 arena elements the program streams (roofline bytes / 16)
     part_b: "Program | None" = None  # multi-GPU: the program launched after the y/u exchange
     stage_elems: int = STAGE_ELEMS  # bulk kernel stage size the pieces were packed for
+    mr_segs: np.ndarray | None = None  # (n, MR_FIELDS) int64: multi-RHS segments, one input source each
+    mr_ranges: np.ndarray | None = None  # (n_ops, 2) int32: mr_segs range of every op
 
     @property
     def n_ops(self) -> int:
@@ -742,6 +745,33 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS):
     return out
 
 
+def _resolve_inputs(segs, in_runs):
+    """Multi-RHS form of an op's segments: each one reads its input from ONE contiguous
+    source (x or work) at an absolute element index; a segment whose input window spans
+    several gather runs (F_s over many u_b vectors) is cut at the run boundaries
+    (column ranges for N, row ranges for H/S)."""
+    runs = sorted(in_runs, key=lambda r: r[3])  # (buf, off, len, dst, flags) by xin position
+    out = []
+    for m_off, buf, rows, cols, ld, mode, in_off, out_off, _x in segs:
+        if mode == MODE_S:
+            out.append((m_off, ld, rows, cols, mode, -1, 0, out_off))
+            continue
+        span = cols if mode == MODE_N else rows
+        pos = in_off
+        end = in_off + span
+        while pos < end:
+            r = next(rr for rr in runs if rr[3] <= pos < rr[3] + rr[2])
+            take = min(end, r[3] + r[2]) - pos
+            k0 = pos - in_off
+            src = r[1] + (pos - r[3])
+            if mode == MODE_N:
+                out.append((m_off + k0, ld, rows, take, mode, r[0], src, out_off))
+            else:
+                out.append((m_off + k0 * ld, ld, take, cols, mode, r[0], src, out_off))
+            pos += take
+    return out
+
+
 def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
     """Flatten op tuples into arrays in the phased order; the fused order is a
     permutation (``fused_order[ticket] = op index``).  ``keep_waits_on``: in a partial program
@@ -760,6 +790,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
     n = len(order)
     ops = np.zeros((n, OP_FIELDS), dtype=np.int32)
     segs, pieces, runs, waits, sigs = [], [], [], [], []
+    mr_segs, mr_ranges = [], []
     in_max = xin_max = out_max = 0
     arena_elems = 0
     local_ctr = None
@@ -786,6 +817,9 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
         pc_b = len(pieces)
         pieces.extend(_pieces(ordered, has_x, stage_elems))
         pc_e = len(pieces)
+        mr_b = len(mr_segs)
+        mr_segs.extend(_resolve_inputs(ordered, in_runs))
+        mr_ranges.append((mr_b, len(mr_segs)))
         w_b = len(waits)
         waits.extend(wt)
         w_e = len(waits)
@@ -813,4 +847,6 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
         kinds=ops[:, 12].copy(),
         arena_elems=arena_elems,
         stage_elems=stage_elems,
+        mr_segs=np.asarray(mr_segs, dtype=np.int64).reshape(-1, MR_FIELDS),
+        mr_ranges=np.asarray(mr_ranges, dtype=np.int32).reshape(-1, 2),
     )

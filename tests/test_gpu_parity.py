@@ -138,3 +138,20 @@ def test_repeated_fused_launches_self_reset(mode):
     torch.cuda.synchronize()
     assert np.array_equal(w.cpu().numpy(), first)
     assert int(dop.counters.abs().sum()) == 0 and int(dop.ticket.item()) == 0
+
+
+@pytest.mark.parametrize("R", [16, 5])
+def test_multi_rhs_dmma(golden, R):
+    """Multi-RHS (config 5 path) on FP64 tensor cores vs the reference column loop."""
+    name, u, ex = golden
+    dop = _dev(u)
+    rng = np.random.default_rng(3)
+    for adjoint in (False, True):
+        n_in = u.shape[0] if adjoint else u.shape[1]
+        V = rng.standard_normal((n_in, R)) + 1j * rng.standard_normal((n_in, R))
+        W = dop.matmat(torch.from_numpy(V).cuda(), adjoint=adjoint).cpu().numpy()
+        ref = np.stack([oracle_matvec_uh(u, V[:, j], adjoint=adjoint) for j in range(R)], axis=1)
+        assert rel(W, ref) <= TOL, (name, adjoint, R, rel(W, ref))
+        if R == 16:  # column j of the block == a single-vector matvec of column j
+            w0 = dop.matvec(torch.from_numpy(np.ascontiguousarray(V[:, 0])).cuda(), adjoint=adjoint).cpu().numpy()
+            assert rel(W[:, 0], w0) <= 1e-13

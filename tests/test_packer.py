@@ -179,3 +179,19 @@ def test_bytes_accounting(golden):
     # the arena is the algorithmic bytes plus 128-B alignment padding only
     assert p.bytes_arena >= p.bytes_alg
     assert p.bytes_arena - p.bytes_alg <= 128 * (len(u.coeffs) + len(u.dense) + 4 * len(u.bct.nodes) + 8)
+
+
+def test_vm_matmat_multi_rhs(golden):
+    """Multi-RHS segments (one input source each) == the reference's column loop."""
+    from matvec_oracle import oracle_matvec_uh
+    from packed_vm import vm_matmat
+
+    name, u, ex = golden
+    p = pack(u)
+    rng = np.random.default_rng(11)
+    for adjoint in (False, True):
+        n_in = u.shape[0] if adjoint else u.shape[1]
+        V = rng.standard_normal((n_in, 5)) + 1j * rng.standard_normal((n_in, 5))
+        W = vm_matmat(p, V, adjoint=adjoint)
+        ref = np.stack([oracle_matvec_uh(u, V[:, j], adjoint=adjoint) for j in range(5)], axis=1)
+        assert rel(W, ref) <= TOL, (name, adjoint)
