@@ -124,6 +124,10 @@ int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int*
  * producer waiting for a free stage / an op slot, ops, pieces. */
 int uhmv_plan_set_profile(uhmv_plan* plan, void* counters);
 
+/* Diagnostics: measured FP64 tensor-core (DMMA m16n8k16) throughput of the device, TFLOP/s
+ * (the roofline denominator of the multi-RHS product; MEASURED_PEAKS.json has no FP64 entry). */
+int uhmv_dmma_peak(int device, double* tflops);
+
 int uhmv_plan_destroy(uhmv_plan* plan);
 
 /* Thread-local text of the last failure ("" if none). */

@@ -72,6 +72,7 @@ EXPORTS = (
     "uhmv_execute_mrhs",
     "uhmv_plan_info",
     "uhmv_plan_set_profile",
+    "uhmv_dmma_peak",
     "uhmv_plan_destroy",
     "uhmv_last_error",
 )
@@ -103,6 +104,8 @@ def lib():
     pi = ctypes.POINTER(i32)
     L.uhmv_plan_info.argtypes = [vp, i32, i32, pi, pi, pi, pi]
     L.uhmv_plan_info.restype = i32
+    L.uhmv_dmma_peak.argtypes = [i32, ctypes.POINTER(ctypes.c_double)]
+    L.uhmv_dmma_peak.restype = i32
     L.uhmv_plan_set_profile.argtypes = [vp, vp]
     L.uhmv_plan_set_profile.restype = i32
     L.uhmv_plan_destroy.argtypes = [vp]

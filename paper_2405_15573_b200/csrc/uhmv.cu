@@ -771,6 +771,36 @@ int uhmv_plan_set_profile(uhmv_plan* plan, void* counters) {
     return UHMV_OK;
 }
 
+int uhmv_dmma_peak(int device, double* tflops) {
+    if (!tflops) return fail(UHMV_EINVAL, "uhmv_dmma_peak: null output");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    double* sink = nullptr;
+    e = cudaMalloc(&sink, sizeof(double));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    const int grid = sms * 8, iters = 4096;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    mrhs::dmma_peak_kernel<<<grid, 128>>>(64, sink);  // warm-up
+    cudaEventRecord(a);
+    mrhs::dmma_peak_kernel<<<grid, 128>>>(iters, sink);
+    cudaEventRecord(b);
+    e = cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return cuda_fail(e, "dmma_peak_kernel");
+    // 4 MMAs per iteration per warp, m16n8k16 = 16*8*16 multiply-adds = 4096 flops
+    const double flops = 4096.0 * 4.0 * iters * (grid * 4.0);
+    *tflops = flops / (ms * 1e-3) / 1e12;
+    return UHMV_OK;
+}
+
 int uhmv_plan_destroy(uhmv_plan* plan) {
     delete plan;
     return UHMV_OK;

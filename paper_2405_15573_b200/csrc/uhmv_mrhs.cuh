@@ -271,4 +271,24 @@ __global__ void __launch_bounds__(kThreads) uhmv_mrhs_kernel(const Params p) {
     }
 }
 
+// FP64 tensor-core peak probe: independent DMMA chains in registers, no memory traffic.
+__global__ void __launch_bounds__(128) dmma_peak_kernel(int iters, double* sink) {
+    double a[8], b[4], c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0}, c2[4] = {0, 0, 0, 0},
+                      c3[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = 1e-3 * (threadIdx.x + i);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) b[i] = 1e-3 * (blockIdx.x + i);
+    for (int it = 0; it < iters; ++it) {
+        dmma(c0, a, b);
+        dmma(c1, a, b);
+        dmma(c2, a, b);
+        dmma(c3, a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s += c0[i] + c1[i] + c2[i] + c3[i];
+    if (s == 12345.678) *sink = s;
+}
+
 }  // namespace mrhs

@@ -12,6 +12,13 @@ from paper_2405_15573_b200 import workloads  # noqa: E402
 from paper_2405_15573_b200.device import DeviceOperator  # noqa: E402
 from paper_2405_15573_b200.packer import pack  # noqa: E402
 
+import ctypes  # noqa: E402
+
+from paper_2405_15573_b200 import _lib  # noqa: E402
+
+pk = ctypes.c_double()
+_lib.check(_lib.lib().uhmv_dmma_peak(0, ctypes.byref(pk)), "dmma_peak")
+print(f"measured DMMA peak: {pk.value:.2f} TFLOP/s")
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 u = workloads.build_operator(cfg)
