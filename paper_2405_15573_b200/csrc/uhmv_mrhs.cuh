@@ -175,8 +175,7 @@ __global__ void __launch_bounds__(kThreads) uhmv_mrhs_kernel(const Params p) {
                 for (int si = s; si < e; ++si) {
                     const Seg sg = load_seg(p, si);
                     const double* T = reinterpret_cast<const double*>(p.arena + sg.m_off);
-                    const bool in_x = (sg.in_buf == kBufX);
-                    const double2* IN = (in_x ? p.x : p.work) + sg.in_abs * (int64_t)R + rbase;
+                    const double2* IN = (sg.in_buf == kBufX ? p.x : p.work) + sg.in_abs * (int64_t)R + rbase;
                     const int K2 = 2 * (hm ? sg.rows : sg.cols);
                     const int nlim = hm ? sg.cols : sg.rows;
                     for (int kb = 0; kb < K2; kb += 16) {
@@ -191,10 +190,12 @@ __global__ void __launch_bounds__(kThreads) uhmv_mrhs_kernel(const Params p) {
                                 const int c = kp & 1;
                                 double val = 0.0;
                                 if (kp < K2) {
-                                    // N: {ir,-ii; ii,ir}   H: {ir,ii; ii,-ir}: one double per lane
-                                    const double* zp = reinterpret_cast<const double*>(
-                                                           IN + (int64_t)(kp >> 1) * R + r) + (d ^ c);
-                                    val = in_x ? __ldg(zp) : __ldcg(zp);  // work: coherent (L2)
+                                    // N: {ir,-ii; ii,ir}   H: {ir,ii; ii,-ir}.  x is read-only; a
+                                    // work row (R >= 16 complex, 256-B aligned) is written once per
+                                    // launch before any reader passes its dependency poll, whose
+                                    // ld.acquire.gpu invalidates L1
+                                    const double2 z = IN[(int64_t)(kp >> 1) * R + r];
+                                    val = (d ^ c) ? z.y : z.x;
                                     if (!hm && d == 0 && c == 1) val = -val;
                                     if (hm && d == 1 && c == 1) val = -val;
                                 }
