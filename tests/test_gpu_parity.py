@@ -155,3 +155,18 @@ def test_multi_rhs_dmma(golden, R):
         if R == 16:  # column j of the block == a single-vector matvec of column j
             w0 = dop.matvec(torch.from_numpy(np.ascontiguousarray(V[:, 0])).cuda(), adjoint=adjoint).cpu().numpy()
             assert rel(W[:, 0], w0) <= 1e-13
+
+
+def test_power_iteration_on_device(golden):
+    """Device-resident spectral norm / compression error == the reference's values."""
+    from matvec_oracle import farfield_only
+    from paper_2405_15573_b200 import verification
+
+    name, u, ex = golden
+    if "pi_est" not in ex:
+        pytest.skip("no verification values stored")
+    est = verification.spectral_norm_estimate(u, iters=30, seed=0)
+    assert abs(est - float(ex["pi_est"])) <= 1e-10 * float(ex["pi_est"])
+    rep = verification.compression_error(u, farfield_only(u), iters=30, seed=0)
+    assert abs(rep.rel_spectral_estimate - float(ex["ce_rel"])) <= 1e-9 * float(ex["ce_rel"])
+    assert rep.iterations == int(ex["ce_used"])

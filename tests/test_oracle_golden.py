@@ -59,3 +59,21 @@ def test_oracle_result_dtype():
     assert u._dtype == np.float64
     assert oracle_matvec_uh(u, ex["vf_0"]).dtype == np.float64
     assert oracle_matvec_uh(u, ex["vf_0"] + 0j).dtype == np.complex128
+
+
+def test_power_iteration_oracle_pinned(golden):
+    """oracle/verification_oracle.py reproduces the reference power iteration values."""
+    from matvec_oracle import farfield_only
+    from verification_oracle import compression_error, power_iteration
+
+    name, u, ex = golden
+    if "x_pi_est" not in ex and "pi_est" not in ex:
+        pytest.skip("no verification values stored")
+    est, used, resid = power_iteration(
+        lambda v: oracle_matvec_uh(u, v), lambda v: oracle_matvec_uh(u, v, adjoint=True), u.shape[1], 30, 0
+    )
+    assert abs(est - float(ex["pi_est"])) <= 1e-10 * float(ex["pi_est"])
+    assert used == int(ex["pi_used"])
+    rel, used, resid = compression_error(u, farfield_only(u), iters=30, seed=0)
+    assert abs(rel - float(ex["ce_rel"])) <= 1e-9 * float(ex["ce_rel"])
+    assert used == int(ex["ce_used"])

@@ -92,9 +92,26 @@ def outputs(u, vecs, nvec, with_dense=True):
     return res
 
 
+def verification_values(u):
+    """Reference power iteration (verification.py:54-138) on the operator: the spectral norm
+    estimate and the compression error against its own farfield-only view."""
+    from uhm_kit.verification import _as_operator, _power_iteration, compression_error
+
+    ap, aa, n = _as_operator(u)
+    est, used, resid = _power_iteration(ap, aa, n, 30, 0)
+    rep = compression_error(u, far_view(u), iters=30, seed=0)
+    return {
+        "pi_est": np.float64(est), "pi_used": np.int64(used), "pi_resid": np.float64(resid),
+        "ce_rel": np.float64(rep.rel_spectral_estimate), "ce_used": np.int64(rep.iterations),
+        "ce_resid": np.float64(rep.residual),
+    }
+
+
 def emit(name, u, complex_vec, seeds=(1, 2), with_dense=True, exact=None, **meta):
     vecs = vectors(u.shape[1], u.shape[0], complex_vec, seeds)
     res = outputs(u, vecs, len(seeds), with_dense)
+    if len(u.coeffs) and len(u.dense):
+        res.update(verification_values(u))
     if exact is not None:  # the exact kernel matrix (EntryOracle.to_dense) for the 1e-3/1e-4 pins
         for k in range(len(seeds)):
             res[f"exact_fwd_{k}"] = exact @ vecs[f"vf_{k}"]
