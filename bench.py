@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--adjoint", action="store_true")
     ap.add_argument("--view", default="full", choices=["full", "far", "near"], help="diagnostics: parity view")
+    ap.add_argument("--format", default="uh", choices=["uh", "h"],
+                    help="uh: uniform H-matrix (the hot path); h: the source H-matrix (matvec_h)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     return ap.parse_args()
@@ -189,7 +191,9 @@ def main():
     torch.cuda.set_device(dev)
 
     t_build = time.perf_counter()
-    u = workloads.build_operator(args.config)
+    u = workloads.build_operator(args.config) if args.format == "uh" else workloads.build_h_operator(args.config)
+    if args.format == "h":
+        config["format"] = "H-matrix (matvec_h, hmatrix.py:143-184), ranks of the reference's assemble_h"
     if args.view != "full":
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         from matvec_oracle import farfield_only, nearfield_only
@@ -207,7 +211,12 @@ def main():
     else:
         from paper_2405_15573_b200.device import DeviceOperator
 
-        packed = pack(u)
+        if args.format == "h":
+            from paper_2405_15573_b200.packer_h import pack_h
+
+            packed = pack_h(u)
+        else:
+            packed = pack(u)
         op = DeviceOperator(packed, device=dev)
     t_build = time.perf_counter() - t_build
 
@@ -349,7 +358,7 @@ def main():
     }
     if os.environ.get("UHMV_PROFILE") and world == 1 and args.mode == "bulk":
         line["engine_cycles"] = op.profile(args.adjoint, args.mode)
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and args.format == "uh":
         line["cpu_baseline"] = cpu_baseline(u, x_np, args.cpu_sample_s) if not args.adjoint else None
     print(json.dumps(line), flush=True)
     if world > 1:

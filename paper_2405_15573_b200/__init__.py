@@ -4,7 +4,7 @@ The reference (arXiv 2405.15573, package ``uhm_kit``) builds the operator; this 
 packs it into HBM and replaces only the product (reference uniform.py:476-556).
 """
 
-from .matvec import clear_cache, device_operator, matmat_uh, matvec_uh
+from .matvec import clear_cache, device_operator, matmat_uh, matvec_h, matvec_uh
 from .packer import PackedOperator, pack
 from .uh_types import (
     BlockClusterTree,
@@ -13,13 +13,16 @@ from .uh_types import (
     ClusterBasis,
     ClusterTree,
     CoefficientPair,
+    HMatrix,
     MatvecStats,
+    SVDForm,
     UniformHMatrix,
 )
 
 __all__ = [
     "matvec_uh",
     "matmat_uh",
+    "matvec_h",
     "device_operator",
     "clear_cache",
     "pack",
@@ -32,7 +35,10 @@ __all__ = [
     "BlockClusterTree",
     "BlockNode",
     "MatvecStats",
+    "HMatrix",
+    "SVDForm",
     "install",
+    "uninstall",
 ]
 
 
@@ -44,11 +50,26 @@ def install():
     (bound at import, verification.py:20).  Returns the originals for restoring.
     """
     import uhm_kit
+    import uhm_kit.hmatrix
     import uhm_kit.uniform
     import uhm_kit.verification
 
-    orig = (uhm_kit.matvec_uh, uhm_kit.uniform.matvec_uh, uhm_kit.verification.matvec_uh)
-    uhm_kit.matvec_uh = matvec_uh
-    uhm_kit.uniform.matvec_uh = matvec_uh
-    uhm_kit.verification.matvec_uh = matvec_uh
+    targets = [
+        (uhm_kit, "matvec_uh", matvec_uh),
+        (uhm_kit.uniform, "matvec_uh", matvec_uh),
+        (uhm_kit.verification, "matvec_uh", matvec_uh),
+        # the H-matrix product too (hmatrix.py:143-184; HMatrix.matvec resolves it at call time)
+        (uhm_kit, "matvec_h", matvec_h),
+        (uhm_kit.hmatrix, "matvec_h", matvec_h),
+        (uhm_kit.verification, "matvec_h", matvec_h),
+    ]
+    orig = [(mod, name, getattr(mod, name)) for mod, name, _ in targets]
+    for mod, name, fn in targets:
+        setattr(mod, name, fn)
     return orig
+
+
+def uninstall(orig) -> None:
+    """Restore the bindings returned by :func:`install`."""
+    for mod, name, fn in orig:
+        setattr(mod, name, fn)

@@ -26,13 +26,15 @@ import numpy as np
 from .device import DeviceOperator
 from .packer import pack
 
-__all__ = ["matvec_uh", "matmat_uh", "device_operator", "clear_cache"]
+__all__ = ["matvec_uh", "matmat_uh", "matvec_h", "device_operator", "clear_cache"]
 
 _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
 def _fingerprint(u):
+    if hasattr(u, "admissible"):  # HMatrix
+        return (id(u.bct), id(u.admissible), len(u.admissible), id(u.dense), len(u.dense))
     return (
         id(u.bct),
         id(u.row_basis),
@@ -45,8 +47,17 @@ def _fingerprint(u):
     )
 
 
+def _pack_any(u):
+    if hasattr(u, "admissible") and not hasattr(u, "coeffs"):
+        from .packer_h import pack_h
+
+        return pack_h(u)
+    return pack(u)
+
+
 def device_operator(u, device=None) -> DeviceOperator:
-    """Packed, HBM-resident form of ``u`` (built on first use, then cached)."""
+    """Packed, HBM-resident form of ``u`` -- a UniformHMatrix or an HMatrix (built on first
+    use, then cached)."""
     key = id(u)
     fp = _fingerprint(u)
     with _cache_lock:
@@ -55,7 +66,7 @@ def device_operator(u, device=None) -> DeviceOperator:
             ref, fp_old, dop = hit
             if ref() is u and fp_old == fp and (device is None or str(dop.device) == str(device)):
                 return dop
-        dop = DeviceOperator(pack(u), device=device)
+        dop = DeviceOperator(_pack_any(u), device=device)
         try:
             ref = weakref.ref(u, lambda _r, k=key: _cache.pop(k, None))
         except TypeError:  # not weak-referenceable: keep it alive with the plan
@@ -106,6 +117,13 @@ def matvec_uh(u, v, workers: int = 1, adjoint: bool = False, stats=None):
     return w.real.astype(dtype)
 
 
+def matvec_h(h, v, workers: int = 1, adjoint: bool = False, stats=None):
+    """Drop-in for the H-matrix product ``matvec_h`` (reference hmatrix.py:143-184): same
+    signature, ValueError, result dtype (hmatrix.py:155-157) and stats semantics (one count
+    per admissible and dense block), run on the same sm_100a engine."""
+    return matvec_uh(h, v, workers=workers, adjoint=adjoint, stats=stats)
+
+
 def matmat_uh(u, V, adjoint: bool = False):
     """Multi-RHS extension (BASELINE config 5): ``(n_in, nrhs)`` -> ``(n_out, nrhs)``.
 
@@ -119,8 +137,14 @@ def matmat_uh(u, V, adjoint: bool = False):
         raise ValueError(f"block of shape {V.shape} does not match operator input size {n_in}")
     dtype = np.result_type(V.dtype, u._dtype)
     dop = device_operator(u)
-    cols = [dop.matvec_host(V[:, j].astype(np.complex128), adjoint=adjoint) for j in range(V.shape[1])]
-    W = np.stack(cols, axis=1) if cols else np.zeros((n_rows if not adjoint else n_cols, 0), np.complex128)
+    import torch
+
+    n_out = n_cols if adjoint else n_rows
+    if V.shape[1] == 0:
+        W = np.zeros((n_out, 0), np.complex128)
+    else:
+        X = torch.from_numpy(np.ascontiguousarray(V, dtype=np.complex128)).to(dop.device)
+        W = dop.matmat(X, adjoint=adjoint).cpu().numpy()
     if np.issubdtype(dtype, np.complexfloating):
         return W.astype(dtype, copy=False)
     return W.real.astype(dtype)

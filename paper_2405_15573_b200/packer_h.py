@@ -1,0 +1,266 @@
+"""Packer for the H-matrix product ``matvec_h`` (reference hmatrix.py:143-184, paper Alg 4).
+
+Same arena + op-program format as :mod:`packer` (so the same sm_100a engines run it), but
+every admissible block carries its own bases (SVDForm U_b diag(sigma_b) V_b^H,
+lowrank.py:51-64).  Stored per block (128-B aligned, contiguous):
+  W_b = V_b diag(sigma_b)   |t| x k_b   (sigma folded in: the product needs only sigma V^H x)
+  U_b                       |s| x k_b
+  D_b                       dense leaves, as for the uniform format
+Forward: P1 per column-leaf chunk: partial_b = W_b[chunk]^H x[chunk] for every block whose
+column cluster contains the chunk; RED: y_b = sum of partials; FAR per row-leaf chunk:
+w[chunk] += sum_b U_b[chunk,:] y_b; NEAR: w[chunk] += D_b x.  The adjoint swaps the roles
+(P1 over U_b, FAR over W_b: V diag(sigma) (U^H x)).  No coupling stage -- which is exactly
+what the uniform format trades for smaller shared bases.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .packer import (
+    BUF_ARENA,
+    BUF_W,
+    BUF_WORK,
+    BUF_X,
+    KIND_FAR,
+    KIND_NEAR,
+    KIND_P1,
+    KIND_RED,
+    MODE_H,
+    MODE_N,
+    MODE_S,
+    P1_CHUNK,
+    ROWS_PER_CHUNK,
+    RUN_ATOMIC,
+    STAGE_ELEMS,
+    PackedOperator,
+    _align,
+    _chunks,
+    _finish,
+    _leaves_under,
+    _seg,
+)
+
+__all__ = ["pack_h"]
+
+P1_MAX_OUT = 512  # output entries per P1 op (bounds the consumers' shared-memory vector)
+
+
+def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = None,
+           near_interleave=(0.35, 0.1, 0.2, 0.35)) -> PackedOperator:
+    import os
+
+    if rows_per_chunk is None:
+        rows_per_chunk = int(os.environ.get("UHMV_ROWS_PER_CHUNK", ROWS_PER_CHUNK))
+    if stage_elems is None:
+        stage_elems = int(os.environ.get("UHMV_STAGE_ELEMS", STAGE_ELEMS))
+    bct = h.bct
+    n_rows, n_cols = bct.shape
+    rnodes, cnodes = bct.row_tree.nodes, bct.col_tree.nodes
+    adm = [b for b in sorted(h.admissible) if h.admissible[b].rank > 0]
+    kb = {b: int(h.admissible[b].rank) for b in adm}
+    offs, cursor = {}, 0
+
+    def alloc(key, n):
+        nonlocal cursor
+        offs[key] = cursor
+        cursor += _align(n)
+
+    for b in adm:
+        blk = bct.nodes[b]
+        alloc(("W", b), cnodes[blk.col].size * kb[b])
+        alloc(("U", b), rnodes[blk.row].size * kb[b])
+    dense_by_rleaf, dense_by_cleaf = {}, {}
+    for bid in h.dense:
+        blk = bct.nodes[bid]
+        dense_by_rleaf.setdefault(blk.row, []).append(bid)
+        dense_by_cleaf.setdefault(blk.col, []).append(bid)
+    for r in dense_by_rleaf:
+        dense_by_rleaf[r].sort(key=lambda bid: cnodes[bct.nodes[bid].col].lo)
+    for c in dense_by_cleaf:
+        dense_by_cleaf[c].sort(key=lambda bid: rnodes[bct.nodes[bid].row].lo)
+    for r in sorted(dense_by_rleaf, key=lambda r: rnodes[r].lo):
+        for bid in dense_by_rleaf[r]:
+            rr, cc = bct.block_shape(bid)
+            alloc(("D", bid), rr * cc)
+    arena = np.zeros(max(cursor, 8), dtype=np.complex128)
+    elems = 0
+    for b in adm:
+        f = h.admissible[b]
+        wmat = np.asarray(f.V, dtype=np.complex128) * np.asarray(f.sigma, dtype=np.float64)[None, :]
+        arena[offs[("W", b)] : offs[("W", b)] + wmat.size] = wmat.reshape(-1)
+        um = np.asarray(f.U, dtype=np.complex128)
+        arena[offs[("U", b)] : offs[("U", b)] + um.size] = um.reshape(-1)
+        elems += wmat.size + um.size
+    dense_elems = 0
+    for bid, d in h.dense.items():
+        arena[offs[("D", bid)] : offs[("D", bid)] + d.size] = np.asarray(d).reshape(-1)
+        dense_elems += d.size
+    geo = dict(bct=bct, adm=adm, kb=kb, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf)
+    kw = dict(rows_per_chunk=rows_per_chunk, stage_elems=stage_elems, near_interleave=near_interleave)
+    fwd, work_f = _build_h(geo, adjoint=False, **kw)
+    adj, work_a = _build_h(geo, adjoint=True, **kw)
+    # reference storage_report (hmatrix.py:187-208) counts k (m + n + 1); sigma is folded here
+    return PackedOperator(
+        n_rows=n_rows, n_cols=n_cols, dtype=np.dtype(h._dtype), arena=arena,
+        work_len=max(work_f, work_a, 1), fwd=fwd, adj=adj, n_adm=len(h.admissible),
+        n_dense=len(h.dense), bytes_alg=16 * (elems + dense_elems), bytes_arena=16 * int(arena.size),
+        storage=dict(bases=16 * elems, coupling=0, dense=16 * dense_elems, format="H"),
+    )
+
+
+def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
+    bct, adm, kb, offs = geo["bct"], geo["adm"], geo["kb"], geo["offs"]
+    if adjoint:
+        in_tree, out_tree = bct.row_tree, bct.col_tree
+        in_key, out_key = "U", "W"
+        dense_by_outleaf = geo["dense_by_cleaf"]
+
+        def in_c(b):
+            return bct.nodes[b].row
+
+        def out_c(b):
+            return bct.nodes[b].col
+    else:
+        in_tree, out_tree = bct.col_tree, bct.row_tree
+        in_key, out_key = "W", "U"
+        dense_by_outleaf = geo["dense_by_rleaf"]
+
+        def in_c(b):
+            return bct.nodes[b].col
+
+        def out_c(b):
+            return bct.nodes[b].row
+    in_nodes, out_nodes = in_tree.nodes, out_tree.nodes
+    in_leaves, in_span = _leaves_under(in_tree)
+    out_leaves, out_span = _leaves_under(out_tree)
+    in_blocks = [[] for _ in in_leaves]  # blocks whose input cluster contains the leaf
+    out_blocks = [[] for _ in out_leaves]
+    for b in adm:
+        a, e = in_span[in_c(b)]
+        for p in range(a, e):
+            in_blocks[p].append(b)
+        a, e = out_span[out_c(b)]
+        for p in range(a, e):
+            out_blocks[p].append(b)
+
+    work = 0
+
+    def walloc(n):
+        nonlocal work
+        o = work
+        work += int(n)
+        return o
+
+    n_ctr = 0
+
+    def ctr():
+        nonlocal n_ctr
+        n_ctr += 1
+        return n_ctr - 1
+
+    # P1 items: (leafpos, lo, hi, block group)
+    items = []
+    for p, leaf in enumerate(in_leaves):
+        bl = in_blocks[p]
+        if not bl:
+            continue
+        n = in_nodes[leaf]
+        groups, cur, tot = [], [], 0
+        for b in bl:
+            if cur and tot + kb[b] > P1_MAX_OUT:
+                groups.append(cur)
+                cur, tot = [], 0
+            cur.append(b)
+            tot += kb[b]
+        groups.append(cur)
+        for a, e in _chunks(n.lo, n.hi, P1_CHUNK):
+            for grp in groups:
+                items.append((p, a, e, grp))
+    chunks_of = {b: [] for b in adm}
+    for idx, (p, a, e, grp) in enumerate(items):
+        for b in grp:
+            chunks_of[b].append(idx)
+    y_off, part_off = {}, {}
+    for b in adm:
+        y_off[b] = walloc(kb[b])
+    for b in adm:
+        part_off[b] = y_off[b] if len(chunks_of[b]) == 1 else walloc(len(chunks_of[b]) * kb[b])
+    c_part = {b: ctr() for b in adm}
+    c_y = {b: ctr() for b in adm}
+    ops = {k: [] for k in range(7)}
+    for idx, (p, a, e, grp) in enumerate(items):
+        segs, outs, sigs = [], [], []
+        oo = 0
+        for b in grp:
+            k = kb[b]
+            lo_c = in_nodes[in_c(b)].lo
+            segs.append(_seg(offs[(in_key, b)] + (a - lo_c) * k, BUF_ARENA, e - a, k, k, MODE_H, 0, oo, a))
+            outs.append((BUF_WORK, part_off[b] + chunks_of[b].index(idx) * k, k, oo, 0))
+            sigs.append(c_part[b])
+            oo += k
+        ops[KIND_P1].append((KIND_P1, e - a, oo, [(BUF_X, a, e - a, 0, 0)], segs, outs, [], sigs, (e - a) * oo))
+    y_wait = {}
+    for b in adm:
+        nchunk = len(chunks_of[b])
+        if nchunk <= 1:
+            y_wait[b] = (c_part[b], nchunk)
+            continue
+        k = kb[b]
+        ops[KIND_RED].append(
+            (KIND_RED, 0, k, [], [_seg(part_off[b], BUF_WORK, nchunk, k, k, MODE_S, 0, 0)],
+             [(BUF_WORK, y_off[b], k, 0, 0)], [(c_part[b], nchunk)], [c_y[b]], nchunk * k)
+        )
+        y_wait[b] = (c_y[b], 1)
+    for p, leaf in enumerate(out_leaves):
+        n = out_nodes[leaf]
+        dlist = dense_by_outleaf.get(leaf, [])
+        near_chunks = _chunks(n.lo, n.hi, rows_per_chunk) if not adjoint else [(n.lo, n.hi)]
+        for a, e in near_chunks:
+            if not dlist:
+                continue
+            rows = e - a
+            in_runs, segs, pos, nbytes = [], [], 0, 0
+            for bid in dlist:
+                blk = bct.nodes[bid]
+                if not adjoint:
+                    c = bct.col_tree.nodes[blk.col]
+                    in_runs.append((BUF_X, c.lo, c.size, pos, 0))
+                    segs.append(_seg(offs[("D", bid)] + (a - n.lo) * c.size, BUF_ARENA, rows, c.size, c.size, MODE_N, pos, 0, c.lo))
+                    pos += c.size
+                    nbytes += rows * c.size
+                else:
+                    r = bct.row_tree.nodes[blk.row]
+                    in_runs.append((BUF_X, r.lo, r.size, pos, 0))
+                    segs.append(_seg(offs[("D", bid)], BUF_ARENA, r.size, n.size, n.size, MODE_H, pos, 0, r.lo))
+                    pos += r.size
+                    nbytes += r.size * n.size
+            ops[KIND_NEAR].append((KIND_NEAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], [], [], nbytes))
+        bl = out_blocks[p]
+        if not bl:
+            continue
+        for a, e in _chunks(n.lo, n.hi, rows_per_chunk):
+            rows = e - a
+            in_runs, segs, waits, pos = [], [], [], 0
+            for b in bl:
+                k = kb[b]
+                lo_c = out_nodes[out_c(b)].lo
+                in_runs.append((BUF_WORK, y_off[b], k, pos, 0))
+                segs.append(_seg(offs[(out_key, b)] + (a - lo_c) * k, BUF_ARENA, rows, k, k, MODE_N, pos, 0))
+                waits.append(y_wait[b])
+                pos += k
+            ops[KIND_FAR].append(
+                (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], sorted(set(waits)), [], rows * pos)
+            )
+    for k in ops:
+        ops[k].sort(key=lambda o: -o[-1])
+    near = ops[KIND_NEAR]
+    f = np.cumsum([0.0] + list(near_interleave))
+    f = f / f[-1]
+    cut = [int(round(x * len(near))) for x in f]
+    parts = [near[cut[i] : cut[i + 1]] for i in range(len(near_interleave))]
+    while len(parts) < 4:
+        parts.append([])
+    phased = [ops[KIND_P1] + near, ops[KIND_RED], ops[KIND_FAR]]
+    fused = ops[KIND_P1] + parts[0] + ops[KIND_RED] + parts[1] + parts[2] + parts[3] + ops[KIND_FAR]
+    return _finish(phased, fused, n_ctr, stage_elems=stage_elems), work

@@ -25,6 +25,8 @@ from .uh_types import (
     ClusterBasis,
     ClusterTree,
     CoefficientPair,
+    HMatrix,
+    SVDForm,
     UniformHMatrix,
 )
 
@@ -41,6 +43,8 @@ __all__ = [
     "load_uh",
     "save_bct",
     "load_bct",
+    "save_h",
+    "load_h",
 ]
 
 
@@ -235,3 +239,46 @@ def load_bct(path):
         d = {k: z[k] for k in z.files}
     extra = {k[2:]: v for k, v in d.items() if k.startswith("x_")}
     return bct_from_arrays(d), extra
+
+
+def h_to_arrays(h) -> dict:
+    """HMatrix (reference hmatrix.py:39-69 or mirror) -> arrays (SVD factors + dense)."""
+    out = bct_to_arrays(h.bct)
+    out["format_version"] = np.int64(FORMAT_VERSION)
+    ids = sorted(h.admissible)
+    out["hf_ids"] = np.asarray(ids, dtype=np.int64)
+    out["hu_shape"], out["hu_data"] = _pack_mats({b: h.admissible[b].U for b in ids}, ids)
+    out["hv_shape"], out["hv_data"] = _pack_mats({b: h.admissible[b].V for b in ids}, ids)
+    sig = [np.asarray(h.admissible[b].sigma, dtype=np.float64) for b in ids]
+    out["hs_len"] = np.array([len(x) for x in sig], dtype=np.int64)
+    out["hs_data"] = np.concatenate(sig) if sig else np.zeros(0)
+    dids = sorted(h.dense)
+    out["dn_ids"] = np.asarray(dids, dtype=np.int64)
+    out["dn_shape"], out["dn_data"] = _pack_mats(h.dense, dids)
+    out["dense_order"] = np.asarray(getattr(h, "_dense_order", dids), dtype=np.int64)
+    return out
+
+
+def h_from_arrays(d) -> HMatrix:
+    bct = bct_from_arrays(d)
+    ids = [int(b) for b in d["hf_ids"]]
+    us = _unpack_mats(d["hf_ids"], d["hu_shape"], d["hu_data"])
+    vs = _unpack_mats(d["hf_ids"], d["hv_shape"], d["hv_data"])
+    off = np.concatenate([[0], np.cumsum(d["hs_len"])]).astype(np.int64)
+    adm = {b: SVDForm(us[b], d["hs_data"][off[i] : off[i + 1]].copy(), vs[b]) for i, b in enumerate(ids)}
+    dn_all = _unpack_mats(d["dn_ids"], d["dn_shape"], d["dn_data"])
+    order = [int(b) for b in d["dense_order"]] if "dense_order" in d else sorted(dn_all)
+    return HMatrix(bct, adm, {b: dn_all[b] for b in order})
+
+
+def save_h(h, path, **extra) -> None:
+    arrs = h_to_arrays(h)
+    arrs.update({f"x_{k}": np.asarray(v) for k, v in extra.items()})
+    np.savez_compressed(path, **arrs)
+
+
+def load_h(path):
+    with np.load(path) as z:
+        d = {k: z[k] for k in z.files}
+    extra = {k[2:]: v for k, v in d.items() if k.startswith("x_")}
+    return h_from_arrays(d), extra

@@ -33,6 +33,8 @@ __all__ = [
     "CoefficientPair",
     "UniformHMatrix",
     "MatvecStats",
+    "SVDForm",
+    "HMatrix",
 ]
 
 
@@ -182,3 +184,46 @@ class MatvecStats:
     def count(self, k: int = 1) -> None:
         with self._lock:
             self.leaves_touched += k
+
+
+@dataclass
+class SVDForm:
+    """Mirror of lowrank.SVDForm (lowrank.py:51-64): block ~= U diag(sigma) V^H."""
+
+    U: np.ndarray
+    sigma: np.ndarray
+    V: np.ndarray
+
+    @property
+    def rank(self) -> int:
+        return len(self.sigma)
+
+
+@dataclass
+class HMatrix:
+    """Mirror of hmatrix.HMatrix (hmatrix.py:39-69): SVD-form admissible blocks + dense."""
+
+    bct: BlockClusterTree
+    admissible: dict
+    dense: dict
+    tol_used: object = None
+
+    def __post_init__(self) -> None:
+        shape = self.bct.block_shape
+        self._adm_order = sorted(self.admissible, key=lambda b: -(self.admissible[b].rank * sum(shape(b))))
+        self._dense_order = sorted(self.dense, key=lambda b: -(shape(b)[0] * shape(b)[1]))
+        dtype = np.dtype(np.float64)
+        for f in self.admissible.values():
+            dtype = np.result_type(dtype, f.U.dtype)
+        for d in self.dense.values():
+            dtype = np.result_type(dtype, d.dtype)
+        self._dtype = dtype
+
+    @property
+    def shape(self) -> tuple:
+        return self.bct.shape
+
+    def matvec(self, v, workers: int = 1, adjoint: bool = False):
+        from .matvec import matvec_h
+
+        return matvec_h(self, v, workers=workers, adjoint=adjoint)

@@ -126,6 +126,33 @@ def build_operator(cfg: int, seed: int = 0):
     return UniformHMatrix(bct, ClusterBasis(rb), ClusterBasis(cb), coeffs, dense)
 
 
+def build_h_operator(cfg: int, seed: int = 0):
+    """Seeded HMatrix (mirror types) with the block ranks of the H-matrix the reference
+    assembled for config ``cfg`` (``assemble_h`` at 1e-6/1e-7, the source of the uniform
+    compression): U_b, V_b scaled complex Gaussian, sigma_b decaying, dense leaves as
+    build_operator.  Same shapes and bytes as the reference's H-matrix."""
+    from .uh_types import HMatrix, SVDForm
+
+    bct, d = load_structure(cfg)
+    if "x_kb_h" not in d:
+        raise ValueError(f"config {cfg} fixture has no H-matrix ranks")
+    kh = d["x_kb_h"]
+    rnodes, cnodes = bct.row_tree.nodes, bct.col_tree.nodes
+    rng = np.random.default_rng([seed, 5])
+    groups = {}
+    for b in bct.admissible_leaves:
+        blk = bct.nodes[b]
+        groups.setdefault((rnodes[blk.row].size, cnodes[blk.col].size, int(kh[b])), []).append(b)
+    adm = {}
+    for (m, n, k), bs in sorted(groups.items()):
+        qu = _gauss(rng, (len(bs), m, k)) / np.sqrt(max(m, 1))
+        qv = _gauss(rng, (len(bs), n, k)) / np.sqrt(max(n, 1))
+        for i, b in enumerate(bs):
+            adm[b] = SVDForm(qu[i], np.geomspace(1.0, 1e-6, k) if k else np.zeros(0), qv[i])
+    u = build_operator(cfg, seed)
+    return HMatrix(bct, adm, u.dense)
+
+
 def seeded_vector(n: int, seed: int = 0) -> np.ndarray:
     rng = np.random.default_rng(seed)
     re = rng.standard_normal(n)

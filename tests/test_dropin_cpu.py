@@ -30,10 +30,14 @@ def test_install_patches_reference_names():
     import uhm_kit.uniform
     import uhm_kit.verification
 
+    import uhm_kit.hmatrix
+
     orig = pk.install()
     try:
         assert uhm_kit.matvec_uh is pk.matvec_uh
         assert uhm_kit.uniform.matvec_uh is pk.matvec_uh
         assert uhm_kit.verification.matvec_uh is pk.matvec_uh
+        assert uhm_kit.hmatrix.matvec_h is pk.matvec_h
     finally:
-        uhm_kit.matvec_uh, uhm_kit.uniform.matvec_uh, uhm_kit.verification.matvec_uh = orig
+        pk.uninstall(orig)
+    assert uhm_kit.matvec_uh is not pk.matvec_uh

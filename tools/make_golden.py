@@ -34,7 +34,8 @@ from uhm_kit import (  # noqa: E402
     to_dense_uh,
 )
 
-from paper_2405_15573_b200.uh_io import save_uh  # noqa: E402
+from paper_2405_15573_b200.uh_io import save_h, save_uh  # noqa: E402
+from uhm_kit import matvec_h, to_dense  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
 
@@ -121,6 +122,22 @@ def emit(name, u, complex_vec, seeds=(1, 2), with_dense=True, exact=None, **meta
           f"size={os.path.getsize(path) / 1e6:.2f} MB")
 
 
+def emit_h(name, h, complex_vec, seeds=(1,)):
+    """H-matrix fixture: reference matvec_h outputs (hmatrix.py:143-184), fwd + adjoint."""
+    vecs = vectors(h.shape[1], h.shape[0], complex_vec, seeds)
+    res = {}
+    for k in range(len(seeds)):
+        res[f"ref_fwd_{k}"] = matvec_h(h, vecs[f"vf_{k}"])
+        res[f"ref_adj_{k}"] = matvec_h(h, vecs[f"va_{k}"], adjoint=True)
+    st = MatvecStats()
+    matvec_h(h, vecs["vf_0"], stats=st)
+    res["leaves_touched"] = np.int64(st.leaves_touched)
+    path = os.path.join(OUT, f"{name}.npz")
+    save_h(h, path, nvec=np.int64(len(seeds)), **vecs, **res)
+    print(f"{name}: H shape={h.shape} adm={len(h.admissible)} dense={len(h.dense)} "
+          f"size={os.path.getsize(path) / 1e6:.2f} MB")
+
+
 def two_cloud():
     """Rectangular two-tree operator (tests/test_uniform.py:45-60 geometry)."""
     rng = np.random.default_rng(0)
@@ -182,6 +199,8 @@ def main():
     helm = Instance(400, kernel="helmholtz", kappa=2.0)
     uh400 = direct_build_uh(helm.oracle, helm.bct, 1e-5)
     emit("helm400", uh400, complex_vec=True, seeds=(5,), exact=helm.dense)
+    h800 = assemble_h(inst.oracle, inst.bct, ToleranceSpec(1e-4 / 3), ToleranceSpec(1e-5), workers=2)
+    emit_h("h_h800_laplace", h800, complex_vec=False, seeds=(3,))
 
     # configs' construction at small scale: icosphere L=2 centroids, eta=2 weak, compress path
     pts, w = icosphere_centroids(2)
@@ -191,6 +210,7 @@ def main():
     oracle = EntryOracle(g, g, KernelSpec("helmholtz", 2.0), tree.permutation, tree.permutation)
     h = assemble_h(oracle, bct, ToleranceSpec(1e-6), ToleranceSpec(1e-7), workers=4)
     ico2 = compress_h_to_uh(h, 1e-6)
+    emit_h("h_ico2_helm", h, complex_vec=True)
     emit("ico2_helm_compress", ico2, complex_vec=True, seeds=(0,))
 
     emit("two_cloud", two_cloud(), complex_vec=True, seeds=(7,))

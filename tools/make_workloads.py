@@ -57,6 +57,14 @@ def main():
         kb = np.full(len(bct.nodes), -1, dtype=np.int64)
         for b, p in uh.coeffs.items():
             kb[b] = p.s_x.shape[1]
+        hp = os.path.join("data", f"ref_cfg{cfg}_h.pkl")
+        if os.path.exists(hp):  # ranks of the source H-matrix (for the H-format bench)
+            with open(hp, "rb") as fh:
+                hsrc = pickle.load(fh)
+            kh = np.full(len(bct.nodes), -1, dtype=np.int64)
+            for b, f in hsrc.admissible.items():
+                kh[b] = f.rank
+            extra["kb_h"] = kh
         rep = storage_report_uh(uh)
         extra["ref_bytes_estimate"] = np.int64(rep.bytes_estimate)
         rng = np.random.default_rng(0)
