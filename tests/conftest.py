@@ -17,7 +17,7 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
-GOLDEN_NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+GOLDEN_NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")) if not os.path.basename(p).startswith("h_"))
 
 _cache = {}
 
