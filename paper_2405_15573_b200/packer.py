@@ -73,6 +73,8 @@ ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op (= consumer row-groups: one r
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
+# work splitting of the farfield chain ops across CTAs (output entries per op)
+SPLIT_DEFAULTS = {"p1_out": 1 << 30, "u_cols": 1 << 30, "z_rows": 1 << 30}
 
 
 def _align(n: int) -> int:
@@ -322,7 +324,9 @@ def pack(
         part = dict(rank=rank, world=world, row_bounds=rb, col_bounds=cb)
     else:
         part = None
-    kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems)
+    split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in SPLIT_DEFAULTS.items()}
+    kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems,
+              split=split)
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
     adj, work_a, ex_a = _build_program(geo, adjoint=True, **kw)
     elems_alg = bytes_bases + bytes_coupling + bytes_dense
@@ -378,7 +382,10 @@ def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
     return (int(m_off), int(buf), int(rows), int(cols), int(ld), int(mode), int(in_off), int(out_off), int(x_off))
 
 
-def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS):
+def _build_program(
+    geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS, split=None
+):
+    split = dict(SPLIT_DEFAULTS, **(split or {}))
     bct = geo["bct"]
     offs = geo["offs"]
     fcols, ycols = geo["fcols"], geo["ycols"]
@@ -489,17 +496,28 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, 
     c_z = {s: ctr() for s in out_map}
     ops = {k: [] for k in range(7)}
 
-    # P1: partial_t = B_t[chunk rows]^H x[chunk]
+    # P1: partial_t = B_t[chunk rows]^H x[chunk]; the ancestors of a chunk are grouped into
+    # ops of <= split["p1_out"] outputs so the head of the dependency chain spreads over CTAs
     for idx, (p, a, b) in enumerate(p1_items):
-        segs, outs, sigs = [], [], []
-        oo = 0
+        groups, cur, tot = [], [], 0
         for t in in_anc[p]:
-            lt = in_rank[t]
-            segs.append(_seg(offs[(in_basis_key, t)] + (a - in_nodes[t].lo) * lt, BUF_ARENA, b - a, lt, lt, MODE_H, 0, oo, a))
-            outs.append((BUF_WORK, part_off[t] + chunks_of[t].index(idx) * lt, lt, oo, 0))
-            sigs.append(c_part[t])
-            oo += lt
-        ops[KIND_P1].append((KIND_P1, b - a, oo, [(BUF_X, a, b - a, 0, 0)], segs, outs, [], sigs, (b - a) * oo))
+            if cur and tot + in_rank[t] > split["p1_out"]:
+                groups.append(cur)
+                cur, tot = [], 0
+            cur.append(t)
+            tot += in_rank[t]
+        if cur:
+            groups.append(cur)
+        for grp in groups:
+            segs, outs, sigs = [], [], []
+            oo = 0
+            for t in grp:
+                lt = in_rank[t]
+                segs.append(_seg(offs[(in_basis_key, t)] + (a - in_nodes[t].lo) * lt, BUF_ARENA, b - a, lt, lt, MODE_H, 0, oo, a))
+                outs.append((BUF_WORK, part_off[t] + chunks_of[t].index(idx) * lt, lt, oo, 0))
+                sigs.append(c_part[t])
+                oo += lt
+            ops[KIND_P1].append((KIND_P1, b - a, oo, [(BUF_X, a, b - a, 0, 0)], segs, outs, [], sigs, (b - a) * oo))
     # RED: y_t = sum of chunk partials (skipped when the single partial is y_t itself)
     for t in in_map:
         lt, nchunk = in_rank[t], len(chunks_of[t])
@@ -527,11 +545,12 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, 
             continue
         u_wait[t] = [(c_u[t], 1)]
         base = offs[("Y", t)] if not adjoint else offs[("F", t)]
-        segs = [_seg(base, BUF_ARENA, lt, n, n, MODE_H, 0, 0)]
-        ops[KIND_U].append(
-            (KIND_U, lt, n, [(BUF_WORK, y_off[t], lt, 0, 0)], segs, [(BUF_WORK, u_off[t], n, 0, 0)],
-             list(y_wait[t]), [c_u[t]], lt * n)
-        )
+        for c0, c1 in _chunks(0, n, split["u_cols"]):  # column panels: one op each
+            segs = [_seg(base + c0, BUF_ARENA, lt, c1 - c0, n, MODE_H, 0, 0)]
+            ops[KIND_U].append(
+                (KIND_U, lt, c1 - c0, [(BUF_WORK, y_off[t], lt, 0, 0)], segs, [(BUF_WORK, u_off[t] + c0, c1 - c0, 0, 0)],
+                 list(y_wait[t]), [c_u[t]], lt * (c1 - c0))
+            )
     # Z: coupling, owned by the output cluster (row cluster forward, column cluster adjoint)
     for s in out_map:
         ls = out_rank[s]
@@ -578,9 +597,13 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, 
                 segs.append(_seg(offs[("S", bid)], BUF_ARENA, lr, ls, ls, MODE_H, n_in, 0))
                 n_in += lr
                 nbytes += lr * ls
-        ops[KIND_Z].append(
-            (KIND_Z, n_in, ls, in_runs, segs, [(BUF_WORK, z_off[s], ls, 0, 0)], sorted(set(waits)), [c_z[s]], nbytes)
-        )
+        for o0, o1 in _chunks(0, ls, split["z_rows"]):  # output-row parts: one op each
+            part = _restrict(segs, o0, o1)
+            nb = sum(q[2] * q[3] for q in part)
+            ops[KIND_Z].append(
+                (KIND_Z, n_in, o1 - o0, in_runs, part, [(BUF_WORK, z_off[s] + o0, o1 - o0, 0, 0)],
+                 sorted(set(waits)), [c_z[s]], nb)
+            )
 
     # NEAR + FAR per output-leaf chunk
     # The output w is zeroed by the launcher and every entry receives at most one NEAR and one
@@ -633,6 +656,16 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, 
                 (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], waits, [], rows * pos)
             )
 
+    # ---- a wait means "every op signalling this counter is done": count the producers ----
+    producers = {}
+    for k in ops:
+        for o in ops[k]:
+            for c in o[7]:
+                producers[c] = producers.get(c, 0) + 1
+    for k in ops:
+        ops[k] = [
+            o[:6] + ([(c, producers.get(c, 0)) for c, _n in o[6]],) + o[7:] for o in ops[k]
+        ]
     # ---- order: largest first inside each kind (reference uniform.py:505-506) ----
     for k in ops:
         ops[k].sort(key=lambda o: -o[-1])
@@ -665,6 +698,23 @@ def _build_program(geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, 
     prog_b.zero_output = False
     prog_a.part_b = prog_b
     return prog_a, work, ex
+
+
+def _restrict(segs, o0, o1):
+    """The part of an op's logical segments that produces output entries [o0, o1) (N: rows,
+    H/S: columns), re-based so the part's outputs start at 0."""
+    out = []
+    for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in segs:
+        span = rows if mode == MODE_N else cols
+        lo, hi = max(o0, out_off), min(o1, out_off + span)
+        if lo >= hi:
+            continue
+        d = lo - out_off
+        if mode == MODE_N:
+            out.append((m_off + d * ld, buf, hi - lo, cols, ld, mode, in_off, lo - o0, x_off))
+        else:
+            out.append((m_off + d, buf, rows, hi - lo, ld, mode, in_off, lo - o0, x_off))
+    return out
 
 
 def _panel_split(s):
