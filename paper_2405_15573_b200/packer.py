@@ -74,7 +74,7 @@ P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 # work splitting of the farfield chain ops across CTAs (output entries per op)
-SPLIT_DEFAULTS = {"p1_out": 1 << 30, "u_cols": 1 << 30, "z_rows": 1 << 30}
+SPLIT_DEFAULTS = {"p1_out": 1 << 30, "u_cols": 1 << 30, "z_rows": 1 << 30, "far_rows": ROWS_PER_CHUNK}
 
 
 def _align(n: int) -> int:
@@ -325,6 +325,9 @@ def pack(
     else:
         part = None
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in SPLIT_DEFAULTS.items()}
+    if os.environ.get("UHMV_NEAR_INTERLEAVE"):
+        near_interleave = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE"].split(","))
+    split["far_rows"] = int(os.environ.get("UHMV_FAR_ROWS", rows_per_chunk))
     kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems,
               split=split)
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
@@ -642,7 +645,7 @@ def _build_program(
         anc = out_anc[p]
         if not anc:
             continue
-        for a, b in _chunks(n.lo, n.hi, rows_per_chunk):
+        for a, b in _chunks(n.lo, n.hi, split["far_rows"]):
             rows = b - a
             in_runs, segs, waits = [], [], []
             pos = 0
