@@ -69,7 +69,8 @@ KIND_NAMES = ["P1", "NEAR", "RED", "U", "Z", "FAR", "ZERO"]
 
 ALIGN = 8  # complex128 elements per 128 B
 HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
-ROWS_PER_CHUNK = 16  # output rows per NEAR/FAR op (= consumer row-groups: one row each)
+ROWS_PER_CHUNK = 16  # output rows per NEAR op (= consumer row-groups: one row each)
+FAR_ROWS = 64  # output rows per FAR op (4 register slots of 16 row-groups)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
@@ -327,7 +328,7 @@ def pack(
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in SPLIT_DEFAULTS.items()}
     if os.environ.get("UHMV_NEAR_INTERLEAVE"):
         near_interleave = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE"].split(","))
-    split["far_rows"] = int(os.environ.get("UHMV_FAR_ROWS", rows_per_chunk))
+    split["far_rows"] = int(os.environ.get("UHMV_FAR_ROWS", FAR_ROWS))
     kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems,
               split=split)
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
