@@ -63,24 +63,31 @@ class DistributedOperator:
         return self.a.launch_info(adjoint, mode)
 
     def matvec(self, x, adjoint=False, out=None, mode=None, gather=False):
-        import torch
-        import torch.distributed as dist
-
         out = self.a.matvec(x, adjoint=adjoint, out=out, mode=mode)
         region, mine = exchange_views(self.a.work, self.packed_local, adjoint)
         if region.numel():
-            dist.all_gather_into_tensor(
-                torch.view_as_real(region), torch.view_as_real(mine), group=self.group
-            )
+            self._all_gather(region, mine)
         out = self.b.matvec(x, adjoint=adjoint, out=out, mode=mode)
         if gather:
             out = self.gather_output(out, adjoint)
         return out
 
+    def _all_gather(self, out, inp):
+        """all_gather_into_tensor over the group; NCCL works on the device buffers in place.
+        A gloo group (multi-process tests on one GPU) stages through host memory."""
+        import torch
+        import torch.distributed as dist
+
+        if out.is_cuda and dist.get_backend(self.group) == "gloo":
+            host = torch.empty(out.shape, dtype=out.dtype)
+            dist.all_gather_into_tensor(torch.view_as_real(host), torch.view_as_real(inp.cpu()), group=self.group)
+            out.copy_(host)
+            return
+        dist.all_gather_into_tensor(torch.view_as_real(out), torch.view_as_real(inp), group=self.group)
+
     def gather_output(self, w, adjoint=False):
         """All-gather the ranks' output slices into the full vector (padded blocks)."""
         import torch
-        import torch.distributed as dist
 
         bounds = self.packed_local.part["col_bounds" if adjoint else "row_bounds"]
         lens = np.diff(bounds)
@@ -89,7 +96,7 @@ class DistributedOperator:
         send = torch.zeros(blk, dtype=w.dtype, device=w.device)
         send[: hi - lo] = w[lo:hi]
         recv = torch.empty(blk * self.world, dtype=w.dtype, device=w.device)
-        dist.all_gather_into_tensor(torch.view_as_real(recv), torch.view_as_real(send), group=self.group)
+        self._all_gather(recv, send)
         full = torch.empty_like(w)
         for r in range(self.world):
             full[bounds[r] : bounds[r + 1]] = recv[r * blk : r * blk + lens[r]]
