@@ -344,6 +344,7 @@ __device__ void run_op(const ExecParams& p, int op, double2* xin, double2* outv,
 
 #include "uhmv_bulk.cuh"
 #include "uhmv_mrhs.cuh"
+#include "uhmv_mrtc.cuh"
 
 namespace {
 
@@ -433,6 +434,8 @@ struct uhmv_plan {
     unsigned long long* prof;  // diagnostics only (uhmv_plan_set_profile)
     int debug_flags;           // diagnostics only (UHMV_DEBUG_FLAGS): results are wrong
     int mrhs_grid;
+    int mrtc_grid;
+    int mrhs_engine;  // 0: staged tensor-core engine (mrtc), 1: register engine (UHMV_MRHS_ENGINE=simple)
 };
 
 extern "C" {
@@ -570,6 +573,18 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
             return cuda_fail(e, "occupancy(mrhs)");
         }
         p->mrhs_grid = (per_sm < 1 ? 1 : per_sm) * p->sm_count;
+        e = cudaFuncSetAttribute(mrtc::uhmv_mrtc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 mrtc::kSmemBytes);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrtc::uhmv_mrtc_kernel,
+                                                              mrtc::kThreads, mrtc::kSmemBytes);
+        if (e != cudaSuccess) {
+            delete p;
+            return cuda_fail(e, "occupancy(mrtc)");
+        }
+        p->mrtc_grid = (per_sm < 1 ? 1 : per_sm) * p->sm_count;
+        const char* ev = getenv("UHMV_MRHS_ENGINE");
+        p->mrhs_engine = (ev && strcmp(ev, "simple") == 0) ? 1 : 0;
     }
     if (const char* ev = getenv("UHMV_DEBUG_SKIP_WAITS")) p->debug_skip_waits = atoi(ev);
     if (const char* ev = getenv("UHMV_DEBUG_FLAGS")) p->debug_flags = atoi(ev);
@@ -724,10 +739,15 @@ int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, in
     mp.ticket = plan->d.ticket;
     mp.exit_count = plan->d.exit_count;
     mp.n_counters = pr.n_counters;
-    int grid = plan->mrhs_grid < pr.n_ops ? plan->mrhs_grid : pr.n_ops;
-    mrhs::uhmv_mrhs_kernel<<<grid, mrhs::kThreads, 0, st>>>(mp);
+    if (plan->mrhs_engine == 1) {
+        int grid = plan->mrhs_grid < pr.n_ops ? plan->mrhs_grid : pr.n_ops;
+        mrhs::uhmv_mrhs_kernel<<<grid, mrhs::kThreads, 0, st>>>(mp);
+    } else {
+        int grid = plan->mrtc_grid < pr.n_ops ? plan->mrtc_grid : pr.n_ops;
+        mrtc::uhmv_mrtc_kernel<<<grid, mrtc::kThreads, mrtc::kSmemBytes, st>>>(mp);
+    }
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "uhmv_mrhs_kernel launch");
+    if (e != cudaSuccess) return cuda_fail(e, "multi-RHS kernel launch");
     return UHMV_OK;
 }
 

@@ -1,0 +1,416 @@
+// uhmv_mrtc.cuh -- multi-RHS uniform-H product, shared-memory-staged FP64 tensor-core engine.
+//
+// Same op programs, fused ticket order and dependency counters as the single-RHS engines; every
+// segment group is a small complex GEMM  OUT (nout x R) += op(T) (nout x K) * IN (K x R)  on
+// DMMA (mma.sync.aligned.m16n8k16.row.col.f64) through the complex -> real embedding:
+//
+//   D (2R' x n) += A' (2R' x 2K) * B' (2K x n),  A' = embedded IN^T,  B' = T read as reals.
+//
+// Warp specialisation (one CTA of 8 consumer warps + 1 producer warp per SM):
+//   * the producer warp claims ops, polls their dependency counters (ld.acquire.gpu), then
+//     streams every K-chunk of every segment -- KC = 16 complex inputs: the matching T slab
+//     (N: nout rows x KC, H: KC rows x nout) and the IN block (KC rows x 64 RHS) -- into a
+//     5-deep shared-memory ring with cp.async.bulk (TMA engine) completing on mbarriers;
+//   * the consumer warps own a fixed (16-RHS, n-tile) share of the output block, accumulate
+//     the whole segment group in registers (up to 2 x 5 DMMA tiles per warp) and flush it once
+//     (fp64 atomics into w -- at most two addends per entry, so order-independent -- or
+//     read-add-write into work outputs zeroed at op start).
+//
+// Fragment mapping.  The mma k index (16 reals = 8 complex) and the RHS rows are permuted so
+// that every lane reads whole complex numbers with 16-B shared loads and no selects:
+//   lane (g = lane>>2, t = lane&3); logical mma k = t + 4j  <->  physical real k = 4t + j,
+//   i.e. complex inputs 2t and 2t+1 of the k-step; A rows m = g + 8d hold RHS g, part d.
+//   A (N: {re,-im; im,re}, H: {re,im; im,-re}) from z0 = IN[2t][g], z1 = IN[2t+1][g];
+//   B = T[n][2t], T[n][2t+1] (N) or T[2t][n], T[2t+1][n] (H) with n = g;
+//   D: v = e + 2d -> out[2t+e][g], part d: every lane flushes whole complex outputs.
+// Shared-memory row pitches (in complex): IN 65, T_N 17, T_H 81 -- each quarter-warp's 8
+// 16-B accesses hit 8 distinct bank groups (conflict-free).
+
+#pragma once
+
+namespace mrtc {
+
+constexpr int kCW = 8;                  // consumer warps
+constexpr int kCT = kCW * 32;           // consumer threads
+constexpr int kThreads = kCT + 32;      // + producer warp
+constexpr int kRP = 64;                 // complex RHS per pass
+constexpr int kNP = 80;                 // outputs per pass
+constexpr int kKC = 16;                 // complex inputs per stage
+constexpr int kNST = 5;                 // ring depth
+constexpr int kMaxNT = 5;               // n-tiles per warp
+constexpr int kLdTN = kKC + 1;          // 17
+constexpr int kLdTH = kNP + 1;          // 81
+constexpr int kLdI = kRP + 1;           // 65
+constexpr int kTElems = (kNP * kLdTN > kKC * kLdTH) ? kNP * kLdTN : kKC * kLdTH;
+constexpr int kIElems = kKC * kLdI;
+constexpr int kStageElems = kTElems + kIElems;  // complex
+constexpr int kOpSlots = 2;
+constexpr int kSmemStages = kNST * kStageElems * 16;
+constexpr int kSmemBytes = kSmemStages + kNP * 8 + kNP * 4 + (2 * kNST + 2 * kOpSlots) * 8 + 64;
+
+using mrhs::Params;
+using bulk::mbar_arrive;
+using bulk::mbar_arrive_expect_tx;
+using bulk::mbar_init;
+using bulk::mbar_wait;
+using bulk::su32;
+
+__device__ __forceinline__ void cons_sync() {
+    asm volatile("bar.sync 2, %0;" ::"n"(kCT) : "memory");
+}
+
+__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar))
+        : "memory");
+}
+
+struct SegD {
+    int64_t m_off, ld, in_abs;
+    int rows, cols, mode, in_buf, out_off;
+};
+
+__device__ __forceinline__ SegD seg_at(const Params& p, int i) {
+    const int64_t* d = p.mr_segs + (int64_t)i * 8;
+    SegD s;
+    s.m_off = __ldg(d + 0);
+    s.ld = __ldg(d + 1);
+    s.rows = (int)__ldg(d + 2);
+    s.cols = (int)__ldg(d + 3);
+    s.mode = (int)__ldg(d + 4);
+    s.in_buf = (int)__ldg(d + 5);
+    s.in_abs = __ldg(d + 6);
+    s.out_off = (int)__ldg(d + 7);
+    return s;
+}
+__device__ __forceinline__ int seg_nout(const SegD& s) { return s.mode == kModeN ? s.rows : s.cols; }
+__device__ __forceinline__ int seg_k(const SegD& s) { return s.mode == kModeN ? s.cols : s.rows; }
+
+// end of the segment group starting at s (same mode and outputs)
+__device__ __forceinline__ int group_end(const Params& p, int s, int se, const SegD& s0) {
+    const int nout = seg_nout(s0);
+    int e = s + 1;
+    while (e < se) {
+        const SegD sn = seg_at(p, e);
+        if (sn.mode != s0.mode || sn.out_off != s0.out_off || seg_nout(sn) != nout) break;
+        ++e;
+    }
+    return e;
+}
+
+__device__ void producer(const Params& p, double2* stages, uint64_t* full, uint64_t* empty,
+                         uint64_t* opfull, uint64_t* opempty, int* s_opq) {
+    const int lane = threadIdx.x & 31;
+    const int R = p.nrhs;
+    uint32_t stage = 0, sphase = 0, qphase = 0;
+    int q = 0;
+    for (;;) {
+        int op = -1;
+        if (lane == 0) {
+            const unsigned long long tk = atomicAdd(p.ticket, 1ull);
+            op = (tk < (unsigned long long)p.op_count) ? __ldg(p.fused_order + tk) : -1;
+        }
+        op = __shfl_sync(0xffffffffu, op, 0);
+        mbar_wait(&opempty[q], qphase ^ 1u);
+        if (op >= 0) {
+            const int32_t* hp = p.ops + (int64_t)op * kOpFields;
+            const int wb = __ldg(hp + 8), we = __ldg(hp + 9);
+            for (int i = wb + lane; i < we; i += 32) {
+                const int c = __ldg(p.waits + 2 * i);
+                const uint32_t need = (uint32_t)__ldg(p.waits + 2 * i + 1);
+                while (ld_acquire(p.counters + c) < need) __nanosleep(32);
+            }
+            __syncwarp();
+            // work inputs written by other CTAs (generic proxy) are read below by the TMA engine
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        if (lane == 0) {
+            s_opq[q] = op;
+            mbar_arrive(&opfull[q]);
+        }
+        if (op < 0) break;
+        const int sb = __ldg(p.mr_ranges + 2 * op), se = __ldg(p.mr_ranges + 2 * op + 1);
+        int s = sb;
+        while (s < se) {
+            const SegD s0 = seg_at(p, s);
+            const int e = group_end(p, s, se, s0);
+            if (s0.mode == kModeS) {
+                s = e;
+                continue;
+            }
+            const bool hm = s0.mode == kModeH;
+            const int nout = seg_nout(s0);
+            for (int rp = 0; rp < R; rp += kRP) {
+                const int rpn = min(kRP, R - rp);
+                for (int n0 = 0; n0 < nout; n0 += kNP) {
+                    const int np = min(kNP, nout - n0);
+                    for (int si = s; si < e; ++si) {
+                        const SegD sg = seg_at(p, si);
+                        const int K = seg_k(sg);
+                        const double2* T = p.arena + sg.m_off;
+                        const double2* IN = (sg.in_buf == kBufX ? p.x : p.work) + sg.in_abs * (int64_t)R + rp;
+                        for (int k0 = 0; k0 < K; k0 += kKC) {
+                            const int kv = min(kKC, K - k0);
+                            mbar_wait(&empty[stage], sphase ^ 1u);
+                            double2* st = stages + (int64_t)stage * kStageElems;
+                            double2* ti = st + kTElems;
+                            const uint32_t bytes = (uint32_t)(np * kv + kv * rpn) * 16u;
+                            if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+                            __syncwarp();
+                            if (!hm) {  // T rows n0.., columns k0..k0+kv
+                                for (int n = lane; n < np; n += 32)
+                                    g2s(st + n * kLdTN, T + (int64_t)(n0 + n) * sg.ld + k0, kv * 16u, &full[stage]);
+                            } else {  // T rows k0..k0+kv, columns n0..
+                                for (int k = lane; k < kv; k += 32)
+                                    g2s(st + k * kLdTH, T + (int64_t)(k0 + k) * sg.ld + n0, np * 16u, &full[stage]);
+                            }
+                            for (int k = lane; k < kv; k += 32)
+                                g2s(ti + k * kLdI, IN + (int64_t)(k0 + k) * R, rpn * 16u, &full[stage]);
+                            if (++stage == kNST) {
+                                stage = 0;
+                                sphase ^= 1u;
+                            }
+                        }
+                    }
+                }
+            }
+            s = e;
+        }
+        if (++q == kOpSlots) {
+            q = 0;
+            qphase ^= 1u;
+        }
+    }
+}
+
+__device__ void consumer(const Params& p, double2* stages, double2** s_out, uint32_t* s_at,
+                         uint64_t* full, uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
+                         const int* s_opq) {
+    const int ctid = threadIdx.x;  // 0 .. kCT-1
+    const int lane = ctid & 31, cw = ctid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int R = p.nrhs;
+    uint32_t stage = 0, sphase = 0, qphase = 0;
+    int q = 0;
+    for (;;) {
+        mbar_wait(&opfull[q], qphase);
+        const int op = s_opq[q];
+        if (op < 0) break;
+        const int32_t* hp = p.ops + (int64_t)op * kOpFields;
+        const int out_b = __ldg(hp + 6), out_e = __ldg(hp + 7);
+        // zero the op's work outputs (groups add into them); w is zeroed by the launcher
+        for (int r = out_b; r < out_e; ++r) {
+            const int64_t* rd = p.runs + (int64_t)r * kRunFields;
+            if (__ldg(rd + 4) & 2) continue;
+            double2* dp = p.work + __ldg(rd + 1) * (int64_t)R;
+            const int64_t n = (int64_t)__ldg(rd + 2) * R;
+            for (int64_t i = ctid; i < n; i += kCT) __stcg(dp + i, make_double2(0.0, 0.0));
+        }
+        const int sb = __ldg(p.mr_ranges + 2 * op), se = __ldg(p.mr_ranges + 2 * op + 1);
+        int s = sb;
+        while (s < se) {
+            const SegD s0 = seg_at(p, s);
+            const int e = group_end(p, s, se, s0);
+            const int nout = seg_nout(s0);
+            if (s0.mode == kModeS) {
+                // partial-vector reduction: out[j][r] = sum_k W[k][j][r] (work, L2 reads)
+                cons_sync();
+                const int64_t tot = (int64_t)nout * R;
+                for (int64_t qq = ctid; qq < tot; qq += kCT) {
+                    const int j = (int)(qq / R), r = (int)(qq % R);
+                    double2 acc = make_double2(0.0, 0.0);
+                    for (int si = s; si < e; ++si) {
+                        const SegD sg = seg_at(p, si);
+                        for (int k = 0; k < sg.rows; ++k) {
+                            const double2 v = __ldcg(p.work + (sg.m_off + k * sg.ld + j) * (int64_t)R + r);
+                            acc.x += v.x;
+                            acc.y += v.y;
+                        }
+                    }
+                    bool at;
+                    double2* dp = mrhs::out_ptr(p, out_b, out_e, s0.out_off + j, &at) + r;
+                    const double2 o = __ldcg(dp);
+                    __stcg(dp, make_double2(o.x + acc.x, o.y + acc.y));
+                }
+                s = e;
+                continue;
+            }
+            const bool hm = s0.mode == kModeH;
+            for (int rp = 0; rp < R; rp += kRP) {
+                const int n_mg = min(kRP, R - rp) / 16;
+                const int nsplit = kCW / n_mg;
+                const bool active = cw < n_mg * nsplit;
+                const int mg = cw % n_mg, ns = cw / n_mg;
+                for (int n0 = 0; n0 < nout; n0 += kNP) {
+                    const int np = min(kNP, nout - n0);
+                    const int ntiles = (np + 7) >> 3;
+                    cons_sync();  // previous flush done with the table; work outputs zeroed
+                    for (int i = ctid; i < np; i += kCT) {
+                        bool at;
+                        s_out[i] = mrhs::out_ptr(p, out_b, out_e, s0.out_off + n0 + i, &at);
+                        s_at[i] = at ? 1u : 0u;
+                    }
+                    cons_sync();
+                    double acc[2][kMaxNT][4];
+#pragma unroll
+                    for (int a = 0; a < 2; ++a)
+#pragma unroll
+                        for (int b = 0; b < kMaxNT; ++b)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
+                    for (int si = s; si < e; ++si) {
+                        const int K = seg_k(seg_at(p, si));
+                        for (int k0 = 0; k0 < K; k0 += kKC) {
+                            const int kv = min(kKC, K - k0);
+                            mbar_wait(&full[stage], sphase);
+                            if (active) {
+                                const double2* st = stages + (int64_t)stage * kStageElems;
+                                const double2* ti = st + kTElems + mg * 16 + g;
+#pragma unroll
+                                for (int ks = 0; ks < 2; ++ks) {
+                                    const int kc = ks * 8 + 2 * t;  // this lane's complex inputs kc, kc+1
+                                    if (ks * 8 >= kv) break;
+                                    const bool v0 = kc < kv, v1 = kc + 1 < kv;
+                                    double afr[2][8];
+#pragma unroll
+                                    for (int mt = 0; mt < 2; ++mt) {
+                                        const double2 zero = make_double2(0.0, 0.0);
+                                        const double2 z0 = v0 ? ti[kc * kLdI + mt * 8] : zero;
+                                        const double2 z1 = v1 ? ti[(kc + 1) * kLdI + mt * 8] : zero;
+                                        if (!hm) {  // {re,-im; im,re}
+                                            afr[mt][0] = z0.x; afr[mt][1] = z0.y;
+                                            afr[mt][2] = -z0.y; afr[mt][3] = z0.x;
+                                            afr[mt][4] = z1.x; afr[mt][5] = z1.y;
+                                            afr[mt][6] = -z1.y; afr[mt][7] = z1.x;
+                                        } else {  // {re,im; im,-re}
+                                            afr[mt][0] = z0.x; afr[mt][1] = z0.y;
+                                            afr[mt][2] = z0.y; afr[mt][3] = -z0.x;
+                                            afr[mt][4] = z1.x; afr[mt][5] = z1.y;
+                                            afr[mt][6] = z1.y; afr[mt][7] = -z1.x;
+                                        }
+                                    }
+#pragma unroll
+                                    for (int j = 0; j < kMaxNT; ++j) {
+                                        const int nt = ns + j * nsplit;
+                                        if (nt >= ntiles) break;
+                                        const int n = nt * 8 + g;
+                                        double2 b0, b1;
+                                        if (!hm) {
+                                            b0 = st[n * kLdTN + kc];
+                                            b1 = st[n * kLdTN + kc + 1];
+                                        } else {
+                                            b0 = st[kc * kLdTH + n];
+                                            b1 = st[(kc + 1) * kLdTH + n];
+                                        }
+                                        if (!v0) b0 = make_double2(0.0, 0.0);
+                                        if (!v1) b1 = make_double2(0.0, 0.0);
+                                        const double bfr[4] = {b0.x, b0.y, b1.x, b1.y};
+                                        mrhs::dmma(acc[0][j], afr[0], bfr);
+                                        mrhs::dmma(acc[1][j], afr[1], bfr);
+                                    }
+                                }
+                            }
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive(&empty[stage]);
+                            if (++stage == kNST) {
+                                stage = 0;
+                                sphase ^= 1u;
+                            }
+                        }
+                    }
+                    if (active) {  // flush: lane holds out[2t+e][g] for its tiles (re d=0, im d=1)
+#pragma unroll
+                        for (int j = 0; j < kMaxNT; ++j) {
+                            const int nt = ns + j * nsplit;
+                            if (nt >= ntiles) break;
+#pragma unroll
+                            for (int ee = 0; ee < 2; ++ee) {
+                                const int n = nt * 8 + 2 * t + ee;
+                                if (n >= np) continue;
+                                double2* base = s_out[n] + rp + mg * 16 + g;
+                                const bool at = s_at[n] != 0u;
+#pragma unroll
+                                for (int mt = 0; mt < 2; ++mt) {
+                                    double2* dp = base + mt * 8;
+                                    const double re = acc[mt][j][ee], im = acc[mt][j][2 + ee];
+                                    if (at) {
+                                        atomicAdd(&dp->x, re);
+                                        atomicAdd(&dp->y, im);
+                                    } else {
+                                        const double2 o = __ldcg(dp);
+                                        __stcg(dp, make_double2(o.x + re, o.y + im));
+                                    }
+                                }
+                            }
+                        }
+                    }
+                }
+            }
+            s = e;
+        }
+        cons_sync();  // every flush of the op issued
+        if (ctid == 0) {
+            const int gb = __ldg(hp + 10), ge = __ldg(hp + 11);
+            if (ge > gb) {
+                __threadfence();
+                for (int i = gb; i < ge; ++i) bulk::red_release_add(p.counters + __ldg(p.sigs + i), 1u);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&opempty[q]);
+        if (++q == kOpSlots) {
+            q = 0;
+            qphase ^= 1u;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) uhmv_mrtc_kernel(const Params p) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    double2* stages = reinterpret_cast<double2*>(smem);
+    double2** s_out = reinterpret_cast<double2**>(smem + kSmemStages);
+    uint32_t* s_at = reinterpret_cast<uint32_t*>(s_out + kNP);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemStages + kNP * 8 + kNP * 4);
+    uint64_t* empty = full + kNST;
+    uint64_t* opfull = empty + kNST;
+    uint64_t* opempty = opfull + kOpSlots;
+    int* s_opq = reinterpret_cast<int*>(opempty + kOpSlots);
+    int* flag = s_opq + kOpSlots;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kNST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kCW);
+        }
+        for (int s = 0; s < kOpSlots; ++s) {
+            mbar_init(&opfull[s], 1);
+            mbar_init(&opempty[s], kCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if ((threadIdx.x >> 5) == kCW) {
+        producer(p, stages, full, empty, opfull, opempty, s_opq);
+    } else {
+        consumer(p, stages, s_out, s_at, full, empty, opfull, opempty, s_opq);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(p.exit_count, 1u);
+        flag[0] = (prev == gridDim.x - 1) ? 1 : 0;
+    }
+    __syncthreads();
+    if (flag[0]) {
+        __threadfence();
+        for (int i = threadIdx.x; i < p.n_counters; i += kThreads) p.counters[i] = 0u;
+        if (threadIdx.x == 0) {
+            *p.ticket = 0ull;
+            *p.exit_count = 0u;
+        }
+        __threadfence();
+    }
+}
+
+}  // namespace mrtc

@@ -100,6 +100,9 @@ class DeviceOperator:
         if share_with is not None:
             for name in ("arena", "work", "counters", "ticket", "exit_count", "x_scratch", "w_scratch"):
                 setattr(self, name, getattr(share_with, name))
+            need = max(fwd_p.n_counters, adj_p.n_counters, 1)
+            if self.counters.numel() < need:
+                self.counters = torch.zeros(need, dtype=torch.int32, device=dev)
         else:
             self.arena = torch.from_numpy(packed.arena).to(dev)
             self.work = torch.zeros(packed.work_len, dtype=torch.complex128, device=dev)
@@ -218,11 +221,12 @@ class DeviceOperator:
         else:
             Xp = X.contiguous()
         W = torch.empty((n_out, Rp), dtype=torch.complex128, device=self.device)
-        need = p.work_len * Rp
+        mr, work_len = self._mr_plan()
+        need = work_len * Rp
         if getattr(self, "_work_mr", None) is None or self._work_mr.numel() < need:
             self._work_mr = torch.zeros(need, dtype=torch.complex128, device=self.device)
         rc = _lib.lib().uhmv_execute_mrhs(
-            self._plan, ctypes.c_void_p(Xp.data_ptr()), ctypes.c_void_p(W.data_ptr()),
+            mr._plan, ctypes.c_void_p(Xp.data_ptr()), ctypes.c_void_p(W.data_ptr()),
             ctypes.c_void_p(self._work_mr.data_ptr()), int(Rp), int(adjoint), self._stream(stream),
         )
         _lib.check(rc, "uhmv_execute_mrhs")
@@ -231,6 +235,21 @@ class DeviceOperator:
             out.copy_(res)
             return out
         return res
+
+    def _mr_plan(self):
+        """The multi-RHS plan: the same arena with whole-leaf NEAR / FAR ops
+        (packer.MR_ROWS; ``UHMV_MR_ROWS=0`` keeps the single-RHS programs)."""
+        if getattr(self, "_mr", None) is None:
+            from .packer import MR_ROWS
+
+            p = self.packed
+            rows = int(os.environ.get("UHMV_MR_ROWS", MR_ROWS))
+            if rows > 0 and p.geo is not None and p.world == 1 and self.progs == (p.fwd, p.adj):
+                fwd, adj, work_len = p.programs(rows_per_chunk=rows, far_rows=rows)
+                self._mr = (DeviceOperator(p, device=self.device, programs=(fwd, adj), share_with=self), work_len)
+            else:
+                self._mr = (self, p.work_len)
+        return self._mr
 
     def execute_phases(self, x, out, adjoint, lo, hi, stream=None):
         rc = _lib.lib().uhmv_execute_phases(
@@ -258,6 +277,10 @@ class DeviceOperator:
         return out
 
     def close(self):
+        mr = getattr(self, "_mr", None)
+        if mr is not None and mr[0] is not self:
+            mr[0].close()
+        self._mr = None
         if getattr(self, "_plan", None):
             _lib.lib().uhmv_plan_destroy(self._plan)
             self._plan = None

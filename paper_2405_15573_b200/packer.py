@@ -70,6 +70,7 @@ KIND_NAMES = ["P1", "NEAR", "RED", "U", "Z", "FAR", "ZERO"]
 ALIGN = 8  # complex128 elements per 128 B
 HCOLS_MAX = 32  # widest H/S segment of the register kernel (= csrc kHColsMax)
 ROWS_PER_CHUNK = 16  # output rows per NEAR op (= consumer row-groups: one row each)
+MR_ROWS = 80  # multi-RHS programs: NEAR / FAR output rows per op (= mrtc kNP, one pass)
 FAR_ROWS = 64  # output rows per FAR op (4 register slots of 16 row-groups)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
@@ -129,6 +130,20 @@ class PackedOperator:
     world: int = 1
     part: dict | None = None
     exchange: dict = field(default_factory=dict)  # per direction: (ex_off, ex_len) block layout
+    geo: dict | None = field(default=None, repr=False)  # index structure, for re-chunked programs
+    build_kw: dict | None = field(default=None, repr=False)
+
+    def programs(self, *, rows_per_chunk: int, far_rows: int):
+        """(fwd, adj, work_len): the same operator and arena with NEAR / FAR ops re-chunked
+        (the multi-RHS engine wants whole-leaf output blocks).  Single-GPU only."""
+        if self.geo is None or self.world != 1:
+            raise ValueError("re-chunking needs a single-GPU pack")
+        kw = dict(self.build_kw)
+        kw["rows_per_chunk"] = rows_per_chunk
+        kw["split"] = dict(kw["split"], far_rows=far_rows)
+        fwd, work_f, _ = _build_program(self.geo, adjoint=False, **kw)
+        adj, work_a, _ = _build_program(self.geo, adjoint=True, **kw)
+        return fwd, adj, max(work_f, work_a, 1)
 
 
 def _leaves_under(tree):
@@ -350,6 +365,8 @@ def pack(
         world=world,
         part=part,
         exchange={"fwd": ex_f, "adj": ex_a},
+        geo=geo,
+        build_kw=kw,
         storage=dict(
             bases=16 * bytes_bases,
             coupling=16 * bytes_coupling,

@@ -140,9 +140,17 @@ def test_repeated_fused_launches_self_reset(mode):
     assert int(dop.counters.abs().sum()) == 0 and int(dop.ticket.item()) == 0
 
 
-@pytest.mark.parametrize("R", [16, 5])
-def test_multi_rhs_dmma(golden, R):
-    """Multi-RHS (config 5 path) on FP64 tensor cores vs the reference column loop."""
+@pytest.mark.parametrize("engine", ["tc", "simple"])
+@pytest.mark.parametrize("R", [16, 5, 64, 80])
+def test_multi_rhs_dmma(golden, R, engine, monkeypatch):
+    """Multi-RHS (config 5 path) on FP64 tensor cores vs the reference column loop.  ``tc``:
+    the staged engine on whole-leaf programs (R = 80: two RHS passes, 64 + 16); ``simple``:
+    the register engine on the single-RHS programs."""
+    if engine == "simple":
+        if R > 16:
+            pytest.skip("register engine: cross-check at small R only")
+        monkeypatch.setenv("UHMV_MRHS_ENGINE", "simple")
+        monkeypatch.setenv("UHMV_MR_ROWS", "0")
     name, u, ex = golden
     dop = _dev(u)
     rng = np.random.default_rng(3)
