@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 5
+#define UHMV_ABI_VERSION 6
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -60,8 +60,10 @@ typedef struct uhmv_program {
     int32_t zero_output; /* zero w before the launch (0 for the post-exchange program of a
                             multi-GPU rank, which adds into w)                          */
     int32_t stage_elems; /* complex128 elements per shared-memory stage (bulk engine)  */
-    const int64_t* mr_segs;   /* multi-RHS segments, n x 8 int64 (one input source each)   */
-    const int32_t* mr_ranges; /* n_ops x 2 int32: mr_segs range of every op                 */
+    const int64_t* mr_segs;   /* multi-RHS segments, n x 8 int64 (one input source each);
+                                 mode field: low byte mode, bit 8 first writer of its outputs */
+    const int32_t* mr_ranges; /* n_ops x 3 int32: mr_segs range of every op + flags
+                                 (bit 0: zero the op's work outputs first)                   */
 } uhmv_program;
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */

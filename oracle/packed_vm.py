@@ -18,6 +18,8 @@ from paper_2405_15573_b200.packer import (
     MODE_H,
     MODE_N,
     MODE_S,
+    MR_FIRST,
+    MR_ZERO,
     PI_DIRECT,
     PI_XGLOBAL,
     PI_XSTAGE,
@@ -97,29 +99,52 @@ def vm_matvec(packed, v, adjoint=False, order="phased", engine="segs"):
 
 
 def run_op_mr(prog, i, bufs, R):
-    """Multi-RHS op: vectors are (len, R) blocks; uses the resolved ``mr_segs``."""
-    n_out = int(prog.ops[i, 1])
+    """Multi-RHS op exactly as the device engines flush it: vectors are (len, R) blocks; the
+    resolved ``mr_segs`` form groups (same mode and outputs) that are summed and flushed once
+    -- fp64 add for atomic (w) runs, store for a group flagged MR_FIRST, add otherwise; the
+    op's work outputs are zeroed first only when it carries MR_ZERO."""
     out_b, out_e = (int(v) for v in prog.ops[i, 6:8])
-    a, b = (int(v) for v in prog.mr_ranges[i])
-    out = np.zeros((n_out, R), dtype=np.complex128)
-    for m_off, ld, rows, cols, mode, in_buf, in_abs, out_off in prog.mr_segs[a:b]:
-        if mode == MODE_S:
-            src = bufs[BUF_WORK]
-            for k in range(rows):
-                out[out_off : out_off + cols] += src[m_off + k * ld : m_off + k * ld + cols]
-            continue
-        idx = m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]
-        m = bufs[BUF_ARENA][idx]
-        vin = bufs[int(in_buf)]
-        if mode == MODE_N:
-            out[out_off : out_off + rows] += m @ vin[in_abs : in_abs + cols]
-        else:
-            out[out_off : out_off + cols] += np.conj(m).T @ vin[in_abs : in_abs + rows]
-    for buf, off, ln, dst, flags in prog.runs[out_b:out_e]:
-        if flags & (RUN_ADD | RUN_ATOMIC):
-            bufs[buf][off : off + ln] += out[dst : dst + ln]
-        else:
-            bufs[buf][off : off + ln] = out[dst : dst + ln]
+    a, b, flags = (int(v) for v in prog.mr_ranges[i])
+    out_runs = prog.runs[out_b:out_e]
+    if flags & MR_ZERO:
+        for buf, off, ln, dst, fl in out_runs:
+            if not fl & RUN_ATOMIC:
+                bufs[int(buf)][off : off + ln] = 0
+
+    def flush(o0, blk, first):
+        for j in range(blk.shape[0]):
+            o = o0 + j
+            buf, off, ln, dst, fl = next(r for r in out_runs if r[3] <= o < r[3] + r[2])
+            tgt = bufs[int(buf)]
+            if (fl & RUN_ATOMIC) or not first:
+                tgt[off + o - dst] += blk[j]
+            else:
+                tgt[off + o - dst] = blk[j]
+
+    segs = [tuple(int(v) for v in q) for q in prog.mr_segs[a:b]]
+    g = 0
+    while g < len(segs):
+        mode, o0 = segs[g][4] & 0xFF, segs[g][7]
+        nout = segs[g][2] if mode == MODE_N else segs[g][3]
+        e = g + 1
+        while e < len(segs) and segs[e][4] == segs[g][4] and segs[e][7] == o0 and (segs[e][2] if mode == MODE_N else segs[e][3]) == nout:
+            e += 1
+        blk = np.zeros((nout, R), dtype=np.complex128)
+        for m_off, ld, rows, cols, _mode, in_buf, in_abs, _o in segs[g:e]:
+            if mode == MODE_S:
+                src = bufs[BUF_WORK]
+                for k in range(rows):
+                    blk += src[m_off + k * ld : m_off + k * ld + cols]
+                continue
+            idx = m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]
+            m = bufs[BUF_ARENA][idx]
+            vin = bufs[in_buf]
+            if mode == MODE_N:
+                blk += m @ vin[in_abs : in_abs + cols]
+            else:
+                blk += np.conj(m).T @ vin[in_abs : in_abs + rows]
+        flush(o0, blk, bool(segs[g][4] & MR_FIRST))
+        g = e
 
 
 def vm_matmat(packed, V, adjoint=False):

@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "check", "LIB_PATH", "MAX_PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 5
+ABI_VERSION = 6
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 

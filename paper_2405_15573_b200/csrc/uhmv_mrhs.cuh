@@ -69,7 +69,7 @@ __device__ __forceinline__ Seg load_seg(const Params& p, int i) {
     s.ld = __ldg(d + 1);
     s.rows = (int)__ldg(d + 2);
     s.cols = (int)__ldg(d + 3);
-    s.mode = (int)__ldg(d + 4);
+    s.mode = (int)__ldg(d + 4) & 0xFF;  // low byte: mode (bit 8: first-writer flag)
     s.in_buf = (int)__ldg(d + 5);
     s.in_abs = __ldg(d + 6);
     s.out_off = (int)__ldg(d + 7);
@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads) uhmv_mrhs_kernel(const Params p) {
             for (int64_t i = tid; i < n; i += kThreads) __stcg(dp + i, make_double2(0.0, 0.0));
         }
         __syncthreads();
-        const int sb = __ldg(p.mr_ranges + 2 * op), se = __ldg(p.mr_ranges + 2 * op + 1);
+        const int sb = __ldg(p.mr_ranges + 3 * op), se = __ldg(p.mr_ranges + 3 * op + 1);
         int s = sb;
         while (s < se) {
             const Seg s0 = load_seg(p, s);

@@ -13,8 +13,8 @@
 //     5-deep shared-memory ring with cp.async.bulk (TMA engine) completing on mbarriers;
 //   * the consumer warps own a fixed (16-RHS, n-tile) share of the output block, accumulate
 //     the whole segment group in registers (up to 2 x 5 DMMA tiles per warp) and flush it once
-//     (fp64 atomics into w -- at most two addends per entry, so order-independent -- or
-//     read-add-write into work outputs zeroed at op start).
+//     (fp64 atomics into w -- at most two addends per entry, so order-independent -- a store
+//     for the first group on a work output range, read-add-write for a later one).
 //
 // Fragment mapping.  The mma k index (16 reals = 8 complex) and the RHS rows are permuted so
 // that every lane reads whole complex numbers with 16-B shared loads and no selects:
@@ -70,6 +70,7 @@ __device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, 
 struct SegD {
     int64_t m_off, ld, in_abs;
     int rows, cols, mode, in_buf, out_off;
+    int first;  // first group writing these outputs: the flush stores (packer.MR_FIRST)
 };
 
 __device__ __forceinline__ SegD seg_at(const Params& p, int i) {
@@ -79,7 +80,9 @@ __device__ __forceinline__ SegD seg_at(const Params& p, int i) {
     s.ld = __ldg(d + 1);
     s.rows = (int)__ldg(d + 2);
     s.cols = (int)__ldg(d + 3);
-    s.mode = (int)__ldg(d + 4);
+    const int mf = (int)__ldg(d + 4);
+    s.mode = mf & 0xFF;
+    s.first = (mf >> 8) & 1;
     s.in_buf = (int)__ldg(d + 5);
     s.in_abs = __ldg(d + 6);
     s.out_off = (int)__ldg(d + 7);
@@ -94,7 +97,8 @@ __device__ __forceinline__ int group_end(const Params& p, int s, int se, const S
     int e = s + 1;
     while (e < se) {
         const SegD sn = seg_at(p, e);
-        if (sn.mode != s0.mode || sn.out_off != s0.out_off || seg_nout(sn) != nout) break;
+        if (sn.mode != s0.mode || sn.first != s0.first || sn.out_off != s0.out_off || seg_nout(sn) != nout)
+            break;
         ++e;
     }
     return e;
@@ -131,7 +135,7 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
             mbar_arrive(&opfull[q]);
         }
         if (op < 0) break;
-        const int sb = __ldg(p.mr_ranges + 2 * op), se = __ldg(p.mr_ranges + 2 * op + 1);
+        const int sb = __ldg(p.mr_ranges + 3 * op), se = __ldg(p.mr_ranges + 3 * op + 1);
         int s = sb;
         while (s < se) {
             const SegD s0 = seg_at(p, s);
@@ -185,6 +189,61 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
     }
 }
 
+// One ring stage (KC = 16 complex inputs = two mma k-steps) of a warp's tiles.  Both k-steps'
+// A fragments are loaded up front; FULL: every input of the stage is valid (no masking).
+template <bool HM, bool FULL>
+__device__ __forceinline__ void stage_mma(double (&acc)[2][kMaxNT][4], const double2* st,
+                                          const double2* ti, int kv, int ns, int nsplit, int ntiles,
+                                          int g, int t) {
+    const double2 zero = make_double2(0.0, 0.0);
+    double afr[2][2][8];
+    bool val[2][2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+        const int kc = ks * 8 + 2 * t;  // this lane's complex inputs kc, kc+1
+        val[ks][0] = FULL || kc < kv;
+        val[ks][1] = FULL || kc + 1 < kv;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+            const double2 z0 = val[ks][0] ? ti[kc * kLdI + mt * 8] : zero;
+            const double2 z1 = val[ks][1] ? ti[(kc + 1) * kLdI + mt * 8] : zero;
+            double* a = afr[ks][mt];
+            if (!HM) {  // {re,-im; im,re}
+                a[0] = z0.x; a[1] = z0.y; a[2] = -z0.y; a[3] = z0.x;
+                a[4] = z1.x; a[5] = z1.y; a[6] = -z1.y; a[7] = z1.x;
+            } else {  // {re,im; im,-re}
+                a[0] = z0.x; a[1] = z0.y; a[2] = z0.y; a[3] = -z0.x;
+                a[4] = z1.x; a[5] = z1.y; a[6] = z1.y; a[7] = -z1.x;
+            }
+        }
+    }
+    const bool two = FULL || kv > 8;
+#pragma unroll
+    for (int j = 0; j < kMaxNT; ++j) {
+        const int nt = ns + j * nsplit;
+        if (nt >= ntiles) break;
+        const int n = nt * 8 + g;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks) {
+            if (ks == 1 && !two) break;
+            const int kc = ks * 8 + 2 * t;
+            double2 b0, b1;
+            if (!HM) {
+                b0 = st[n * kLdTN + kc];
+                b1 = st[n * kLdTN + kc + 1];
+            } else {
+                b0 = st[kc * kLdTH + n];
+                b1 = st[(kc + 1) * kLdTH + n];
+            }
+            if (!val[ks][0]) b0 = zero;
+            if (!val[ks][1]) b1 = zero;
+            const double bfr[4] = {b0.x, b0.y, b1.x, b1.y};
+            mrhs::dmma(acc[0][j], afr[ks][0], bfr);
+            mrhs::dmma(acc[1][j], afr[ks][1], bfr);
+        }
+    }
+}
+
 __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint32_t* s_at,
                          uint64_t* full, uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
                          const int* s_opq) {
@@ -200,15 +259,16 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
         if (op < 0) break;
         const int32_t* hp = p.ops + (int64_t)op * kOpFields;
         const int out_b = __ldg(hp + 6), out_e = __ldg(hp + 7);
-        // zero the op's work outputs (groups add into them); w is zeroed by the launcher
-        for (int r = out_b; r < out_e; ++r) {
+        // work outputs no group writes are zeroed (packer.MR_ZERO; none at configs 1-4); the
+        // first group on an output range stores, later ones add; w is zeroed by the launcher
+        if (__ldg(p.mr_ranges + 3 * op + 2) & 1) for (int r = out_b; r < out_e; ++r) {
             const int64_t* rd = p.runs + (int64_t)r * kRunFields;
             if (__ldg(rd + 4) & 2) continue;
             double2* dp = p.work + __ldg(rd + 1) * (int64_t)R;
             const int64_t n = (int64_t)__ldg(rd + 2) * R;
             for (int64_t i = ctid; i < n; i += kCT) __stcg(dp + i, make_double2(0.0, 0.0));
         }
-        const int sb = __ldg(p.mr_ranges + 2 * op), se = __ldg(p.mr_ranges + 2 * op + 1);
+        const int sb = __ldg(p.mr_ranges + 3 * op), se = __ldg(p.mr_ranges + 3 * op + 1);
         int s = sb;
         while (s < se) {
             const SegD s0 = seg_at(p, s);
@@ -223,16 +283,33 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                     double2 acc = make_double2(0.0, 0.0);
                     for (int si = s; si < e; ++si) {
                         const SegD sg = seg_at(p, si);
-                        for (int k = 0; k < sg.rows; ++k) {
-                            const double2 v = __ldcg(p.work + (sg.m_off + k * sg.ld + j) * (int64_t)R + r);
+                        const double2* src = p.work + (sg.m_off + j) * (int64_t)R + r;
+                        const int64_t stride = sg.ld * (int64_t)R;
+                        int k = 0;
+                        for (; k + 4 <= sg.rows; k += 4) {  // four loads in flight, summed in order
+                            double2 v[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + (k + u) * stride);
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                acc.x += v[u].x;
+                                acc.y += v[u].y;
+                            }
+                        }
+                        for (; k < sg.rows; ++k) {
+                            const double2 v = __ldcg(src + k * stride);
                             acc.x += v.x;
                             acc.y += v.y;
                         }
                     }
                     bool at;
                     double2* dp = mrhs::out_ptr(p, out_b, out_e, s0.out_off + j, &at) + r;
-                    const double2 o = __ldcg(dp);
-                    __stcg(dp, make_double2(o.x + acc.x, o.y + acc.y));
+                    if (s0.first) {
+                        __stcg(dp, acc);
+                    } else {
+                        const double2 o = __ldcg(dp);
+                        __stcg(dp, make_double2(o.x + acc.x, o.y + acc.y));
+                    }
                 }
                 s = e;
                 continue;
@@ -268,48 +345,12 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                             if (active) {
                                 const double2* st = stages + (int64_t)stage * kStageElems;
                                 const double2* ti = st + kTElems + mg * 16 + g;
-#pragma unroll
-                                for (int ks = 0; ks < 2; ++ks) {
-                                    const int kc = ks * 8 + 2 * t;  // this lane's complex inputs kc, kc+1
-                                    if (ks * 8 >= kv) break;
-                                    const bool v0 = kc < kv, v1 = kc + 1 < kv;
-                                    double afr[2][8];
-#pragma unroll
-                                    for (int mt = 0; mt < 2; ++mt) {
-                                        const double2 zero = make_double2(0.0, 0.0);
-                                        const double2 z0 = v0 ? ti[kc * kLdI + mt * 8] : zero;
-                                        const double2 z1 = v1 ? ti[(kc + 1) * kLdI + mt * 8] : zero;
-                                        if (!hm) {  // {re,-im; im,re}
-                                            afr[mt][0] = z0.x; afr[mt][1] = z0.y;
-                                            afr[mt][2] = -z0.y; afr[mt][3] = z0.x;
-                                            afr[mt][4] = z1.x; afr[mt][5] = z1.y;
-                                            afr[mt][6] = -z1.y; afr[mt][7] = z1.x;
-                                        } else {  // {re,im; im,-re}
-                                            afr[mt][0] = z0.x; afr[mt][1] = z0.y;
-                                            afr[mt][2] = z0.y; afr[mt][3] = -z0.x;
-                                            afr[mt][4] = z1.x; afr[mt][5] = z1.y;
-                                            afr[mt][6] = z1.y; afr[mt][7] = -z1.x;
-                                        }
-                                    }
-#pragma unroll
-                                    for (int j = 0; j < kMaxNT; ++j) {
-                                        const int nt = ns + j * nsplit;
-                                        if (nt >= ntiles) break;
-                                        const int n = nt * 8 + g;
-                                        double2 b0, b1;
-                                        if (!hm) {
-                                            b0 = st[n * kLdTN + kc];
-                                            b1 = st[n * kLdTN + kc + 1];
-                                        } else {
-                                            b0 = st[kc * kLdTH + n];
-                                            b1 = st[(kc + 1) * kLdTH + n];
-                                        }
-                                        if (!v0) b0 = make_double2(0.0, 0.0);
-                                        if (!v1) b1 = make_double2(0.0, 0.0);
-                                        const double bfr[4] = {b0.x, b0.y, b1.x, b1.y};
-                                        mrhs::dmma(acc[0][j], afr[0], bfr);
-                                        mrhs::dmma(acc[1][j], afr[1], bfr);
-                                    }
+                                if (kv == kKC) {
+                                    if (hm) stage_mma<true, true>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
+                                    else stage_mma<false, true>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
+                                } else {
+                                    if (hm) stage_mma<true, false>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
+                                    else stage_mma<false, false>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
                                 }
                             }
                             __syncwarp();
@@ -338,6 +379,8 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                                     if (at) {
                                         atomicAdd(&dp->x, re);
                                         atomicAdd(&dp->y, im);
+                                    } else if (s0.first) {
+                                        __stcg(dp, make_double2(re, im));
                                     } else {
                                         const double2 o = __ldcg(dp);
                                         __stcg(dp, make_double2(o.x + re, o.y + im));

@@ -58,6 +58,9 @@ SEG_FIELDS = 8  # int64: m_off, buf, rows, cols, ld, mode, in_off, out_off
 RUN_FIELDS = 5  # int64: buf, off, len, dst, flags
 PIECE_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_off, out_off, info
 MR_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_buf, in_abs (element index), out_off
+MR_FIRST = 1 << 8  # mode-field flag: first group writing its outputs (flush stores, no read-add)
+MR_RANGE_FIELDS = 3  # int32 per op: mr_segs begin, end, flags
+MR_ZERO = 1  # op flag: some output position is written by no group -- zero the outputs first
 # piece info bits: [0,24) smem element offset in its stage, 24 stage_begin, 25 stage_end,
 # 26 direct (no stage: coherent loads from the work buffer), 27 input read from x directly,
 # 28 x window carried in the stage behind the matrix rows (in_off = its x index),
@@ -105,7 +108,7 @@ class Program:
     part_b: "Program | None" = None  # multi-GPU: the program launched after the y/u exchange
     stage_elems: int = STAGE_ELEMS  # bulk kernel stage size the pieces were packed for
     mr_segs: np.ndarray | None = None  # (n, MR_FIELDS) int64: multi-RHS segments, one input source each
-    mr_ranges: np.ndarray | None = None  # (n_ops, 2) int32: mr_segs range of every op
+    mr_ranges: np.ndarray | None = None  # (n_ops, 3) int32: mr_segs range + MR_ZERO flag of every op
 
     @property
     def n_ops(self) -> int:
@@ -843,6 +846,27 @@ def _resolve_inputs(segs, in_runs):
     return out
 
 
+def _mr_groups(mr, n_out):
+    """Mark the group structure of an op's multi-RHS segments.  A group is a run of
+    consecutive segments with the same mode and outputs (the engines accumulate it in
+    registers and flush once); the first group writing an output range gets MR_FIRST (its
+    flush stores).  Returns (segments, op flags): MR_ZERO when some output is left unwritten."""
+    out = []
+    covered = np.zeros(n_out, dtype=bool)
+    i = 0
+    while i < len(mr):
+        mode, o = mr[i][4], mr[i][7]
+        nout = mr[i][2] if mode == MODE_N else mr[i][3]
+        j = i + 1
+        while j < len(mr) and mr[j][4] == mode and mr[j][7] == o and (mr[j][2] if mode == MODE_N else mr[j][3]) == nout:
+            j += 1
+        first = not covered[o : o + nout].any()
+        covered[o : o + nout] = True
+        out.extend(q[:4] + (q[4] | (MR_FIRST if first else 0),) + q[5:] for q in mr[i:j])
+        i = j
+    return out, (0 if covered.all() else MR_ZERO)
+
+
 def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
     """Flatten op tuples into arrays in the phased order; the fused order is a
     permutation (``fused_order[ticket] = op index``).  ``keep_waits_on``: in a partial program
@@ -889,8 +913,9 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
         pieces.extend(_pieces(ordered, has_x, stage_elems))
         pc_e = len(pieces)
         mr_b = len(mr_segs)
-        mr_segs.extend(_resolve_inputs(ordered, in_runs))
-        mr_ranges.append((mr_b, len(mr_segs)))
+        mr, mr_flags = _mr_groups(_resolve_inputs(ordered, in_runs), n_out)
+        mr_segs.extend(mr)
+        mr_ranges.append((mr_b, len(mr_segs), mr_flags))
         w_b = len(waits)
         waits.extend(wt)
         w_e = len(waits)
@@ -919,5 +944,5 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
         arena_elems=arena_elems,
         stage_elems=stage_elems,
         mr_segs=np.asarray(mr_segs, dtype=np.int64).reshape(-1, MR_FIELDS),
-        mr_ranges=np.asarray(mr_ranges, dtype=np.int32).reshape(-1, 2),
+        mr_ranges=np.asarray(mr_ranges, dtype=np.int32).reshape(-1, MR_RANGE_FIELDS),
     )
