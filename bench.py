@@ -458,6 +458,8 @@ def run_multi_rhs(args, world, rank, local_rank):
         "gpu_launches": steps,
         "clocks": clk,
     }
+    if os.environ.get("UHMV_PROFILE"):
+        line["engine_cycles"] = op.profile_mr(R)
     print(json.dumps(line), flush=True)
 
 

@@ -573,10 +573,13 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
             return cuda_fail(e, "occupancy(mrhs)");
         }
         p->mrhs_grid = (per_sm < 1 ? 1 : per_sm) * p->sm_count;
-        e = cudaFuncSetAttribute(mrtc::uhmv_mrtc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(mrtc::uhmv_mrtc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  mrtc::kSmemBytes);
         if (e == cudaSuccess)
-            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrtc::uhmv_mrtc_kernel,
+            e = cudaFuncSetAttribute(mrtc::uhmv_mrtc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     mrtc::kSmemBytes);
+        if (e == cudaSuccess)
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrtc::uhmv_mrtc_kernel<false>,
                                                               mrtc::kThreads, mrtc::kSmemBytes);
         if (e != cudaSuccess) {
             delete p;
@@ -739,12 +742,17 @@ int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, in
     mp.ticket = plan->d.ticket;
     mp.exit_count = plan->d.exit_count;
     mp.n_counters = pr.n_counters;
+    mp.prof = nullptr;
     if (plan->mrhs_engine == 1) {
         int grid = plan->mrhs_grid < pr.n_ops ? plan->mrhs_grid : pr.n_ops;
         mrhs::uhmv_mrhs_kernel<<<grid, mrhs::kThreads, 0, st>>>(mp);
     } else {
         int grid = plan->mrtc_grid < pr.n_ops ? plan->mrtc_grid : pr.n_ops;
-        mrtc::uhmv_mrtc_kernel<<<grid, mrtc::kThreads, mrtc::kSmemBytes, st>>>(mp);
+        mp.prof = plan->prof;
+        if (mp.prof)
+            mrtc::uhmv_mrtc_kernel<true><<<grid, mrtc::kThreads, mrtc::kSmemBytes, st>>>(mp);
+        else
+            mrtc::uhmv_mrtc_kernel<false><<<grid, mrtc::kThreads, mrtc::kSmemBytes, st>>>(mp);
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "multi-RHS kernel launch");

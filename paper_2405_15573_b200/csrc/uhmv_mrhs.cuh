@@ -44,6 +44,7 @@ struct Params {
     unsigned long long* ticket;
     uint32_t* exit_count;
     int32_t n_counters;
+    unsigned long long* prof;  // diagnostics: per-CTA cycle counters (staged engine), or null
 };
 
 __device__ __forceinline__ void dmma(double (&d)[4], const double (&a)[8], const double (&b)[4]) {

@@ -46,7 +46,7 @@ constexpr int kIElems = kKC * kLdI;
 constexpr int kStageElems = kTElems + kIElems;  // complex
 constexpr int kOpSlots = 2;
 constexpr int kSmemStages = kNST * kStageElems * 16;
-constexpr int kSmemBytes = kSmemStages + kNP * 8 + kNP * 4 + (2 * kNST + 2 * kOpSlots) * 8 + 64;
+constexpr int kSmemBytes = kSmemStages + kNP * 8 + kNP * 4 + (2 * kNST + 2 * kOpSlots) * 8 + 32 + 48 * 8;
 
 using mrhs::Params;
 using bulk::mbar_arrive;
@@ -104,13 +104,20 @@ __device__ __forceinline__ int group_end(const Params& p, int s, int se, const S
     return e;
 }
 
+// Diagnostics (PROF): per-CTA cycle counters, summed by DeviceOperator.profile_mr --
+//   [0] producer waiting for a free stage   [1] producer waiting on dependencies
+//   [2] producer issuing copies            [3] producer ticket + op slot
+//   [8 + 4*kind + {0 wait data, 1 mma, 2 table + flush, 3 S reduction}]  consumer warp 0
+//   [40] consumer warp 0 waiting for the next op
+template <bool PROF>
 __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint64_t* empty,
-                         uint64_t* opfull, uint64_t* opempty, int* s_opq) {
+                         uint64_t* opfull, uint64_t* opempty, int* s_opq, unsigned long long* pr) {
     const int lane = threadIdx.x & 31;
     const int R = p.nrhs;
     uint32_t stage = 0, sphase = 0, qphase = 0;
     int q = 0;
     for (;;) {
+        long long t0 = PROF ? clock64() : 0;
         int op = -1;
         if (lane == 0) {
             const unsigned long long tk = atomicAdd(p.ticket, 1ull);
@@ -118,6 +125,11 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
         }
         op = __shfl_sync(0xffffffffu, op, 0);
         mbar_wait(&opempty[q], qphase ^ 1u);
+        if (PROF && lane == 0) {
+            const long long t1 = clock64();
+            pr[3] += t1 - t0;
+            t0 = t1;
+        }
         if (op >= 0) {
             const int32_t* hp = p.ops + (int64_t)op * kOpFields;
             const int wb = __ldg(hp + 8), we = __ldg(hp + 9);
@@ -129,6 +141,11 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
             __syncwarp();
             // work inputs written by other CTAs (generic proxy) are read below by the TMA engine
             asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        if (PROF && lane == 0) {
+            const long long t1 = clock64();
+            pr[1] += t1 - t0;
+            t0 = t1;
         }
         if (lane == 0) {
             s_opq[q] = op;
@@ -157,7 +174,9 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
                         const double2* IN = (sg.in_buf == kBufX ? p.x : p.work) + sg.in_abs * (int64_t)R + rp;
                         for (int k0 = 0; k0 < K; k0 += kKC) {
                             const int kv = min(kKC, K - k0);
+                            long long tw = PROF ? clock64() : 0;
                             mbar_wait(&empty[stage], sphase ^ 1u);
+                            if (PROF && lane == 0) pr[0] += clock64() - tw;
                             double2* st = stages + (int64_t)stage * kStageElems;
                             double2* ti = st + kTElems;
                             const uint32_t bytes = (uint32_t)(np * kv + kv * rpn) * 16u;
@@ -182,6 +201,7 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
             }
             s = e;
         }
+        if (PROF && lane == 0) pr[2] += clock64() - t0;
         if (++q == kOpSlots) {
             q = 0;
             qphase ^= 1u;
@@ -244,20 +264,25 @@ __device__ __forceinline__ void stage_mma(double (&acc)[2][kMaxNT][4], const dou
     }
 }
 
+template <bool PROF>
 __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint32_t* s_at,
                          uint64_t* full, uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
-                         const int* s_opq) {
+                         const int* s_opq, unsigned long long* pr) {
     const int ctid = threadIdx.x;  // 0 .. kCT-1
     const int lane = ctid & 31, cw = ctid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int R = p.nrhs;
     uint32_t stage = 0, sphase = 0, qphase = 0;
     int q = 0;
+    const bool rec = PROF && ctid == 0;
     for (;;) {
+        long long t0 = PROF ? clock64() : 0;
         mbar_wait(&opfull[q], qphase);
         const int op = s_opq[q];
+        if (rec) pr[40] += clock64() - t0;
         if (op < 0) break;
         const int32_t* hp = p.ops + (int64_t)op * kOpFields;
+        unsigned long long* pk = pr + 8 + 4 * (PROF ? __ldg(hp + 12) : 0);
         const int out_b = __ldg(hp + 6), out_e = __ldg(hp + 7);
         // work outputs no group writes are zeroed (packer.MR_ZERO; none at configs 1-4); the
         // first group on an output range stores, later ones add; w is zeroed by the launcher
@@ -276,6 +301,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
             const int nout = seg_nout(s0);
             if (s0.mode == kModeS) {
                 // partial-vector reduction: out[j][r] = sum_k W[k][j][r] (work, L2 reads)
+                if (PROF) t0 = clock64();
                 cons_sync();
                 const int64_t tot = (int64_t)nout * R;
                 for (int64_t qq = ctid; qq < tot; qq += kCT) {
@@ -311,6 +337,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                         __stcg(dp, make_double2(o.x + acc.x, o.y + acc.y));
                     }
                 }
+                if (rec) pk[3] += clock64() - t0;
                 s = e;
                 continue;
             }
@@ -323,6 +350,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                 for (int n0 = 0; n0 < nout; n0 += kNP) {
                     const int np = min(kNP, nout - n0);
                     const int ntiles = (np + 7) >> 3;
+                    if (PROF) t0 = clock64();
                     cons_sync();  // previous flush done with the table; work outputs zeroed
                     for (int i = ctid; i < np; i += kCT) {
                         bool at;
@@ -330,6 +358,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                         s_at[i] = at ? 1u : 0u;
                     }
                     cons_sync();
+                    if (rec) pk[2] += clock64() - t0;
                     double acc[2][kMaxNT][4];
 #pragma unroll
                     for (int a = 0; a < 2; ++a)
@@ -341,7 +370,13 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                         const int K = seg_k(seg_at(p, si));
                         for (int k0 = 0; k0 < K; k0 += kKC) {
                             const int kv = min(kKC, K - k0);
+                            if (PROF) t0 = clock64();
                             mbar_wait(&full[stage], sphase);
+                            if (rec) {
+                                const long long t1 = clock64();
+                                pk[0] += t1 - t0;
+                                t0 = t1;
+                            }
                             if (active) {
                                 const double2* st = stages + (int64_t)stage * kStageElems;
                                 const double2* ti = st + kTElems + mg * 16 + g;
@@ -354,6 +389,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                                 }
                             }
                             __syncwarp();
+                            if (rec) pk[1] += clock64() - t0;
                             if (lane == 0) mbar_arrive(&empty[stage]);
                             if (++stage == kNST) {
                                 stage = 0;
@@ -361,6 +397,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                             }
                         }
                     }
+                    if (PROF) t0 = clock64();
                     if (active) {  // flush: lane holds out[2t+e][g] for its tiles (re d=0, im d=1)
 #pragma unroll
                         for (int j = 0; j < kMaxNT; ++j) {
@@ -389,6 +426,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                             }
                         }
                     }
+                    if (rec) pk[2] += clock64() - t0;
                 }
             }
             s = e;
@@ -410,6 +448,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
     }
 }
 
+template <bool PROF>
 __global__ void __launch_bounds__(kThreads, 1) uhmv_mrtc_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     double2* stages = reinterpret_cast<double2*>(smem);
@@ -421,6 +460,8 @@ __global__ void __launch_bounds__(kThreads, 1) uhmv_mrtc_kernel(const Params p) 
     uint64_t* opempty = opfull + kOpSlots;
     int* s_opq = reinterpret_cast<int*>(opempty + kOpSlots);
     int* flag = s_opq + kOpSlots;
+    unsigned long long* sprof = reinterpret_cast<unsigned long long*>(flag + 2);  // 8-aligned
+    if (PROF && threadIdx.x < 48) sprof[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kNST; ++s) {
             mbar_init(&full[s], 1);
@@ -434,11 +475,12 @@ __global__ void __launch_bounds__(kThreads, 1) uhmv_mrtc_kernel(const Params p) 
     }
     __syncthreads();
     if ((threadIdx.x >> 5) == kCW) {
-        producer(p, stages, full, empty, opfull, opempty, s_opq);
+        producer<PROF>(p, stages, full, empty, opfull, opempty, s_opq, sprof);
     } else {
-        consumer(p, stages, s_out, s_at, full, empty, opfull, opempty, s_opq);
+        consumer<PROF>(p, stages, s_out, s_at, full, empty, opfull, opempty, s_opq, sprof);
     }
     __syncthreads();
+    if (PROF && threadIdx.x < 48) p.prof[(int64_t)blockIdx.x * 64 + threadIdx.x] = sprof[threadIdx.x];
     if (threadIdx.x == 0) {
         __threadfence();
         const uint32_t prev = atomicAdd(p.exit_count, 1u);

@@ -181,6 +181,31 @@ class DeviceOperator:
                 out["kinds"][name] = dict(zip(cats, row))
         return out
 
+    def profile_mr(self, R=64, adjoint=False):
+        """Diagnostics: one multi-RHS block product with the staged engine's per-CTA cycle
+        counters on (csrc/uhmv_mrtc.cuh), summed over CTAs."""
+        torch = self.torch
+        mr, _ = self._mr_plan()
+        buf = torch.zeros((4096, 64), dtype=torch.int64, device=self.device)
+        _lib.check(_lib.lib().uhmv_plan_set_profile(mr._plan, ctypes.c_void_p(buf.data_ptr())), "set_profile")
+        p = self.packed
+        n_in = p.n_rows if adjoint else p.n_cols
+        try:
+            self.matmat(torch.ones((n_in, R), dtype=torch.complex128, device=self.device), adjoint=adjoint)
+            torch.cuda.synchronize(self.device)
+        finally:
+            _lib.check(_lib.lib().uhmv_plan_set_profile(mr._plan, None), "set_profile")
+        from .packer import KIND_NAMES
+
+        tot = buf.sum(dim=0).tolist()
+        out = {"producer": dict(wait_stage=tot[0], wait_dep=tot[1], issue=tot[2], ticket_slot=tot[3]),
+               "consumer_wait_op": tot[40], "kinds": {}}
+        for k, name in enumerate(KIND_NAMES[:6]):
+            row = tot[8 + 4 * k : 12 + 4 * k]
+            if any(row):
+                out["kinds"][name] = dict(zip(["wait_data", "mma", "table_flush", "s_reduce"], row))
+        return out
+
     # ---- execution ----
     def _stream(self, stream):
         torch = self.torch
