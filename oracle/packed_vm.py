@@ -147,15 +147,20 @@ def run_op_mr(prog, i, bufs, R):
         g = e
 
 
-def vm_matmat(packed, V, adjoint=False):
-    """Multi-RHS program interpreter: V (n_in, R) -> W (n_out, R)."""
+def vm_matmat(packed, V, adjoint=False, programs=None):
+    """Multi-RHS program interpreter: V (n_in, R) -> W (n_out, R).  ``programs``: a
+    (fwd, adj, work_len) re-chunked pair (PackedOperator.programs) instead of fwd / adj."""
     prog = packed.adj if adjoint else packed.fwd
+    work_len = packed.work_len
+    if programs is not None:
+        prog = programs[1] if adjoint else programs[0]
+        work_len = programs[2]
     n_in, n_out = (packed.n_rows, packed.n_cols) if adjoint else (packed.n_cols, packed.n_rows)
     X = np.asarray(V, dtype=np.complex128)
     R = X.shape[1]
     assert X.shape[0] == n_in
     W = np.zeros((n_out, R), dtype=np.complex128)
-    work = np.zeros((packed.work_len, R), dtype=np.complex128)
+    work = np.zeros((work_len, R), dtype=np.complex128)
     bufs = {BUF_ARENA: packed.arena, BUF_WORK: work, BUF_X: X, BUF_W: W}
     for i in prog.fused_order.tolist():
         run_op_mr(prog, i, bufs, R)

@@ -269,7 +269,8 @@ class DeviceOperator:
 
             p = self.packed
             rows = int(os.environ.get("UHMV_MR_ROWS", MR_ROWS))
-            if rows > 0 and p.geo is not None and p.world == 1 and self.progs == (p.fwd, p.adj):
+            can = p.geo is not None or (rows, rows) in p.rechunked
+            if rows > 0 and can and p.world == 1 and self.progs == (p.fwd, p.adj):
                 fwd, adj, work_len = p.programs(rows_per_chunk=rows, far_rows=rows)
                 self._mr = (DeviceOperator(p, device=self.device, programs=(fwd, adj), share_with=self), work_len)
             else:

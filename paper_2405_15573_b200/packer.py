@@ -135,18 +135,24 @@ class PackedOperator:
     exchange: dict = field(default_factory=dict)  # per direction: (ex_off, ex_len) block layout
     geo: dict | None = field(default=None, repr=False)  # index structure, for re-chunked programs
     build_kw: dict | None = field(default=None, repr=False)
+    rechunked: dict = field(default_factory=dict, repr=False)  # (rows, far_rows) -> (fwd, adj, work_len)
 
     def programs(self, *, rows_per_chunk: int, far_rows: int):
         """(fwd, adj, work_len): the same operator and arena with NEAR / FAR ops re-chunked
-        (the multi-RHS engine wants whole-leaf output blocks).  Single-GPU only."""
+        (the multi-RHS engine wants whole-leaf output blocks).  Single-GPU only; cached (and
+        saved by packed_io) per chunking."""
+        key = (int(rows_per_chunk), int(far_rows))
+        if key in self.rechunked:
+            return self.rechunked[key]
         if self.geo is None or self.world != 1:
-            raise ValueError("re-chunking needs a single-GPU pack")
+            raise ValueError("re-chunking needs a single-GPU pack with its index structure")
         kw = dict(self.build_kw)
         kw["rows_per_chunk"] = rows_per_chunk
         kw["split"] = dict(kw["split"], far_rows=far_rows)
         fwd, work_f, _ = _build_program(self.geo, adjoint=False, **kw)
         adj, work_a, _ = _build_program(self.geo, adjoint=True, **kw)
-        return fwd, adj, max(work_f, work_a, 1)
+        self.rechunked[key] = (fwd, adj, max(work_f, work_a, 1))
+        return self.rechunked[key]
 
 
 def _leaves_under(tree):

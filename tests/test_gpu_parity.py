@@ -178,3 +178,22 @@ def test_power_iteration_on_device(golden):
     rep = verification.compression_error(u, farfield_only(u), iters=30, seed=0)
     assert abs(rep.rel_spectral_estimate - float(ex["ce_rel"])) <= 1e-9 * float(ex["ce_rel"])
     assert rep.iterations == int(ex["ce_used"])
+
+
+def test_loaded_packed_operator(golden, tmp_path):
+    """A packed operator saved to disk and reloaded (packed_io) runs on the device without
+    the source operator: single-RHS (bulk) and multi-RHS (re-chunked programs from the file)."""
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packed_io import load_packed, save_packed
+    from paper_2405_15573_b200.packer import pack
+
+    name, u, ex = golden
+    path = str(tmp_path / "op.npz")
+    save_packed(path, pack(u))
+    dop = DeviceOperator(load_packed(path), device="cuda:0")
+    for adjoint, vk, rk in ((False, "vf_0", "ref_fwd_0"), (True, "va_0", "ref_adj_0")):
+        x = torch.from_numpy(np.asarray(ex[vk], dtype=np.complex128)).cuda()
+        assert rel(dop.matvec(x, adjoint=adjoint, mode="bulk").cpu().numpy(), ex[rk]) <= TOL
+        X = torch.stack([x, 2 * x], dim=1)
+        W = dop.matmat(X, adjoint=adjoint).cpu().numpy()
+        assert rel(W[:, 0], ex[rk]) <= TOL and rel(W[:, 1], 2 * ex[rk]) <= TOL
