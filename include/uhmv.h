@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 6
+#define UHMV_ABI_VERSION 7
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -64,6 +64,12 @@ typedef struct uhmv_program {
                                  mode field: low byte mode, bit 8 first writer of its outputs */
     const int32_t* mr_ranges; /* n_ops x 3 int32: mr_segs range of every op + flags
                                  (bit 0: zero the op's work outputs first)                   */
+    int32_t n_tmaps;          /* distinct leading dimensions of the arena matrices the
+                                 multi-RHS segments read (mr_segs mode field bits 16..)      */
+    const int64_t* tmap_lds;  /* HOST array of n_tmaps leading dimensions (complex elements) */
+    void* tmaps;              /* DEVICE buffer, 2 * n_tmaps * 128 bytes, 64-B aligned, that
+                                 uhmv_plan_create fills with TMA tensor maps over the arena
+                                 (per ld: a 16 x 16 and a 16 x 80 complex box)              */
 } uhmv_program;
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */
@@ -72,6 +78,8 @@ typedef struct uhmv_desc {
     int32_t device;           /* CUDA device ordinal */
     int64_t n_rows, n_cols;   /* operator shape (bct.shape, clustering.py:196-198) */
     const void* arena;        /* complex128 bases, coupling and dense slabs (read-only) */
+    int64_t arena_len;        /* arena elements; the allocation extends max(tmap_lds)
+                                 elements further (TMA rows of the last ld may overhang) */
     void* work;               /* complex128 scratch: partials, y, staging u, z */
     int64_t work_len;
     uint32_t* counters;       /* >= max(n_counters) zero-initialised uint32 */

@@ -127,7 +127,7 @@ def run_op_mr(prog, i, bufs, R):
         mode, o0 = segs[g][4] & 0xFF, segs[g][7]
         nout = segs[g][2] if mode == MODE_N else segs[g][3]
         e = g + 1
-        while e < len(segs) and segs[e][4] == segs[g][4] and segs[e][7] == o0 and (segs[e][2] if mode == MODE_N else segs[e][3]) == nout:
+        while e < len(segs) and segs[e][4] & 0x1FF == segs[g][4] & 0x1FF and segs[e][7] == o0 and (segs[e][2] if mode == MODE_N else segs[e][3]) == nout:
             e += 1
         blk = np.zeros((nout, R), dtype=np.complex128)
         for m_off, ld, rows, cols, _mode, in_buf, in_abs, _o in segs[g:e]:

@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "check", "LIB_PATH", "MAX_PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 6
+ABI_VERSION = 7
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -39,6 +39,9 @@ class UhmvProgram(ctypes.Structure):
         ("stage_elems", ctypes.c_int32),
         ("mr_segs", ctypes.c_void_p),
         ("mr_ranges", ctypes.c_void_p),
+        ("n_tmaps", ctypes.c_int32),
+        ("tmap_lds", ctypes.c_void_p),
+        ("tmaps", ctypes.c_void_p),
     ]
 
 
@@ -49,6 +52,7 @@ class UhmvDesc(ctypes.Structure):
         ("n_rows", ctypes.c_int64),
         ("n_cols", ctypes.c_int64),
         ("arena", ctypes.c_void_p),
+        ("arena_len", ctypes.c_int64),
         ("work", ctypes.c_void_p),
         ("work_len", ctypes.c_int64),
         ("counters", ctypes.c_void_p),

@@ -29,6 +29,8 @@
 // progress does not depend on co-residency.  The last CTA to exit resets all counters, so the
 // launch is self-cleaning and CUDA-graph capturable.
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors of the multi-RHS engine)
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -36,6 +38,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/uhmv.h"
 
@@ -457,6 +460,48 @@ static int check_program(const uhmv_program& pr, const char* name) {
     return UHMV_OK;
 }
 
+// TMA tensor maps over the arena for the staged multi-RHS engine: for every leading dimension
+// L the arena is viewed as a 2-D tensor of ceil(arena_len / L) rows x 2L doubles (row stride
+// 16 L bytes), so a segment at element offset m_off starts at (row, col) = divmod(m_off, L)
+// whatever its alignment.  Box 0 (N segments): 16 rows x 16 complex; box 1 (H segments):
+// 16 rows x 80 complex.  Columns past 2L are zero-filled by the TMA unit.
+static int encode_tmaps(const uhmv_desc* d, const uhmv_program& pr, const char* name) {
+    if (pr.n_tmaps <= 0) return UHMV_OK;
+    if (!pr.tmap_lds || !pr.tmaps) return fail(UHMV_EINVAL, std::string(name) + ": null tensor-map buffers");
+    if (reinterpret_cast<uintptr_t>(pr.tmaps) % 64 || reinterpret_cast<uintptr_t>(d->arena) % 16)
+        return fail(UHMV_EINVAL, std::string(name) + ": misaligned tensor-map buffer or arena");
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+            return fail(UHMV_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    std::vector<CUtensorMap> maps(2 * (size_t)pr.n_tmaps);
+    for (int i = 0; i < pr.n_tmaps; ++i) {
+        const int64_t L = pr.tmap_lds[i];
+        if (L <= 0 || L > (1 << 24)) return fail(UHMV_EINVAL, std::string(name) + ": bad leading dimension");
+        const cuuint64_t rows = (cuuint64_t)((d->arena_len + L - 1) / L);
+        const cuuint64_t gdim[2] = {(cuuint64_t)(2 * L), rows > 0 ? rows : 1};
+        const cuuint64_t gstride[1] = {(cuuint64_t)(16 * L)};
+        const cuuint32_t estride[2] = {1, 1};
+        for (int b = 0; b < 2; ++b) {
+            const cuuint32_t box[2] = {b == 0 ? 2u * mrtc::kKC : 2u * mrtc::kNP, (cuuint32_t)mrtc::kKC};
+            CUresult r = encode(&maps[2 * i + b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(d->arena),
+                                gdim, gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(UHMV_ECUDA, std::string(name) + ": cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+        }
+    }
+    cudaError_t e = cudaMemcpy(pr.tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tensor maps)");
+    return UHMV_OK;
+}
+
 int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     if (!desc || !out) return fail(UHMV_EINVAL, "uhmv_plan_create: null argument");
     *out = nullptr;
@@ -475,6 +520,10 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     if (!p) return fail(UHMV_ENOMEM, "uhmv_plan_create: out of host memory");
     std::memset(p, 0, sizeof(*p));
     p->d = *desc;
+    if ((rc = encode_tmaps(desc, desc->fwd, "fwd")) || (rc = encode_tmaps(desc, desc->adj, "adj"))) {
+        delete p;
+        return rc;
+    }
     e = cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, desc->device);
     if (e != cudaSuccess) {
         delete p;
@@ -743,10 +792,12 @@ int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, in
     mp.exit_count = plan->d.exit_count;
     mp.n_counters = pr.n_counters;
     mp.prof = nullptr;
+    mp.tmaps = static_cast<const CUtensorMap*>(pr.tmaps);
     if (plan->mrhs_engine == 1) {
         int grid = plan->mrhs_grid < pr.n_ops ? plan->mrhs_grid : pr.n_ops;
         mrhs::uhmv_mrhs_kernel<<<grid, mrhs::kThreads, 0, st>>>(mp);
     } else {
+        if (pr.n_tmaps <= 0 && pr.n_ops > 0) return fail(UHMV_EINVAL, "multi-RHS program without tensor maps");
         int grid = plan->mrtc_grid < pr.n_ops ? plan->mrtc_grid : pr.n_ops;
         mp.prof = plan->prof;
         if (mp.prof)

@@ -45,6 +45,7 @@ struct Params {
     uint32_t* exit_count;
     int32_t n_counters;
     unsigned long long* prof;  // diagnostics: per-CTA cycle counters (staged engine), or null
+    const CUtensorMap* tmaps;  // staged engine: 2 TMA maps per leading dimension (mr_segs bits 16..)
 };
 
 __device__ __forceinline__ void dmma(double (&d)[4], const double (&a)[8], const double (&b)[4]) {

@@ -9,8 +9,10 @@
 // Warp specialisation (one CTA of 8 consumer warps + 1 producer warp per SM):
 //   * the producer warp claims ops, polls their dependency counters (ld.acquire.gpu), then
 //     streams every K-chunk of every segment -- KC = 16 complex inputs: the matching T slab
-//     (N: nout rows x KC, H: KC rows x nout) and the IN block (KC rows x 64 RHS) -- into a
-//     5-deep shared-memory ring with cp.async.bulk (TMA engine) completing on mbarriers;
+//     (N: nout rows x KC, H: KC rows x nout) as 2-D TMA tensor boxes (one map pair per leading
+//     dimension over the whole arena, cp.async.bulk.tensor) and the IN block (KC rows x 64
+//     RHS, contiguous) as one cp.async.bulk -- into a 6-deep shared-memory ring completing on
+//     mbarriers: 2-6 copy instructions per 16 KFLOP/lane stage;
 //   * the consumer warps own a fixed (16-RHS, n-tile) share of the output block, accumulate
 //     the whole segment group in registers (up to 2 x 5 DMMA tiles per warp) and flush it once
 //     (fp64 atomics into w -- at most two addends per entry, so order-independent -- a store
@@ -23,8 +25,9 @@
 //   A (N: {re,-im; im,re}, H: {re,im; im,-re}) from z0 = IN[2t][g], z1 = IN[2t+1][g];
 //   B = T[n][2t], T[n][2t+1] (N) or T[2t][n], T[2t+1][n] (H) with n = g;
 //   D: v = e + 2d -> out[2t+e][g], part d: every lane flushes whole complex outputs.
-// Shared-memory row pitches (in complex): IN 65, T_N 17, T_H 81 -- each quarter-warp's 8
-// 16-B accesses hit 8 distinct bank groups (conflict-free).
+// Shared-memory row pitches (in complex) are the TMA box widths -- IN rpn, T_N 16, T_H 80 --
+// so some loads take 2-4 bank wavefronts; at one DMMA per 32 clk per SM sub-partition the
+// shared-memory pipe stays far below its limit (ncu: ~10%).
 
 #pragma once
 
@@ -36,13 +39,12 @@ constexpr int kThreads = kCT + 32;      // + producer warp
 constexpr int kRP = 64;                 // complex RHS per pass
 constexpr int kNP = 80;                 // outputs per pass
 constexpr int kKC = 16;                 // complex inputs per stage
-constexpr int kNST = 5;                 // ring depth
+constexpr int kNST = 6;                 // ring depth
 constexpr int kMaxNT = 5;               // n-tiles per warp
-constexpr int kLdTN = kKC + 1;          // 17
-constexpr int kLdTH = kNP + 1;          // 81
-constexpr int kLdI = kRP + 1;           // 65
+constexpr int kLdTN = kKC;              // N slab [nout][16] (TMA boxes of 16 rows x 16 complex)
+constexpr int kLdTH = kNP;              // H slab [16][80]   (one TMA box of 16 rows x 80 complex)
 constexpr int kTElems = (kNP * kLdTN > kKC * kLdTH) ? kNP * kLdTN : kKC * kLdTH;
-constexpr int kIElems = kKC * kLdI;
+constexpr int kIElems = kKC * kRP;      // IN block [16][rpn] (one bulk copy when rpn == R)
 constexpr int kStageElems = kTElems + kIElems;  // complex
 constexpr int kOpSlots = 2;
 constexpr int kSmemStages = kNST * kStageElems * 16;
@@ -59,6 +61,14 @@ __device__ __forceinline__ void cons_sync() {
     asm volatile("bar.sync 2, %0;" ::"n"(kCT) : "memory");
 }
 
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            su32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+        : "memory");
+}
+
 __device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -71,6 +81,7 @@ struct SegD {
     int64_t m_off, ld, in_abs;
     int rows, cols, mode, in_buf, out_off;
     int first;  // first group writing these outputs: the flush stores (packer.MR_FIRST)
+    int tmap;   // index of the TMA map pair of this segment's leading dimension
 };
 
 __device__ __forceinline__ SegD seg_at(const Params& p, int i) {
@@ -83,6 +94,7 @@ __device__ __forceinline__ SegD seg_at(const Params& p, int i) {
     const int mf = (int)__ldg(d + 4);
     s.mode = mf & 0xFF;
     s.first = (mf >> 8) & 1;
+    s.tmap = mf >> 16;
     s.in_buf = (int)__ldg(d + 5);
     s.in_abs = __ldg(d + 6);
     s.out_off = (int)__ldg(d + 7);
@@ -170,8 +182,11 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
                     for (int si = s; si < e; ++si) {
                         const SegD sg = seg_at(p, si);
                         const int K = seg_k(sg);
-                        const double2* T = p.arena + sg.m_off;
+                        // TMA coordinates: the segment starts at (row, col) = divmod(m_off, ld)
+                        const int y0 = (int)(sg.m_off / sg.ld), x0 = (int)(sg.m_off % sg.ld);
+                        const CUtensorMap* map = p.tmaps + 2 * sg.tmap + (hm ? 1 : 0);
                         const double2* IN = (sg.in_buf == kBufX ? p.x : p.work) + sg.in_abs * (int64_t)R + rp;
+                        const int nbox = hm ? 1 : (np + kKC - 1) / kKC;
                         for (int k0 = 0; k0 < K; k0 += kKC) {
                             const int kv = min(kKC, K - k0);
                             long long tw = PROF ? clock64() : 0;
@@ -179,18 +194,23 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
                             if (PROF && lane == 0) pr[0] += clock64() - tw;
                             double2* st = stages + (int64_t)stage * kStageElems;
                             double2* ti = st + kTElems;
-                            const uint32_t bytes = (uint32_t)(np * kv + kv * rpn) * 16u;
+                            // TMA boxes land whole (zero-filled past the row end); rows past kv
+                            // are masked by the consumers
+                            const uint32_t bytes = (uint32_t)(nbox * kKC * (hm ? kNP : kKC) + kv * rpn) * 16u;
                             if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
                             __syncwarp();
-                            if (!hm) {  // T rows n0.., columns k0..k0+kv
-                                for (int n = lane; n < np; n += 32)
-                                    g2s(st + n * kLdTN, T + (int64_t)(n0 + n) * sg.ld + k0, kv * 16u, &full[stage]);
-                            } else {  // T rows k0..k0+kv, columns n0..
-                                for (int k = lane; k < kv; k += 32)
-                                    g2s(st + k * kLdTH, T + (int64_t)(k0 + k) * sg.ld + n0, np * 16u, &full[stage]);
+                            if (!hm) {  // T rows n0 + 16b.., columns k0..k0+16
+                                if (lane < nbox)
+                                    tma2d(st + lane * kKC * kLdTN, map, 2 * (x0 + k0), y0 + n0 + kKC * lane, &full[stage]);
+                            } else if (lane == 0) {  // T rows k0..k0+16, columns n0..n0+80
+                                tma2d(st, map, 2 * (x0 + n0), y0 + k0, &full[stage]);
                             }
-                            for (int k = lane; k < kv; k += 32)
-                                g2s(ti + k * kLdI, IN + (int64_t)(k0 + k) * R, rpn * 16u, &full[stage]);
+                            if (rpn == R) {  // the IN rows are contiguous: one copy
+                                if (lane == 31) g2s(ti, IN + (int64_t)k0 * R, (uint32_t)(kv * R) * 16u, &full[stage]);
+                            } else {
+                                for (int k = lane; k < kv; k += 32)
+                                    g2s(ti + k * rpn, IN + (int64_t)(k0 + k) * R, rpn * 16u, &full[stage]);
+                            }
                             if (++stage == kNST) {
                                 stage = 0;
                                 sphase ^= 1u;
@@ -213,8 +233,8 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
 // A fragments are loaded up front; FULL: every input of the stage is valid (no masking).
 template <bool HM, bool FULL>
 __device__ __forceinline__ void stage_mma(double (&acc)[2][kMaxNT][4], const double2* st,
-                                          const double2* ti, int kv, int ns, int nsplit, int ntiles,
-                                          int g, int t) {
+                                          const double2* ti, int ldi, int kv, int ns, int nsplit,
+                                          int ntiles, int g, int t) {
     const double2 zero = make_double2(0.0, 0.0);
     double afr[2][2][8];
     bool val[2][2];
@@ -225,8 +245,8 @@ __device__ __forceinline__ void stage_mma(double (&acc)[2][kMaxNT][4], const dou
         val[ks][1] = FULL || kc + 1 < kv;
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) {
-            const double2 z0 = val[ks][0] ? ti[kc * kLdI + mt * 8] : zero;
-            const double2 z1 = val[ks][1] ? ti[(kc + 1) * kLdI + mt * 8] : zero;
+            const double2 z0 = val[ks][0] ? ti[kc * ldi + mt * 8] : zero;
+            const double2 z1 = val[ks][1] ? ti[(kc + 1) * ldi + mt * 8] : zero;
             double* a = afr[ks][mt];
             if (!HM) {  // {re,-im; im,re}
                 a[0] = z0.x; a[1] = z0.y; a[2] = -z0.y; a[3] = z0.x;
@@ -343,7 +363,8 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
             }
             const bool hm = s0.mode == kModeH;
             for (int rp = 0; rp < R; rp += kRP) {
-                const int n_mg = min(kRP, R - rp) / 16;
+                const int rpn = min(kRP, R - rp);
+                const int n_mg = rpn / 16;
                 const int nsplit = kCW / n_mg;
                 const bool active = cw < n_mg * nsplit;
                 const int mg = cw % n_mg, ns = cw / n_mg;
@@ -381,11 +402,11 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
                                 const double2* st = stages + (int64_t)stage * kStageElems;
                                 const double2* ti = st + kTElems + mg * 16 + g;
                                 if (kv == kKC) {
-                                    if (hm) stage_mma<true, true>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
-                                    else stage_mma<false, true>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
+                                    if (hm) stage_mma<true, true>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
+                                    else stage_mma<false, true>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
                                 } else {
-                                    if (hm) stage_mma<true, false>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
-                                    else stage_mma<false, false>(acc, st, ti, kv, ns, nsplit, ntiles, g, t);
+                                    if (hm) stage_mma<true, false>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
+                                    else stage_mma<false, false>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
                                 }
                             }
                             __syncwarp();

@@ -52,6 +52,10 @@ class _DeviceProgram:
         self.pieces = up(prog.pieces, torch.int64)
         self.mr_segs = up(prog.mr_segs, torch.int64)
         self.mr_ranges = up(prog.mr_ranges, torch.int32)
+        # TMA tensor maps over the arena, one pair per leading dimension (filled by the plan)
+        lds = prog.mr_lds if prog.mr_lds is not None else np.zeros(0, dtype=np.int64)
+        self.tmap_lds = np.ascontiguousarray(lds, dtype=np.int64)
+        self.tmaps = torch.zeros(max(1, 2 * len(lds)) * 128, dtype=torch.uint8, device=device)
 
     def struct(self) -> _lib.UhmvProgram:
         p = self.prog
@@ -78,6 +82,9 @@ class _DeviceProgram:
         s.stage_elems = int(p.stage_elems)
         s.mr_segs = self.mr_segs.data_ptr()
         s.mr_ranges = self.mr_ranges.data_ptr()
+        s.n_tmaps = len(self.tmap_lds)
+        s.tmap_lds = self.tmap_lds.ctypes.data if len(self.tmap_lds) else None
+        s.tmaps = self.tmaps.data_ptr()
         return s
 
 
@@ -100,11 +107,19 @@ class DeviceOperator:
         if share_with is not None:
             for name in ("arena", "work", "counters", "ticket", "exit_count", "x_scratch", "w_scratch"):
                 setattr(self, name, getattr(share_with, name))
+            lds = [int(q.mr_lds.max()) for q in (fwd_p, adj_p) if q.mr_lds is not None and len(q.mr_lds)]
+            if max(lds + [0]) > share_with._arena_pad:
+                raise ValueError("programs read the arena with a leading dimension beyond its padding")
+            self._arena_pad = share_with._arena_pad
             need = max(fwd_p.n_counters, adj_p.n_counters, 1)
             if self.counters.numel() < need:
                 self.counters = torch.zeros(need, dtype=torch.int32, device=dev)
         else:
-            self.arena = torch.from_numpy(packed.arena).to(dev)
+            # padded by the largest leading dimension: TMA rows of the last matrix may overhang
+            pad = max([int(q.mr_lds.max()) for q in (fwd_p, adj_p) if q.mr_lds is not None and len(q.mr_lds)] + [0])
+            self._arena_pad = pad
+            self.arena = torch.zeros(len(packed.arena) + pad + 16, dtype=torch.complex128, device=dev)
+            self.arena[: len(packed.arena)].copy_(torch.from_numpy(packed.arena))
             self.work = torch.zeros(packed.work_len, dtype=torch.complex128, device=dev)
             n_ctr = max(packed.fwd.n_counters, packed.adj.n_counters, 1)
             self.counters = torch.zeros(n_ctr, dtype=torch.int32, device=dev)
@@ -121,6 +136,7 @@ class DeviceOperator:
         d.n_rows = packed.n_rows
         d.n_cols = packed.n_cols
         d.arena = self.arena.data_ptr()
+        d.arena_len = len(packed.arena)
         d.work = self.work.data_ptr()
         d.work_len = packed.work_len
         d.counters = self.counters.data_ptr()

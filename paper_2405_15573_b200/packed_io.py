@@ -24,7 +24,7 @@ from .packer import PackedOperator, Program
 __all__ = ["save_packed", "load_packed", "FORMAT_VERSION"]
 
 FORMAT_VERSION = 1
-_ARRAYS = ("ops", "segs", "pieces", "runs", "waits", "sigs", "fused_order", "kinds", "mr_segs", "mr_ranges")
+_ARRAYS = ("ops", "segs", "pieces", "runs", "waits", "sigs", "fused_order", "kinds", "mr_segs", "mr_ranges", "mr_lds")
 _SCALARS = ("in_max", "xin_max", "out_max", "n_counters", "zero_output", "arena_elems", "stage_elems")
 
 
@@ -60,6 +60,7 @@ def _get(z, meta, name) -> Program:
         stage_elems=sc["stage_elems"],
         mr_segs=z[f"{name}_mr_segs"],
         mr_ranges=z[f"{name}_mr_ranges"],
+        mr_lds=z[f"{name}_mr_lds"],
     )
     if "part_b" in sc:
         prog.part_b = _get(z, meta, sc["part_b"])

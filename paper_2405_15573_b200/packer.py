@@ -59,6 +59,7 @@ RUN_FIELDS = 5  # int64: buf, off, len, dst, flags
 PIECE_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_off, out_off, info
 MR_FIELDS = 8  # int64: m_off, ld, rows, cols, mode, in_buf, in_abs (element index), out_off
 MR_FIRST = 1 << 8  # mode-field flag: first group writing its outputs (flush stores, no read-add)
+MR_TMAP_SHIFT = 16  # mode-field bits 16..: index into Program.mr_lds (TMA tensor map of that ld)
 MR_RANGE_FIELDS = 3  # int32 per op: mr_segs begin, end, flags
 MR_ZERO = 1  # op flag: some output position is written by no group -- zero the outputs first
 # piece info bits: [0,24) smem element offset in its stage, 24 stage_begin, 25 stage_end,
@@ -109,6 +110,7 @@ class Program:
     stage_elems: int = STAGE_ELEMS  # bulk kernel stage size the pieces were packed for
     mr_segs: np.ndarray | None = None  # (n, MR_FIELDS) int64: multi-RHS segments, one input source each
     mr_ranges: np.ndarray | None = None  # (n_ops, 3) int32: mr_segs range + MR_ZERO flag of every op
+    mr_lds: np.ndarray | None = None  # int64 leading dimensions the mr segments read (one TMA map each)
 
     @property
     def n_ops(self) -> int:
@@ -151,6 +153,7 @@ class PackedOperator:
         kw["split"] = dict(kw["split"], far_rows=far_rows)
         fwd, work_f, _ = _build_program(self.geo, adjoint=False, **kw)
         adj, work_a, _ = _build_program(self.geo, adjoint=True, **kw)
+        _assign_tmaps([fwd, adj])
         self.rechunked[key] = (fwd, adj, max(work_f, work_a, 1))
         return self.rechunked[key]
 
@@ -254,15 +257,19 @@ def pack(
     offs = {}
     cursor = 0
 
-    def alloc(key, n):
+    def alloc(key, n, ld):
+        # every matrix starts at a multiple of its leading dimension: the multi-RHS engine
+        # reads the arena as one 2-D TMA tensor per ld, (row, col) = divmod(offset, ld)
         nonlocal cursor
+        if ld > 1:
+            cursor = (cursor + ld - 1) // ld * ld
         offs[key] = cursor
         cursor += _align(max(n, 0))
 
     for t in sorted(bct.col_map):
-        alloc(("V", t), cnodes[t].size * rank_c[t])
+        alloc(("V", t), cnodes[t].size * rank_c[t], rank_c[t])
     for s in sorted(bct.row_map):
-        alloc(("U", s), rnodes[s].size * rank_r[s])
+        alloc(("U", s), rnodes[s].size * rank_r[s], rank_r[s])
     fcols = {}  # s -> ([(bid, t, pos, k)], kfac)
     for s in sorted(bct.row_map):
         pos, cols = 0, []
@@ -272,11 +279,11 @@ def pack(
                 cols.append((bid, t, pos, kb[bid]))
                 pos += kb[bid]
         fcols[s] = (cols, pos)
-        alloc(("F", s), rank_r[s] * pos)
+        alloc(("F", s), rank_r[s] * pos, pos)
         for t in bct.row_map[s]:
             bid = bct.block_of[(s, t)]
             if not factorized[bid]:
-                alloc(("S", bid), rank_r[s] * rank_c[t])
+                alloc(("S", bid), rank_r[s] * rank_c[t], rank_c[t])
     ycols = {}  # t -> ([(bid, s, pos, k)], K')
     for t in sorted(bct.col_map):
         pos, cols = 0, []
@@ -286,7 +293,7 @@ def pack(
                 cols.append((bid, s, pos, kb[bid]))
                 pos += kb[bid]
         ycols[t] = (cols, pos)
-        alloc(("Y", t), rank_c[t] * pos)
+        alloc(("Y", t), rank_c[t] * pos, pos)
     dense_by_rleaf, dense_by_cleaf = {}, {}
     for bid in dense_ids:
         b = bct.nodes[bid]
@@ -299,7 +306,7 @@ def pack(
     for r in sorted(dense_by_rleaf, key=lambda r: rnodes[r].lo):
         for bid in dense_by_rleaf[r]:
             rr, cc = bct.block_shape(bid)
-            alloc(("D", bid), rr * cc)
+            alloc(("D", bid), rr * cc, cc)
 
     arena = np.zeros(max(cursor, ALIGN), dtype=np.complex128)
 
@@ -357,6 +364,7 @@ def pack(
               split=split)
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
     adj, work_a, ex_a = _build_program(geo, adjoint=True, **kw)
+    _assign_tmaps([fwd, adj] + [q.part_b for q in (fwd, adj) if q.part_b is not None])
     elems_alg = bytes_bases + bytes_coupling + bytes_dense
     return PackedOperator(
         n_rows=n_rows,
@@ -850,6 +858,21 @@ def _resolve_inputs(segs, in_runs):
                 out.append((m_off + k0 * ld, ld, take, cols, mode, r[0], src, out_off))
             pos += take
     return out
+
+
+def _assign_tmaps(progs):
+    """Give every multi-RHS arena segment the index of its leading dimension in one sorted
+    list shared by ``progs`` (mode-field bits 16..; the device plan encodes one pair of TMA
+    tensor maps per distinct ld over the arena)."""
+    lds = sorted({int(q[1]) for p in progs for q in p.mr_segs if (q[4] & 0xFF) != MODE_S})
+    index = {ld: i for i, ld in enumerate(lds)}
+    for p in progs:
+        m = p.mr_segs.copy()
+        for q in m:
+            if (q[4] & 0xFF) != MODE_S:
+                q[4] = (q[4] & 0xFFFF) | (index[int(q[1])] << MR_TMAP_SHIFT)
+        p.mr_segs = m
+        p.mr_lds = np.asarray(lds, dtype=np.int64)
 
 
 def _mr_groups(mr, n_out):

@@ -35,6 +35,7 @@ from .packer import (
     STAGE_ELEMS,
     PackedOperator,
     _align,
+    _assign_tmaps,
     _chunks,
     _finish,
     _leaves_under,
@@ -61,15 +62,17 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
     kb = {b: int(h.admissible[b].rank) for b in adm}
     offs, cursor = {}, 0
 
-    def alloc(key, n):
+    def alloc(key, n, ld):  # start at a multiple of the leading dimension (packer.alloc)
         nonlocal cursor
+        if ld > 1:
+            cursor = (cursor + ld - 1) // ld * ld
         offs[key] = cursor
         cursor += _align(n)
 
     for b in adm:
         blk = bct.nodes[b]
-        alloc(("W", b), cnodes[blk.col].size * kb[b])
-        alloc(("U", b), rnodes[blk.row].size * kb[b])
+        alloc(("W", b), cnodes[blk.col].size * kb[b], kb[b])
+        alloc(("U", b), rnodes[blk.row].size * kb[b], kb[b])
     dense_by_rleaf, dense_by_cleaf = {}, {}
     for bid in h.dense:
         blk = bct.nodes[bid]
@@ -82,7 +85,7 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
     for r in sorted(dense_by_rleaf, key=lambda r: rnodes[r].lo):
         for bid in dense_by_rleaf[r]:
             rr, cc = bct.block_shape(bid)
-            alloc(("D", bid), rr * cc)
+            alloc(("D", bid), rr * cc, cc)
     arena = np.zeros(max(cursor, 8), dtype=np.complex128)
     elems = 0
     for b in adm:
@@ -100,6 +103,7 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
     kw = dict(rows_per_chunk=rows_per_chunk, stage_elems=stage_elems, near_interleave=near_interleave)
     fwd, work_f = _build_h(geo, adjoint=False, **kw)
     adj, work_a = _build_h(geo, adjoint=True, **kw)
+    _assign_tmaps([fwd, adj])
     # reference storage_report (hmatrix.py:187-208) counts k (m + n + 1); sigma is folded here
     return PackedOperator(
         n_rows=n_rows, n_cols=n_cols, dtype=np.dtype(h._dtype), arena=arena,

@@ -14,7 +14,7 @@ from paper_2405_15573_b200.packer import MR_ROWS, pack
 
 
 def _same_prog(a, b):
-    for f in ("ops", "segs", "pieces", "runs", "waits", "sigs", "fused_order", "kinds", "mr_segs", "mr_ranges"):
+    for f in ("ops", "segs", "pieces", "runs", "waits", "sigs", "fused_order", "kinds", "mr_segs", "mr_ranges", "mr_lds"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
     assert [tuple(x) for x in a.phases] == [tuple(x) for x in b.phases]
     for f in ("in_max", "xin_max", "out_max", "n_counters", "zero_output", "arena_elems", "stage_elems"):

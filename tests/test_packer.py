@@ -6,10 +6,12 @@ run.  Structure gate G6: packed block ranges and slabs eq
 reference objects bit for bit.
 """
 
+import os
+
 import numpy as np
 import pytest
 
-from conftest import rel, views
+from conftest import GOLDEN, load_golden, rel, views
 from packed_vm import vm_matvec
 from paper_2405_15573_b200.packer import (
     BUF_ARENA,
@@ -195,3 +197,28 @@ def test_vm_matmat_multi_rhs(golden):
         W = vm_matmat(p, V, adjoint=adjoint)
         ref = np.stack([oracle_matvec_uh(u, V[:, j], adjoint=adjoint) for j in range(5)], axis=1)
         assert rel(W, ref) <= TOL, (name, adjoint)
+
+
+@pytest.mark.parametrize("name", ["helm400", "degenerate", "rect_sphere", "two_cloud", "h_ico2_helm"])
+def test_mr_segments_fit_tma_rows(name):
+    """Multi-RHS arena segments never wrap a TMA row: with (row, col) = divmod(m_off, ld),
+    col + cols <= ld (matrices start at multiples of their ld), and every segment's map index
+    points at its own ld."""
+    from paper_2405_15573_b200.packer import MODE_S, MR_ROWS, MR_TMAP_SHIFT
+
+    if name.startswith("h_"):
+        from paper_2405_15573_b200.packer_h import pack_h
+        from paper_2405_15573_b200.uh_io import load_h
+
+        h, _ = load_h(os.path.join(GOLDEN, f"{name}.npz"))
+        progs = [pack_h(h).fwd, pack_h(h).adj]
+    else:
+        u, _ = load_golden(name)
+        p = pack(u)
+        progs = [p.fwd, p.adj] + list(p.programs(rows_per_chunk=MR_ROWS, far_rows=MR_ROWS)[:2])
+    for prog in progs:
+        for m_off, ld, rows, cols, mode, _b, _a, _o in prog.mr_segs.tolist():
+            if mode & 0xFF == MODE_S:
+                continue
+            assert m_off % ld + cols <= ld, (m_off, ld, cols)
+            assert prog.mr_lds[mode >> MR_TMAP_SHIFT] == ld
