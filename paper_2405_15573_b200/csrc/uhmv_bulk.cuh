@@ -616,7 +616,9 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         consumer_sync();  // all outputs issued; the slot is no longer read
         if (lane == 0) mbar_arrive(&opempty[q]);
         if (tid == 0 && !p.skip_waits && se > sb) {
-            __threadfence();
+            // red.release.gpu orders every output store of the CTA before the signal: the
+            // stores happen-before this thread's release through the bar.sync above
+            // (release cumulativity), so no separate fence is needed
             for (int i2 = sb; i2 < se; ++i2) red_release_add(p.counters + __ldg(p.sigs + i2), 1u);
         }
         if (++q == kOpSlots) {
