@@ -140,6 +140,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_relaxed_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Signal counters sigs[b..e) once every prior write of the CTA (ordered before the caller by
+// a bar.sync) is visible: ONE release fence, then relaxed adds (a release pattern each).
+__device__ __forceinline__ void signal_counters(uint32_t* counters, const int32_t* sigs, int b, int e) {
+    if (e - b == 1) {
+        red_release_add(counters + __ldg(sigs + b), 1u);
+        return;
+    }
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    for (int i = b; i < e; ++i) red_relaxed_add(counters + __ldg(sigs + i), 1u);
+}
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
 }
@@ -619,7 +632,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             // red.release.gpu orders every output store of the CTA before the signal: the
             // stores happen-before this thread's release through the bar.sync above
             // (release cumulativity), so no separate fence is needed
-            for (int i2 = sb; i2 < se; ++i2) red_release_add(p.counters + __ldg(p.sigs + i2), 1u);
+            signal_counters(p.counters, p.sigs, sb, se);
         }
         if (++q == kOpSlots) {
             q = 0;

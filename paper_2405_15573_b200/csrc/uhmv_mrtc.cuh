@@ -456,7 +456,7 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
         if (ctid == 0) {
             const int gb = __ldg(hp + 10), ge = __ldg(hp + 11);
             if (ge > gb)  // release cumulativity orders the CTA's flushes (bar.sync above)
-                for (int i = gb; i < ge; ++i) bulk::red_release_add(p.counters + __ldg(p.sigs + i), 1u);
+                bulk::signal_counters(p.counters, p.sigs, gb, ge);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&opempty[q]);
