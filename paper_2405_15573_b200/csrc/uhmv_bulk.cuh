@@ -86,7 +86,8 @@ struct Params {
 
 // prof layout per CTA (64 x u64): [kind * 8 + c] for op kinds 0..6 with c = 0 consumer waiting
 // for stage data, 1 dependency wait, 2 compute, 3 op prologue/epilogue, 4 pieces, 5 ops;
-// [56] producer waiting for a free stage, [57] producer waiting for a free op slot.
+// [56] producer waiting for a free stage, [57] producer waiting for a free op slot,
+// [58 + w] consumer warp w waiting for stage data (all kinds).
 
 struct Layout {
     int stage_off, xin_off, out_off, slot_off, bar_off, prof_off, total;
@@ -355,6 +356,8 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         if (op < 0) {
             if (prof)
                 for (int i = 0; i < 56; ++i) p.prof[(size_t)blockIdx.x * 64 + i] = sprof[i];
+            __syncwarp();
+            if (PROF && lane == 0) p.prof[(size_t)blockIdx.x * 64 + 58 + (tid >> 5)] = sprof[58 + (tid >> 5)];
             break;
         }
         const int n_out = S->hdr[1];
@@ -481,7 +484,9 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                         pr[kind * 8 + 2] += t1 - t0;
                         t0 = t1;
                     }
+                    long long tw = PROF ? clock64() : 0;
                     mbar_wait(&full[stage], sphase);
+                    if (PROF && lane == 0) sprof[58 + (tid >> 5)] += clock64() - tw;  // every warp
                     if (prof) {
                         const long long t1 = clock64();
                         pr[kind * 8 + 0] += t1 - t0;
@@ -503,20 +508,12 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     const double2* X = xv + g;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
                     double cr = 0.0, ci = 0.0, dr = 0.0, di = 0.0;
-                    // warp-uniform trip count (cols is uniform per piece); ragged tails are
-                    // predicated instead of diverging inside the row-group
-                    const int nk = (cols + kLanesPerRow - 1) / kLanesPerRow;
-                    for (int k = 0; k < nk; k += 4) {
-                        const int j = g + k * kLanesPerRow;
-                        const double2 z = make_double2(0.0, 0.0);
-                        const double2 t0 = (j < cols) ? T[0] : z;
-                        const double2 x0 = (j < cols) ? X[0] : z;
-                        const double2 t1 = (j + 8 < cols) ? T[8] : z;
-                        const double2 x1 = (j + 8 < cols) ? X[8] : z;
-                        const double2 t2 = (j + 16 < cols) ? T[16] : z;
-                        const double2 x2 = (j + 16 < cols) ? X[16] : z;
-                        const double2 t3 = (j + 24 < cols) ? T[24] : z;
-                        const double2 x3 = (j + 24 < cols) ? X[24] : z;
+                    // full 32-column blocks: every lane of the row group has four elements,
+                    // unpredicated (cols is warp-uniform per piece); then the ragged tail
+                    const int nfull = cols >> 5;
+                    for (int k = 0; k < nfull; ++k) {
+                        const double2 t0 = T[0], x0 = X[0], t1 = T[8], x1 = X[8];
+                        const double2 t2 = T[16], x2 = X[16], t3 = T[24], x3 = X[24];
                         cmac(ar, ai, t0, x0);
                         cmac(br, bi, t1, x1);
                         cmac(cr, ci, t2, x2);
@@ -524,6 +521,11 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                         T += 32;
                         X += 32;
                     }
+                    const int tail = cols & 31;
+                    if (g < tail) cmac(ar, ai, T[0], X[0]);
+                    if (g + 8 < tail) cmac(br, bi, T[8], X[8]);
+                    if (g + 16 < tail) cmac(cr, ci, T[16], X[16]);
+                    if (g + 24 < tail) cmac(dr, di, T[24], X[24]);
                     ar += br + (cr + dr);
                     ai += bi + (ci + di);
                     const int o = out_off + r;

@@ -189,7 +189,8 @@ class DeviceOperator:
         from .packer import KIND_NAMES
 
         tot = buf.sum(dim=0).tolist()
-        out = {"grid": grid, "p_wait_stage": tot[56], "p_wait_slot": tot[57], "kinds": {}}
+        out = {"grid": grid, "p_wait_stage": tot[56], "p_wait_slot": tot[57],
+               "warp_wait_data": tot[58:62], "kinds": {}}
         cats = ["wait_data", "wait_dep", "compute", "overhead", "pieces", "ops"]
         for k, name in enumerate(KIND_NAMES):
             row = tot[k * 8 : k * 8 + 6]
