@@ -122,12 +122,14 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t byte
         "r"(bytes)
         : "memory");
 }
+// Blocking wait: with a suspend-time hint the warp sleeps in hardware until the phase
+// completes instead of re-issuing try_wait (spinning warps stole issue slots from consumers).
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAIT_%=;\n\t}" ::"r"(su32(b)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680)
         : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
