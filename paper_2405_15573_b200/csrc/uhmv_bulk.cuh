@@ -172,6 +172,11 @@ __device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64
     return c;
 }
 
+// Lanes per output column of an H/S piece: columns go round-robin over 128/P thread groups
+// in up to kSlots passes; the P lanes of a column (32/P apart in a warp) split its rows and
+// are reduced by shuffles at the flush.  (P = 4 up to 128 columns measured slower.)
+__device__ __forceinline__ int h_lanes(int cols) { return cols <= 32 ? 4 : (cols <= 64 ? 2 : 1); }
+
 template <bool PROF>
 __device__ __forceinline__ void producer(const Params& p, unsigned char* stages, uint64_t* full,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
@@ -433,16 +438,17 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     }
                 }
             } else if (g_mode >= 0) {
-                const int P = g_cols <= 32 ? 4 : (g_cols <= 64 ? 2 : 1);
+                const int P = h_lanes(g_cols);
                 const int nJ = kConsumers / P;
-                const int pp = tid % P;
-                int j0 = (tid / P - (g_out % nJ)) % nJ;
+                const int cw = 32 / P;  // columns per warp: lane = column + cw * row offset
+                const int pp = lane / cw;
+                int j0 = ((tid >> 5) * cw + lane % cw - (g_out % nJ)) % nJ;
                 if (j0 < 0) j0 += nJ;
 #pragma unroll
                 for (int k = 0; k < kSlots; ++k) {
                     if (k * nJ >= g_cols) break;
                     double ar = accr[k], ai = acci[k];
-                    for (int o = 1; o < P; o <<= 1) {
+                    for (int o = cw; o < 32; o <<= 1) {
                         ar += __shfl_xor_sync(0xffffffffu, ar, o);
                         ai += __shfl_xor_sync(0xffffffffu, ai, o);
                     }
@@ -559,10 +565,13 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     }
                 }
             } else {
-                const int P = cols <= 32 ? 4 : (cols <= 64 ? 2 : 1);
+                const int P = h_lanes(cols);
                 const int nJ = kConsumers / P;
-                const int pp = tid % P;
-                int j0 = (tid / P - (out_off % nJ)) % nJ;
+                // a quarter-warp reads 8 consecutive columns of one row (conflict-free 16-B
+                // loads); the P lanes of a column sit cw apart in the warp
+                const int cw = 32 / P;
+                const int pp = lane / cw;
+                int j0 = ((tid >> 5) * cw + lane % cw - (out_off % nJ)) % nJ;
                 if (j0 < 0) j0 += nJ;
                 int64_t dm = 0, dld = 0;
                 if (direct) {
