@@ -35,6 +35,8 @@ constexpr int kThreads = kConsumers + 32;        // + one producer warp
 constexpr int kOpSlots = 2;
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
+static_assert((kRowGroups & (kRowGroups - 1)) == 0 && (kConsumers & (kConsumers - 1)) == 0,
+              "row groups / column groups are addressed with power-of-2 masks");
 constexpr int kPieceFields = 8;
 constexpr int kSlots = 4;         // register accumulator slots per thread
 constexpr int kSlotRuns = 48;     // run descriptors cached per op slot
@@ -442,8 +444,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 const int nJ = kConsumers / P;
                 const int cw = 32 / P;  // columns per warp: lane = column + cw * row offset
                 const int pp = lane / cw;
-                int j0 = ((tid >> 5) * cw + lane % cw - (g_out % nJ)) % nJ;
-                if (j0 < 0) j0 += nJ;
+                const int j0 = ((tid >> 5) * cw + (lane & (cw - 1)) - g_out) & (nJ - 1);  // powers of 2
 #pragma unroll
                 for (int k = 0; k < kSlots; ++k) {
                     if (k * nJ >= g_cols) break;
@@ -509,8 +510,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 // diagnostics: no compute
             } else if (mode == kModeN) {
                 const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
-                int r0 = (rg - (out_off % kRowGroups)) % kRowGroups;
-                if (r0 < 0) r0 += kRowGroups;
+                const int r0 = (rg - out_off) & (kRowGroups - 1);  // first row of this row group
                 for (int r = r0; r < rows; r += kRowGroups) {
                     const double2* T = tile + r * cols + g;
                     const double2* X = xv + g;
@@ -538,7 +538,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     ai += bi + (ci + di);
                     const int o = out_off + r;
                     if (nreg) {
-                        const int k = o / kRowGroups;
+                        const int k = (unsigned)o / kRowGroups;
                         if (k == 0) {
                             accr[0] += ar;
                             acci[0] += ai;
@@ -571,8 +571,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 // loads); the P lanes of a column sit cw apart in the warp
                 const int cw = 32 / P;
                 const int pp = lane / cw;
-                int j0 = ((tid >> 5) * cw + lane % cw - (out_off % nJ)) % nJ;
-                if (j0 < 0) j0 += nJ;
+                const int j0 = ((tid >> 5) * cw + (lane & (cw - 1)) - out_off) & (nJ - 1);
                 int64_t dm = 0, dld = 0;
                 if (direct) {
                     const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
