@@ -13,6 +13,10 @@
 //     dimension over the whole arena, cp.async.bulk.tensor) and the IN block (KC rows x 64
 //     RHS, contiguous) as one cp.async.bulk -- into a 6-deep shared-memory ring completing on
 //     mbarriers: 2-6 copy instructions per 16 KFLOP/lane stage;
+//   * for every group pass the producer also publishes a PASS descriptor in a shared-memory
+//     ring (what to do, how many stages, the destination of every output row, atomic flags),
+//     so the consumers never read the op tables, never search output runs and never meet at
+//     a barrier inside an op; op boundaries travel through the same ring;
 //   * the consumer warps own a fixed (16-RHS, n-tile) share of the output block, accumulate
 //     the whole segment group in registers (up to 2 x 5 DMMA tiles per warp) and flush it once
 //     (fp64 atomics into w -- at most two addends per entry, so order-independent -- a store
@@ -46,9 +50,23 @@ constexpr int kLdTH = kNP;              // H slab [16][80]   (one TMA box of 16 
 constexpr int kTElems = (kNP * kLdTN > kKC * kLdTH) ? kNP * kLdTN : kKC * kLdTH;
 constexpr int kIElems = kKC * kRP;      // IN block [16][rpn] (one bulk copy when rpn == R)
 constexpr int kStageElems = kTElems + kIElems;  // complex
-constexpr int kOpSlots = 2;
+constexpr int kPassSlots = 4;           // pass-descriptor ring depth
 constexpr int kSmemStages = kNST * kStageElems * 16;
-constexpr int kSmemBytes = kSmemStages + kNP * 8 + kNP * 4 + (2 * kNST + 2 * kOpSlots) * 8 + 32 + 48 * 8;
+
+// One unit of consumer work, published by the producer (see the header comment).
+enum PassType : int32_t { kPassExit = 0, kPassGemm = 1, kPassSum = 2, kPassEndOp = 3, kPassZero = 4 };
+struct __align__(16) Pass {
+    int32_t type, op, kind, hm;
+    int32_t first;  // flush stores (first group on these outputs) instead of read-add-write
+    int32_t sync;   // meet at a consumer barrier before the flush (outputs of an earlier group)
+    int32_t rp, rpn, np, nst;  // RHS pass, outputs of the pass, ring stages it consumes
+    int32_t s_rows, s_j0;      // kPassSum: partial vectors and first column
+    int64_t s_moff, s_ld;      // kPassSum: partial block (work element offset, row stride)
+    uint32_t atom[(kNP + 31) / 32];  // bit n: output n is in w (fp64 atomics)
+    double2* out[kNP];         // destination of output n, RHS 0 (row stride nrhs)
+};
+constexpr int kSmemBytes = kSmemStages + kPassSlots * (int)sizeof(Pass) + kNST * 4 +
+                           (2 * kNST + 2 * kPassSlots) * 8 + 32 + 48 * 8;
 
 using mrhs::Params;
 using bulk::mbar_arrive;
@@ -118,16 +136,49 @@ __device__ __forceinline__ int group_end(const Params& p, int s, int se, const S
 
 // Diagnostics (PROF): per-CTA cycle counters, summed by DeviceOperator.profile_mr --
 //   [0] producer waiting for a free stage   [1] producer waiting on dependencies
-//   [2] producer issuing copies            [3] producer ticket + op slot
-//   [8 + 4*kind + {0 wait data, 1 mma, 2 table + flush, 3 S reduction}]  consumer warp 0
-//   [40] consumer warp 0 waiting for the next op
+//   [2] producer issuing (stages + pass descriptors)   [3] producer ticket
+//   [8 + 4*kind + {0 wait data, 1 mma, 2 flush, 3 S reduction}]  consumer warp 0
+//   [40] consumer warp 0 waiting for a pass descriptor
+
+// Producer side of the pass ring: claim slot, fill it (all lanes), publish.
+struct PassRing {
+    Pass* slots;
+    uint64_t* full;
+    uint64_t* empty;
+    int q;
+    uint32_t phase;
+    __device__ __forceinline__ Pass* claim() {
+        mbar_wait(&empty[q], phase ^ 1u);
+        return slots + q;
+    }
+    __device__ __forceinline__ void publish(int lane) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[q]);  // release: the lanes' slot writes precede it
+        if (++q == kPassSlots) {
+            q = 0;
+            phase ^= 1u;
+        }
+    }
+};
+
+// destination table of outputs [o0, o0 + np) of an op (binary search over its out runs)
+__device__ __forceinline__ void fill_outputs(const Params& p, Pass* ps, int out_b, int out_e, int o0, int np,
+                                             int lane) {
+    for (int w = lane; w < (kNP + 31) / 32; w += 32) ps->atom[w] = 0u;
+    __syncwarp();
+    for (int n = lane; n < np; n += 32) {
+        bool at;
+        ps->out[n] = mrhs::out_ptr(p, out_b, out_e, o0 + n, &at);
+        if (at) atomicOr(&ps->atom[n >> 5], 1u << (n & 31));
+    }
+}
+
 template <bool PROF>
-__device__ void producer(const Params& p, double2* stages, uint64_t* full, uint64_t* empty,
-                         uint64_t* opfull, uint64_t* opempty, int* s_opq, unsigned long long* pr) {
+__device__ void producer(const Params& p, double2* stages, int* s_kv, uint64_t* full, uint64_t* empty,
+                         PassRing ring, unsigned long long* pr) {
     const int lane = threadIdx.x & 31;
     const int R = p.nrhs;
-    uint32_t stage = 0, sphase = 0, qphase = 0;
-    int q = 0;
+    uint32_t stage = 0, sphase = 0;
     for (;;) {
         long long t0 = PROF ? clock64() : 0;
         int op = -1;
@@ -136,14 +187,19 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
             op = (tk < (unsigned long long)p.op_count) ? __ldg(p.fused_order + tk) : -1;
         }
         op = __shfl_sync(0xffffffffu, op, 0);
-        mbar_wait(&opempty[q], qphase ^ 1u);
         if (PROF && lane == 0) {
             const long long t1 = clock64();
             pr[3] += t1 - t0;
             t0 = t1;
         }
-        if (op >= 0) {
-            const int32_t* hp = p.ops + (int64_t)op * kOpFields;
+        if (op < 0) {
+            Pass* ps = ring.claim();
+            if (lane == 0) ps->type = kPassExit;
+            ring.publish(lane);
+            break;
+        }
+        const int32_t* hp = p.ops + (int64_t)op * kOpFields;
+        {
             const int wb = __ldg(hp + 8), we = __ldg(hp + 9);
             for (int i = wb + lane; i < we; i += 32) {
                 const int c = __ldg(p.waits + 2 * i);
@@ -151,7 +207,8 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
                 while (ld_acquire(p.counters + c) < need) __nanosleep(32);
             }
             __syncwarp();
-            // work inputs written by other CTAs (generic proxy) are read below by the TMA engine
+            // work inputs written by other CTAs (generic proxy) are read below by the TMA
+            // engine; the consumers' work reads (S passes) are ordered by the pass ring
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
         if (PROF && lane == 0) {
@@ -159,26 +216,72 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
             pr[1] += t1 - t0;
             t0 = t1;
         }
-        if (lane == 0) {
-            s_opq[q] = op;
-            mbar_arrive(&opfull[q]);
+        const int out_b = __ldg(hp + 6), out_e = __ldg(hp + 7);
+        const int kind = __ldg(hp + 12);
+        if (__ldg(p.mr_ranges + 3 * op + 2) & 1) {  // packer.MR_ZERO (no such op at configs 1-4)
+            Pass* ps = ring.claim();
+            if (lane == 0) {
+                ps->type = kPassZero;
+                ps->op = op;
+                ps->kind = kind;
+            }
+            ring.publish(lane);
         }
-        if (op < 0) break;
         const int sb = __ldg(p.mr_ranges + 3 * op), se = __ldg(p.mr_ranges + 3 * op + 1);
         int s = sb;
+        bool prior = false;  // an earlier group of this op was flushed
         while (s < se) {
             const SegD s0 = seg_at(p, s);
             const int e = group_end(p, s, se, s0);
+            const int nout = seg_nout(s0);
+            const bool need_sync = prior && !s0.first;  // adds onto an earlier group's outputs
+            prior = true;
             if (s0.mode == kModeS) {
+                for (int n0 = 0; n0 < nout; n0 += kNP) {
+                    for (int si = s; si < e; ++si) {
+                        const SegD sg = seg_at(p, si);
+                        Pass* ps = ring.claim();
+                        if (lane == 0) {
+                            ps->type = kPassSum;
+                            ps->op = op;
+                            ps->kind = kind;
+                            ps->first = s0.first && si == s;
+                            ps->sync = need_sync && si == s && n0 == 0;
+                            ps->np = min(kNP, nout - n0);
+                            ps->s_rows = sg.rows;
+                            ps->s_j0 = n0;
+                            ps->s_moff = sg.m_off;
+                            ps->s_ld = sg.ld;
+                        }
+                        fill_outputs(p, ps, out_b, out_e, s0.out_off + n0, min(kNP, nout - n0), lane);
+                        ring.publish(lane);
+                    }
+                }
                 s = e;
                 continue;
             }
             const bool hm = s0.mode == kModeH;
-            const int nout = seg_nout(s0);
+            int nst = 0;  // stages of one pass: every K-chunk of every segment of the group
+            for (int si = s; si < e; ++si) nst += (seg_k(seg_at(p, si)) + kKC - 1) / kKC;
             for (int rp = 0; rp < R; rp += kRP) {
                 const int rpn = min(kRP, R - rp);
                 for (int n0 = 0; n0 < nout; n0 += kNP) {
                     const int np = min(kNP, nout - n0);
+                    Pass* ps = ring.claim();
+                    if (lane == 0) {
+                        ps->type = kPassGemm;
+                        ps->op = op;
+                        ps->kind = kind;
+                        ps->hm = hm;
+                        ps->first = s0.first;
+                        ps->sync = need_sync && rp == 0 && n0 == 0;
+                        ps->rp = rp;
+                        ps->rpn = rpn;
+                        ps->np = np;
+                        ps->nst = nst;
+                    }
+                    fill_outputs(p, ps, out_b, out_e, s0.out_off + n0, np, lane);
+                    ring.publish(lane);
                     for (int si = s; si < e; ++si) {
                         const SegD sg = seg_at(p, si);
                         const int K = seg_k(sg);
@@ -197,7 +300,10 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
                             // TMA boxes land whole (zero-filled past the row end); rows past kv
                             // are masked by the consumers
                             const uint32_t bytes = (uint32_t)(nbox * kKC * (hm ? kNP : kKC) + kv * rpn) * 16u;
-                            if (lane == 0) mbar_arrive_expect_tx(&full[stage], bytes);
+                            if (lane == 0) {
+                                s_kv[stage] = kv;  // published by the arrive (release)
+                                mbar_arrive_expect_tx(&full[stage], bytes);
+                            }
                             __syncwarp();
                             if (!hm) {  // T rows n0 + 16b.., columns k0..k0+16
                                 if (lane < nbox)
@@ -221,11 +327,14 @@ __device__ void producer(const Params& p, double2* stages, uint64_t* full, uint6
             }
             s = e;
         }
-        if (PROF && lane == 0) pr[2] += clock64() - t0;
-        if (++q == kOpSlots) {
-            q = 0;
-            qphase ^= 1u;
+        Pass* ps = ring.claim();
+        if (lane == 0) {
+            ps->type = kPassEndOp;
+            ps->op = op;
+            ps->kind = kind;
         }
+        ring.publish(lane);
+        if (PROF && lane == 0) pr[2] += clock64() - t0;
     }
 }
 
@@ -285,9 +394,8 @@ __device__ __forceinline__ void stage_mma(double (&acc)[2][kMaxNT][4], const dou
 }
 
 template <bool PROF>
-__device__ void consumer(const Params& p, double2* stages, double2** s_out, uint32_t* s_at,
-                         uint64_t* full, uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
-                         const int* s_opq, unsigned long long* pr) {
+__device__ void consumer(const Params& p, double2* stages, const int* s_kv, uint64_t* full, uint64_t* empty,
+                         Pass* slots, uint64_t* pfull, uint64_t* pempty, unsigned long long* pr) {
     const int ctid = threadIdx.x;  // 0 .. kCT-1
     const int lane = ctid & 31, cw = ctid >> 5;
     const int g = lane >> 2, t = lane & 3;
@@ -297,170 +405,148 @@ __device__ void consumer(const Params& p, double2* stages, double2** s_out, uint
     const bool rec = PROF && ctid == 0;
     for (;;) {
         long long t0 = PROF ? clock64() : 0;
-        mbar_wait(&opfull[q], qphase);
-        const int op = s_opq[q];
+        mbar_wait(&pfull[q], qphase);
+        const Pass* ps = slots + q;
+        const int type = ps->type;
         if (rec) pr[40] += clock64() - t0;
-        if (op < 0) break;
-        const int32_t* hp = p.ops + (int64_t)op * kOpFields;
-        unsigned long long* pk = pr + 8 + 4 * (PROF ? __ldg(hp + 12) : 0);
-        const int out_b = __ldg(hp + 6), out_e = __ldg(hp + 7);
-        // work outputs no group writes are zeroed (packer.MR_ZERO; none at configs 1-4); the
-        // first group on an output range stores, later ones add; w is zeroed by the launcher
-        if (__ldg(p.mr_ranges + 3 * op + 2) & 1) for (int r = out_b; r < out_e; ++r) {
-            const int64_t* rd = p.runs + (int64_t)r * kRunFields;
-            if (__ldg(rd + 4) & 2) continue;
-            double2* dp = p.work + __ldg(rd + 1) * (int64_t)R;
-            const int64_t n = (int64_t)__ldg(rd + 2) * R;
-            for (int64_t i = ctid; i < n; i += kCT) __stcg(dp + i, make_double2(0.0, 0.0));
-        }
-        const int sb = __ldg(p.mr_ranges + 3 * op), se = __ldg(p.mr_ranges + 3 * op + 1);
-        int s = sb;
-        while (s < se) {
-            const SegD s0 = seg_at(p, s);
-            const int e = group_end(p, s, se, s0);
-            const int nout = seg_nout(s0);
-            if (s0.mode == kModeS) {
-                // partial-vector reduction: out[j][r] = sum_k W[k][j][r] (work, L2 reads)
+        if (type == kPassExit) break;
+        unsigned long long* pk = pr + 8 + 4 * (PROF ? ps->kind : 0);
+        if (type == kPassEndOp) {
+            cons_sync();  // every flush of the op issued
+            if (ctid == 0) {
+                const int32_t* hp = p.ops + (int64_t)ps->op * kOpFields;
+                const int gb = __ldg(hp + 10), ge = __ldg(hp + 11);
+                if (ge > gb)  // release cumulativity orders the CTA's flushes (bar.sync above)
+                    bulk::signal_counters(p.counters, p.sigs, gb, ge);
+            }
+        } else if (type == kPassZero) {
+            const int32_t* hp = p.ops + (int64_t)ps->op * kOpFields;
+            for (int r = __ldg(hp + 6); r < __ldg(hp + 7); ++r) {
+                const int64_t* rd = p.runs + (int64_t)r * kRunFields;
+                if (__ldg(rd + 4) & 2) continue;
+                double2* dp = p.work + __ldg(rd + 1) * (int64_t)R;
+                const int64_t n = (int64_t)__ldg(rd + 2) * R;
+                for (int64_t i = ctid; i < n; i += kCT) __stcg(dp + i, make_double2(0.0, 0.0));
+            }
+            cons_sync();
+        } else if (type == kPassSum) {
+            // partial-vector reduction: out[j][r] = sum_k W[k][j0 + j][r] (work, L2 reads)
+            if (PROF) t0 = clock64();
+            if (ps->sync) cons_sync();
+            const int np = ps->np, rows = ps->s_rows;
+            const int64_t stride = ps->s_ld * (int64_t)R;
+            const double2* base = p.work + (ps->s_moff + ps->s_j0) * (int64_t)R;
+            const int64_t tot = (int64_t)np * R;
+            for (int64_t qq = ctid; qq < tot; qq += kCT) {
+                const int j = (int)(qq / R), r = (int)(qq % R);
+                const double2* src = base + (int64_t)j * R + r;
+                double2 acc = make_double2(0.0, 0.0);
+                int k = 0;
+                for (; k + 8 <= rows; k += 8) {  // eight loads in flight, summed in order
+                    double2 v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) v[u] = __ldcg(src + (k + u) * stride);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        acc.x += v[u].x;
+                        acc.y += v[u].y;
+                    }
+                }
+                for (; k < rows; ++k) {
+                    const double2 v = __ldcg(src + k * stride);
+                    acc.x += v.x;
+                    acc.y += v.y;
+                }
+                double2* dp = ps->out[j] + r;
+                if ((ps->atom[j >> 5] >> (j & 31)) & 1u) {
+                    atomicAdd(&dp->x, acc.x);
+                    atomicAdd(&dp->y, acc.y);
+                } else if (ps->first) {
+                    __stcg(dp, acc);
+                } else {
+                    const double2 o = __ldcg(dp);
+                    __stcg(dp, make_double2(o.x + acc.x, o.y + acc.y));
+                }
+            }
+            if (rec) pk[3] += clock64() - t0;
+        } else {  // kPassGemm
+            const bool hm = ps->hm != 0;
+            const int rpn = ps->rpn, rp = ps->rp, np = ps->np, nst = ps->nst;
+            const int n_mg = rpn / 16;
+            const int nsplit = kCW / n_mg;
+            const bool active = cw < n_mg * nsplit;
+            const int mg = cw % n_mg, ns = cw / n_mg;
+            const int ntiles = (np + 7) >> 3;
+            double acc[2][kMaxNT][4];
+#pragma unroll
+            for (int a = 0; a < 2; ++a)
+#pragma unroll
+                for (int b = 0; b < kMaxNT; ++b)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
+            for (int c = 0; c < nst; ++c) {
                 if (PROF) t0 = clock64();
-                cons_sync();
-                const int64_t tot = (int64_t)nout * R;
-                for (int64_t qq = ctid; qq < tot; qq += kCT) {
-                    const int j = (int)(qq / R), r = (int)(qq % R);
-                    double2 acc = make_double2(0.0, 0.0);
-                    for (int si = s; si < e; ++si) {
-                        const SegD sg = seg_at(p, si);
-                        const double2* src = p.work + (sg.m_off + j) * (int64_t)R + r;
-                        const int64_t stride = sg.ld * (int64_t)R;
-                        int k = 0;
-                        for (; k + 4 <= sg.rows; k += 4) {  // four loads in flight, summed in order
-                            double2 v[4];
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) v[u] = __ldcg(src + (k + u) * stride);
-#pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                acc.x += v[u].x;
-                                acc.y += v[u].y;
-                            }
-                        }
-                        for (; k < sg.rows; ++k) {
-                            const double2 v = __ldcg(src + k * stride);
-                            acc.x += v.x;
-                            acc.y += v.y;
-                        }
-                    }
-                    bool at;
-                    double2* dp = mrhs::out_ptr(p, out_b, out_e, s0.out_off + j, &at) + r;
-                    if (s0.first) {
-                        __stcg(dp, acc);
+                mbar_wait(&full[stage], sphase);
+                const int kv = s_kv[stage];
+                if (rec) {
+                    const long long t1 = clock64();
+                    pk[0] += t1 - t0;
+                    t0 = t1;
+                }
+                if (active) {
+                    const double2* st = stages + (int64_t)stage * kStageElems;
+                    const double2* ti = st + kTElems + mg * 16 + g;
+                    if (kv == kKC) {
+                        if (hm) stage_mma<true, true>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
+                        else stage_mma<false, true>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
                     } else {
-                        const double2 o = __ldcg(dp);
-                        __stcg(dp, make_double2(o.x + acc.x, o.y + acc.y));
+                        if (hm) stage_mma<true, false>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
+                        else stage_mma<false, false>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
                     }
                 }
-                if (rec) pk[3] += clock64() - t0;
-                s = e;
-                continue;
+                __syncwarp();
+                if (rec) pk[1] += clock64() - t0;
+                if (lane == 0) mbar_arrive(&empty[stage]);
+                if (++stage == kNST) {
+                    stage = 0;
+                    sphase ^= 1u;
+                }
             }
-            const bool hm = s0.mode == kModeH;
-            for (int rp = 0; rp < R; rp += kRP) {
-                const int rpn = min(kRP, R - rp);
-                const int n_mg = rpn / 16;
-                const int nsplit = kCW / n_mg;
-                const bool active = cw < n_mg * nsplit;
-                const int mg = cw % n_mg, ns = cw / n_mg;
-                for (int n0 = 0; n0 < nout; n0 += kNP) {
-                    const int np = min(kNP, nout - n0);
-                    const int ntiles = (np + 7) >> 3;
-                    if (PROF) t0 = clock64();
-                    cons_sync();  // previous flush done with the table; work outputs zeroed
-                    for (int i = ctid; i < np; i += kCT) {
-                        bool at;
-                        s_out[i] = mrhs::out_ptr(p, out_b, out_e, s0.out_off + n0 + i, &at);
-                        s_at[i] = at ? 1u : 0u;
-                    }
-                    cons_sync();
-                    if (rec) pk[2] += clock64() - t0;
-                    double acc[2][kMaxNT][4];
+            if (PROF) t0 = clock64();
+            if (ps->sync) cons_sync();  // an earlier group's flush of these outputs is complete
+            if (active) {  // flush: lane holds out[2t+e][g] for its tiles (re d=0, im d=1)
 #pragma unroll
-                    for (int a = 0; a < 2; ++a)
+                for (int j = 0; j < kMaxNT; ++j) {
+                    const int nt = ns + j * nsplit;
+                    if (nt >= ntiles) break;
 #pragma unroll
-                        for (int b = 0; b < kMaxNT; ++b)
+                    for (int ee = 0; ee < 2; ++ee) {
+                        const int n = nt * 8 + 2 * t + ee;
+                        if (n >= np) continue;
+                        double2* base = ps->out[n] + rp + mg * 16 + g;
+                        const bool at = (ps->atom[n >> 5] >> (n & 31)) & 1u;
 #pragma unroll
-                            for (int v = 0; v < 4; ++v) acc[a][b][v] = 0.0;
-                    for (int si = s; si < e; ++si) {
-                        const int K = seg_k(seg_at(p, si));
-                        for (int k0 = 0; k0 < K; k0 += kKC) {
-                            const int kv = min(kKC, K - k0);
-                            if (PROF) t0 = clock64();
-                            mbar_wait(&full[stage], sphase);
-                            if (rec) {
-                                const long long t1 = clock64();
-                                pk[0] += t1 - t0;
-                                t0 = t1;
-                            }
-                            if (active) {
-                                const double2* st = stages + (int64_t)stage * kStageElems;
-                                const double2* ti = st + kTElems + mg * 16 + g;
-                                if (kv == kKC) {
-                                    if (hm) stage_mma<true, true>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
-                                    else stage_mma<false, true>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
-                                } else {
-                                    if (hm) stage_mma<true, false>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
-                                    else stage_mma<false, false>(acc, st, ti, rpn, kv, ns, nsplit, ntiles, g, t);
-                                }
-                            }
-                            __syncwarp();
-                            if (rec) pk[1] += clock64() - t0;
-                            if (lane == 0) mbar_arrive(&empty[stage]);
-                            if (++stage == kNST) {
-                                stage = 0;
-                                sphase ^= 1u;
+                        for (int mt = 0; mt < 2; ++mt) {
+                            double2* dp = base + mt * 8;
+                            const double re = acc[mt][j][ee], im = acc[mt][j][2 + ee];
+                            if (at) {
+                                atomicAdd(&dp->x, re);
+                                atomicAdd(&dp->y, im);
+                            } else if (ps->first) {
+                                __stcg(dp, make_double2(re, im));
+                            } else {
+                                const double2 o = __ldcg(dp);
+                                __stcg(dp, make_double2(o.x + re, o.y + im));
                             }
                         }
                     }
-                    if (PROF) t0 = clock64();
-                    if (active) {  // flush: lane holds out[2t+e][g] for its tiles (re d=0, im d=1)
-#pragma unroll
-                        for (int j = 0; j < kMaxNT; ++j) {
-                            const int nt = ns + j * nsplit;
-                            if (nt >= ntiles) break;
-#pragma unroll
-                            for (int ee = 0; ee < 2; ++ee) {
-                                const int n = nt * 8 + 2 * t + ee;
-                                if (n >= np) continue;
-                                double2* base = s_out[n] + rp + mg * 16 + g;
-                                const bool at = s_at[n] != 0u;
-#pragma unroll
-                                for (int mt = 0; mt < 2; ++mt) {
-                                    double2* dp = base + mt * 8;
-                                    const double re = acc[mt][j][ee], im = acc[mt][j][2 + ee];
-                                    if (at) {
-                                        atomicAdd(&dp->x, re);
-                                        atomicAdd(&dp->y, im);
-                                    } else if (s0.first) {
-                                        __stcg(dp, make_double2(re, im));
-                                    } else {
-                                        const double2 o = __ldcg(dp);
-                                        __stcg(dp, make_double2(o.x + re, o.y + im));
-                                    }
-                                }
-                            }
-                        }
-                    }
-                    if (rec) pk[2] += clock64() - t0;
                 }
             }
-            s = e;
-        }
-        cons_sync();  // every flush of the op issued
-        if (ctid == 0) {
-            const int gb = __ldg(hp + 10), ge = __ldg(hp + 11);
-            if (ge > gb)  // release cumulativity orders the CTA's flushes (bar.sync above)
-                bulk::signal_counters(p.counters, p.sigs, gb, ge);
+            if (rec) pk[2] += clock64() - t0;
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&opempty[q]);
-        if (++q == kOpSlots) {
+        if (lane == 0) mbar_arrive(&pempty[q]);  // this warp is done with the descriptor
+        if (++q == kPassSlots) {
             q = 0;
             qphase ^= 1u;
         }
@@ -471,14 +557,13 @@ template <bool PROF>
 __global__ void __launch_bounds__(kThreads, 1) uhmv_mrtc_kernel(const Params p) {
     extern __shared__ __align__(128) unsigned char smem[];
     double2* stages = reinterpret_cast<double2*>(smem);
-    double2** s_out = reinterpret_cast<double2**>(smem + kSmemStages);
-    uint32_t* s_at = reinterpret_cast<uint32_t*>(s_out + kNP);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kSmemStages + kNP * 8 + kNP * 4);
+    Pass* slots = reinterpret_cast<Pass*>(smem + kSmemStages);
+    int* s_kv = reinterpret_cast<int*>(slots + kPassSlots);
+    uint64_t* full = reinterpret_cast<uint64_t*>(s_kv + ((kNST + 1) & ~1));
     uint64_t* empty = full + kNST;
-    uint64_t* opfull = empty + kNST;
-    uint64_t* opempty = opfull + kOpSlots;
-    int* s_opq = reinterpret_cast<int*>(opempty + kOpSlots);
-    int* flag = s_opq + kOpSlots;
+    uint64_t* pfull = empty + kNST;
+    uint64_t* pempty = pfull + kPassSlots;
+    int* flag = reinterpret_cast<int*>(pempty + kPassSlots);
     unsigned long long* sprof = reinterpret_cast<unsigned long long*>(flag + 2);  // 8-aligned
     if (PROF && threadIdx.x < 48) sprof[threadIdx.x] = 0ull;
     if (threadIdx.x == 0) {
@@ -486,17 +571,18 @@ __global__ void __launch_bounds__(kThreads, 1) uhmv_mrtc_kernel(const Params p) 
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kCW);
         }
-        for (int s = 0; s < kOpSlots; ++s) {
-            mbar_init(&opfull[s], 1);
-            mbar_init(&opempty[s], kCW);
+        for (int s = 0; s < kPassSlots; ++s) {
+            mbar_init(&pfull[s], 1);
+            mbar_init(&pempty[s], kCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if ((threadIdx.x >> 5) == kCW) {
-        producer<PROF>(p, stages, full, empty, opfull, opempty, s_opq, sprof);
+        PassRing ring{slots, pfull, pempty, 0, 0u};
+        producer<PROF>(p, stages, s_kv, full, empty, ring, sprof);
     } else {
-        consumer<PROF>(p, stages, s_out, s_at, full, empty, opfull, opempty, s_opq, sprof);
+        consumer<PROF>(p, stages, s_kv, full, empty, slots, pfull, pempty, sprof);
     }
     __syncthreads();
     if (PROF && threadIdx.x < 48) p.prof[(int64_t)blockIdx.x * 64 + threadIdx.x] = sprof[threadIdx.x];
