@@ -134,6 +134,25 @@ __device__ __forceinline__ int group_end(const Params& p, int s, int se, const S
     return e;
 }
 
+// End of the run of N segments starting at si that are consecutive column ranges of ONE
+// arena matrix (the packer cuts F_s / Y_t at the boundaries of their input runs); the
+// producer streams such a run as one K range so 16-wide chunks are not padded per piece.
+// *K receives the run's total width.
+__device__ __forceinline__ int merged_end(const Params& p, int si, int e, int* K) {
+    const SegD a = seg_at(p, si);
+    int k = seg_k(a), sj = si + 1;
+    if (a.mode == kModeN) {
+        while (sj < e) {
+            const SegD b = seg_at(p, sj);
+            if (b.ld != a.ld || b.rows != a.rows || b.m_off != a.m_off + k) break;
+            k += b.cols;
+            ++sj;
+        }
+    }
+    *K = k;
+    return sj;
+}
+
 // Diagnostics (PROF): per-CTA cycle counters, summed by DeviceOperator.profile_mr --
 //   [0] producer waiting for a free stage   [1] producer waiting on dependencies
 //   [2] producer issuing (stages + pass descriptors)   [3] producer ticket
@@ -261,8 +280,12 @@ __device__ void producer(const Params& p, double2* stages, int* s_kv, uint64_t* 
                 continue;
             }
             const bool hm = s0.mode == kModeH;
-            int nst = 0;  // stages of one pass: every K-chunk of every segment of the group
-            for (int si = s; si < e; ++si) nst += (seg_k(seg_at(p, si)) + kKC - 1) / kKC;
+            int nst = 0;  // stages of one pass: every K-chunk of every merged segment of the group
+            for (int si = s; si < e;) {
+                int K = 0;
+                si = merged_end(p, si, e, &K);
+                nst += (K + kKC - 1) / kKC;
+            }
             for (int rp = 0; rp < R; rp += kRP) {
                 const int rpn = min(kRP, R - rp);
                 for (int n0 = 0; n0 < nout; n0 += kNP) {
@@ -282,14 +305,15 @@ __device__ void producer(const Params& p, double2* stages, int* s_kv, uint64_t* 
                     }
                     fill_outputs(p, ps, out_b, out_e, s0.out_off + n0, np, lane);
                     ring.publish(lane);
-                    for (int si = s; si < e; ++si) {
+                    for (int si = s; si < e;) {
+                        int K = 0;
+                        const int sj = merged_end(p, si, e, &K);  // segments [si, sj): one T matrix
                         const SegD sg = seg_at(p, si);
-                        const int K = seg_k(sg);
                         // TMA coordinates: the segment starts at (row, col) = divmod(m_off, ld)
                         const int y0 = (int)(sg.m_off / sg.ld), x0 = (int)(sg.m_off % sg.ld);
                         const CUtensorMap* map = p.tmaps + 2 * sg.tmap + (hm ? 1 : 0);
-                        const double2* IN = (sg.in_buf == kBufX ? p.x : p.work) + sg.in_abs * (int64_t)R + rp;
                         const int nbox = hm ? 1 : (np + kKC - 1) / kKC;
+                        int sub = si, sub_k = 0;  // input sub-segment holding column k0
                         for (int k0 = 0; k0 < K; k0 += kKC) {
                             const int kv = min(kKC, K - k0);
                             long long tw = PROF ? clock64() : 0;
@@ -311,17 +335,31 @@ __device__ void producer(const Params& p, double2* stages, int* s_kv, uint64_t* 
                             } else if (lane == 0) {  // T rows k0..k0+16, columns n0..n0+80
                                 tma2d(st, map, 2 * (x0 + n0), y0 + k0, &full[stage]);
                             }
-                            if (rpn == R) {  // the IN rows are contiguous: one copy
-                                if (lane == 31) g2s(ti, IN + (int64_t)k0 * R, (uint32_t)(kv * R) * 16u, &full[stage]);
-                            } else {
-                                for (int k = lane; k < kv; k += 32)
-                                    g2s(ti + k * rpn, IN + (int64_t)(k0 + k) * R, rpn * 16u, &full[stage]);
+                            // IN rows k0..k0+kv, possibly from several input runs (one per
+                            // merged sub-segment, e.g. the u_b vectors of F_s)
+                            for (int k = 0; k < kv;) {
+                                while (k0 + k >= sub_k + seg_k(seg_at(p, sub))) {
+                                    sub_k += seg_k(seg_at(p, sub));
+                                    ++sub;
+                                }
+                                const SegD sb2 = seg_at(p, sub);
+                                const int take = min(kv - k, sub_k + seg_k(sb2) - (k0 + k));
+                                const double2* IN = (sb2.in_buf == kBufX ? p.x : p.work) +
+                                                    (sb2.in_abs + (k0 + k - sub_k)) * (int64_t)R + rp;
+                                if (rpn == R) {  // contiguous rows: one copy
+                                    if (lane == 31) g2s(ti + k * rpn, IN, (uint32_t)(take * R) * 16u, &full[stage]);
+                                } else {
+                                    for (int kk = lane; kk < take; kk += 32)
+                                        g2s(ti + (k + kk) * rpn, IN + (int64_t)kk * R, rpn * 16u, &full[stage]);
+                                }
+                                k += take;
                             }
                             if (++stage == kNST) {
                                 stage = 0;
                                 sphase ^= 1u;
                             }
                         }
+                        si = sj;
                     }
                 }
             }
