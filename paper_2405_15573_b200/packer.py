@@ -182,6 +182,40 @@ def _leaves_under(tree):
     return leaves, span
 
 
+def _stacks(tree, cmap, rank):
+    """Leaf-stacked basis layout: {leaf: (W, [(cluster, column offset)])} over the clusters of
+    ``cmap`` with rank > 0 that contain the leaf, root to leaf."""
+    leaves, span = _leaves_under(tree)
+    anc = _ancestors_in(tree, leaves, span, [c for c in cmap if rank[c] > 0])
+    out = {}
+    for p, leaf in enumerate(leaves):
+        cols, w = [], 0
+        for c in anc[p]:
+            cols.append((c, w))
+            w += rank[c]
+        if w:
+            out[leaf] = (w, cols)
+    return out
+
+
+def unstack_basis(packed_arena, geo, which: str, c: int):
+    """Reassemble cluster basis ``c`` (``which`` = "V" column, "U" row) from the leaf stacks
+    (test / inspection helper)."""
+    bct = geo["bct"]
+    tree, stacks, key = (bct.col_tree, geo["vstack"], "VS") if which == "V" else (bct.row_tree, geo["ustack"], "US")
+    nodes = tree.nodes
+    rank = (geo["rank_c"] if which == "V" else geo["rank_r"])[c]
+    out = np.zeros((nodes[c].size, rank), dtype=np.complex128)
+    for leaf, (W, cols) in stacks.items():
+        L = nodes[leaf]
+        if not (nodes[c].lo <= L.lo and L.hi <= nodes[c].hi):
+            continue
+        c0 = dict(cols)[c]
+        blk = packed_arena[geo["offs"][(key, leaf)] : geo["offs"][(key, leaf)] + L.size * W].reshape(L.size, W)
+        out[L.lo - nodes[c].lo : L.hi - nodes[c].lo] = blk[:, c0 : c0 + rank]
+    return out
+
+
 def _ancestors_in(tree, leaves, span, cset):
     """For every leaf position: the clusters of ``cset`` that contain it (root to leaf)."""
     anc = [[] for _ in leaves]
@@ -266,10 +300,16 @@ def pack(
         offs[key] = cursor
         cursor += _align(max(n, 0))
 
-    for t in sorted(bct.col_map):
-        alloc(("V", t), cnodes[t].size * rank_c[t], rank_c[t])
-    for s in sorted(bct.row_map):
-        alloc(("U", s), rnodes[s].size * rank_r[s], rank_r[s])
+    # Cluster bases are stored LEAF-STACKED: for every leaf L, the rows of the bases of all its
+    # ancestors (root to leaf) side by side, [B_t1[L rows] | B_t2[L rows] | ...], one |L| x W_L
+    # row-major matrix.  P1 (H) and FAR (N) of a leaf chunk then read ONE contiguous matrix
+    # with W_L-long rows instead of one short-row slab per ancestor.
+    vstack = _stacks(bct.col_tree, bct.col_map, rank_c)
+    ustack = _stacks(bct.row_tree, bct.row_map, rank_r)
+    for leaf, (W, _cols) in sorted(vstack.items()):
+        alloc(("VS", leaf), cnodes[leaf].size * W, W)
+    for leaf, (W, _cols) in sorted(ustack.items()):
+        alloc(("US", leaf), rnodes[leaf].size * W, W)
     fcols = {}  # s -> ([(bid, t, pos, k)], kfac)
     for s in sorted(bct.row_map):
         pos, cols = 0, []
@@ -315,10 +355,13 @@ def pack(
         if m.size:
             arena[offs[key] : offs[key] + m.size] = m.reshape(-1)
 
-    for t in bct.col_map:
-        put(("V", t), u.col_basis.matrices[t])
-    for s in bct.row_map:
-        put(("U", s), u.row_basis.matrices[s])
+    for key, stacks, nodes, basis in (("VS", vstack, cnodes, u.col_basis), ("US", ustack, rnodes, u.row_basis)):
+        for leaf, (W, cols) in stacks.items():
+            L = nodes[leaf]
+            blk = arena[offs[(key, leaf)] : offs[(key, leaf)] + L.size * W].reshape(L.size, W)
+            for c, c0 in cols:
+                m = np.asarray(basis.matrices[c])
+                blk[:, c0 : c0 + m.shape[1]] = m[L.lo - nodes[c].lo : L.hi - nodes[c].lo]
     for s, (cols, kfac) in fcols.items():
         ls = rank_r[s]
         if ls and kfac:
@@ -349,6 +392,7 @@ def pack(
     geo = dict(
         bct=bct, rank_r=rank_r, rank_c=rank_c, kb=kb, factorized=factorized,
         fcols=fcols, ycols=ycols, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
+        vstack=vstack, ustack=ustack,
     )
     if world > 1:
         rb = partition_bounds(bct.row_tree, world)
@@ -432,13 +476,15 @@ def _build_program(
         in_tree, out_tree = bct.row_tree, bct.col_tree
         in_map, out_map = bct.row_map, bct.col_map
         in_rank, out_rank = geo["rank_r"], geo["rank_c"]
-        in_basis_key, out_basis_key = "U", "V"
+        in_stack_key, out_stack_key = "US", "VS"
+        in_stacks, out_stacks = geo["ustack"], geo["vstack"]
         dense_by_outleaf = geo["dense_by_cleaf"]
     else:
         in_tree, out_tree = bct.col_tree, bct.row_tree
         in_map, out_map = bct.col_map, bct.row_map
         in_rank, out_rank = geo["rank_c"], geo["rank_r"]
-        in_basis_key, out_basis_key = "V", "U"
+        in_stack_key, out_stack_key = "VS", "US"
+        in_stacks, out_stacks = geo["vstack"], geo["ustack"]
         dense_by_outleaf = geo["dense_by_rleaf"]
     in_nodes, out_nodes = in_tree.nodes, out_tree.nodes
     if part is not None:
@@ -466,6 +512,28 @@ def _build_program(
 
         def out_needed(s_):
             return True
+
+    def stack_segs(key, stacks, leaf, leaf_lo, a, b, clist, rank_of, mode, x_off):
+        """Segments reading the basis rows [a, b) of clusters ``clist`` (root to leaf) from the
+        leaf stack: ONE segment when they are adjacent columns of it (always at a single GPU;
+        a rank's own clusters are the deep end of the chain), else one per cluster."""
+        W, cols = stacks[leaf]
+        c0 = dict(cols)
+        base = offs[(key, leaf)] + (a - leaf_lo) * W
+        first = c0[clist[0]]
+        adjacent = all(c0[c] == first + sum(rank_of[q] for q in clist[:i]) for i, c in enumerate(clist))
+        width = sum(rank_of[c] for c in clist)
+        if adjacent:
+            return [_seg(base + first, BUF_ARENA, b - a, width, W, mode, 0, 0, x_off)]
+        out, o = [], 0
+        for c in clist:
+            r = rank_of[c]
+            if mode == MODE_H:
+                out.append(_seg(base + c0[c], BUF_ARENA, b - a, r, W, mode, 0, o, x_off))
+            else:
+                out.append(_seg(base + c0[c], BUF_ARENA, b - a, r, W, mode, o, 0, x_off))
+            o += r
+        return out
 
     # ---- work-buffer layout ----
     work = 0
@@ -546,15 +614,16 @@ def _build_program(
             tot += in_rank[t]
         if cur:
             groups.append(cur)
+        leaf = in_leaves[p]
         for grp in groups:
             segs, outs, sigs = [], [], []
             oo = 0
             for t in grp:
                 lt = in_rank[t]
-                segs.append(_seg(offs[(in_basis_key, t)] + (a - in_nodes[t].lo) * lt, BUF_ARENA, b - a, lt, lt, MODE_H, 0, oo, a))
                 outs.append((BUF_WORK, part_off[t] + chunks_of[t].index(idx) * lt, lt, oo, 0))
                 sigs.append(c_part[t])
                 oo += lt
+            segs = stack_segs(in_stack_key, in_stacks, leaf, in_nodes[leaf].lo, a, b, grp, in_rank, MODE_H, a)
             ops[KIND_P1].append((KIND_P1, b - a, oo, [(BUF_X, a, b - a, 0, 0)], segs, outs, [], sigs, (b - a) * oo))
     # RED: y_t = sum of chunk partials (skipped when the single partial is y_t itself)
     for t in in_map:
@@ -687,9 +756,9 @@ def _build_program(
             for s in anc:
                 ls = out_rank[s]
                 in_runs.append((BUF_WORK, z_off[s], ls, pos, 0))
-                segs.append(_seg(offs[(out_basis_key, s)] + (a - out_nodes[s].lo) * ls, BUF_ARENA, rows, ls, ls, MODE_N, pos, 0))
                 waits.append((c_z[s], 1))
                 pos += ls
+            segs = stack_segs(out_stack_key, out_stacks, leaf, n.lo, a, b, anc, out_rank, MODE_N, -1)
             ops[KIND_FAR].append(
                 (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], waits, [], rows * pos)
             )

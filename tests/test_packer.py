@@ -147,20 +147,19 @@ def test_structure_bit_exact(golden):
             assert np.array_equal(slab, ref)
             seen += rows * cols
     assert seen == sum(d.size for d in u.dense.values())
-    # basis slabs through the FAR ops: rows of U_s for the chunk
+    # cluster bases: reassembled from the leaf stacks, bit for bit
+    from paper_2405_15573_b200.packer import unstack_basis
+
+    for which, cmap, basis in (("U", bct.row_map, u.row_basis), ("V", bct.col_map, u.col_basis)):
+        for c in cmap:
+            m = np.asarray(basis.matrices[c], dtype=np.complex128)
+            if m.shape[1] == 0:
+                continue
+            assert np.array_equal(unstack_basis(p.arena, p.geo, which, c), m), (which, c)
+    # and every FAR op reads one contiguous stacked slab: the rows of all ancestor bases
     for i in np.nonzero(prog.kinds == KIND_FAR)[0]:
-        out = prog.runs[prog.ops[i, 6]]
-        r_lo = out[1]
-        for s in prog.segs[prog.ops[i, 4] : prog.ops[i, 5]]:
-            m_off, _, rows, cols, ld = s[:5]
-            slab = p.arena[m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]]
-            hits = [
-                c for c, m in u.row_basis.matrices.items()
-                if c in bct.row_map and m.shape[1] == cols
-                and bct.row_tree.nodes[c].lo <= r_lo < bct.row_tree.nodes[c].hi
-                and np.array_equal(slab, np.asarray(m, dtype=np.complex128)[r_lo - bct.row_tree.nodes[c].lo :][:rows])
-            ]
-            assert hits
+        segs = prog.segs[prog.ops[i, 4] : prog.ops[i, 5]]
+        assert len({int(q[4]) for q in segs}) == 1  # one leaf stack (panel splits share its ld)
 
 
 def test_bytes_accounting(golden):
