@@ -17,6 +17,7 @@ from paper_2405_15573_b200.packer import (
     BUF_X,
     MODE_H,
     MODE_N,
+    MODE_NW,
     MODE_S,
     MR_FIRST,
     MR_ZERO,
@@ -54,7 +55,7 @@ def run_op(prog, i, bufs, engine="segs"):
         vin = bufs[BUF_X] if xg else xin
         idx = m_off + np.arange(rows)[:, None] * ld + np.arange(cols)[None, :]
         m = src[idx] if rows and cols else np.zeros((rows, cols), dtype=np.complex128)
-        if mode == MODE_N:
+        if mode == MODE_N or mode == MODE_NW:  # NW: same product, warp-per-row on the device
             out[out_off : out_off + rows] += m @ vin[in_off : in_off + cols]
         elif mode == MODE_H:
             out[out_off : out_off + cols] += np.conj(m).T @ vin[in_off : in_off + rows]

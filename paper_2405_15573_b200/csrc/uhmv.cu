@@ -52,6 +52,7 @@ constexpr int kHAcc = 4;                             // H/S accumulators per lan
 constexpr int kHColsMax = kHAcc * kLanesPerRow;      // 32 (= packer.HCOLS_MAX)
 
 constexpr int kModeN = 0, kModeH = 1, kModeS = 2;
+constexpr int kModeNW = 3;  // bulk pieces: N rows of a wide-row op, one warp per row (packer.MODE_NW)
 constexpr int kBufArena = 0, kBufWork = 1, kBufX = 2, kBufW = 3;
 constexpr int kOpFields = 16, kSegFields = 8, kRunFields = 5;
 

@@ -284,7 +284,7 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                                      (uint32_t)cols * 16, &full[stage], policy);
                     }
                     if (info & kPiXStage) {  // the piece's x window, right behind its rows
-                        const int w = (pmode == kModeN) ? cols : rows;
+                        const int w = (pmode == kModeN || pmode == kModeNW) ? cols : rows;
                         bulk_g2s(dst + (size_t)rows * cols * 16, p.x + xo, (uint32_t)w * 16,
                                  &full[stage], policy_keep);
                     }
@@ -439,7 +439,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                         }
                     }
                 }
-            } else if (g_mode >= 0) {
+            } else if (g_mode == kModeH || g_mode == kModeS) {  // (NW rows went to outv directly)
                 const int P = h_lanes(g_cols);
                 const int nJ = kConsumers / P;
                 const int cw = 32 / P;  // columns per warp: lane = column + cw * row offset
@@ -476,11 +476,13 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             const int in_off = c.y, out_off = c.z;
             const int mode = (c.w >> 16) & 0xF;
             const bool direct = (c.w & kCDirect) != 0;
-            if (mode == kModeN ? (g_mode != kModeN)
-                               : (g_mode != mode || g_out != out_off || g_cols != cols)) {
-                const bool to_h = (g_mode == kModeN) && mode != kModeN;
+            if ((mode == kModeN || mode == kModeNW) ? (g_mode != mode)
+                                                    : (g_mode != mode || g_out != out_off || g_cols != cols)) {
+                // row-group (N), warp (NW) and column (H/S) owners differ: order their outv adds
+                const bool to_other = g_mode >= 0 && g_mode != mode &&
+                                      (g_mode == kModeN || g_mode == kModeNW || mode == kModeN || mode == kModeNW);
                 flush();
-                if (to_h) consumer_sync();  // N owners and H owners differ: order their outv adds
+                if (to_other) consumer_sync();
                 g_mode = mode;
                 g_out = out_off;
                 g_cols = cols;
@@ -562,6 +564,46 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                             v.y += ai;
                             outv[o] = v;
                         }
+                    }
+                }
+            } else if (mode == kModeNW) {
+                // wide rows (few per piece): warp per row, 32 lanes x 16 B, reduced across the
+                // warp; row o belongs to warp o mod 4 in every piece (deterministic outv adds)
+                const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
+                const int w = tid >> 5;
+                for (int r = (w - out_off) & (kConsumerWarps - 1); r < rows; r += kConsumerWarps) {
+                    const double2* T = tile + r * cols + lane;
+                    const double2* X = xv + lane;
+                    double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
+                    double cr = 0.0, ci = 0.0, dr = 0.0, di = 0.0;
+                    const int nfull = cols >> 7;
+                    for (int k = 0; k < nfull; ++k) {
+                        const double2 t0 = T[0], x0 = X[0], t1 = T[32], x1 = X[32];
+                        const double2 t2 = T[64], x2 = X[64], t3 = T[96], x3 = X[96];
+                        cmac(ar, ai, t0, x0);
+                        cmac(br, bi, t1, x1);
+                        cmac(cr, ci, t2, x2);
+                        cmac(dr, di, t3, x3);
+                        T += 128;
+                        X += 128;
+                    }
+                    const int tail = cols & 127;
+                    if (lane < tail) cmac(ar, ai, T[0], X[0]);
+                    if (lane + 32 < tail) cmac(br, bi, T[32], X[32]);
+                    if (lane + 64 < tail) cmac(cr, ci, T[64], X[64]);
+                    if (lane + 96 < tail) cmac(dr, di, T[96], X[96]);
+                    ar += br + (cr + dr);
+                    ai += bi + (ci + di);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+                    }
+                    if (lane == 0) {
+                        double2 v = outv[out_off + r];
+                        v.x += ar;
+                        v.y += ai;
+                        outv[out_off + r] = v;
                     }
                 }
             } else {

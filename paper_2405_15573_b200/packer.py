@@ -47,6 +47,8 @@ import numpy as np
 __all__ = ["PackedOperator", "Program", "pack", "MODE_N", "MODE_H", "MODE_S"]
 
 MODE_N, MODE_H, MODE_S = 0, 1, 2
+MODE_NW = 3  # bulk-kernel piece mode: an N piece of a wide-row op (one warp per row)
+WIDE_COLS = 288  # an op whose N segments all have rows this long (<= 4 rows per stage) runs them warp-per-row
 BUF_ARENA, BUF_WORK, BUF_X, BUF_W = 0, 1, 2, 3
 RUN_ADD = 1  # out run: read-modify-write add (single writer)
 RUN_ATOMIC = 2  # out run: fp64 red.add -- w is zeroed first; <= 2 addends per entry
@@ -311,6 +313,7 @@ def pack(
     for leaf, (W, _cols) in sorted(ustack.items()):
         alloc(("US", leaf), rnodes[leaf].size * W, W)
     fcols = {}  # s -> ([(bid, t, pos, k)], kfac)
+    spos, cwidth = {}, {}  # product block -> column in C_s; s -> width of C_s
     for s in sorted(bct.row_map):
         pos, cols = 0, []
         for t in bct.row_map[s]:
@@ -319,11 +322,22 @@ def pack(
                 cols.append((bid, t, pos, kb[bid]))
                 pos += kb[bid]
         fcols[s] = (cols, pos)
-        alloc(("F", s), rank_r[s] * pos, pos)
+        # C_s = [F_s | S_b1 | S_b2 | ...]: the coupling of row cluster s as ONE l_s-row matrix
+        # (factorized s_x columns, then the product-form blocks in row_map order), so the
+        # forward Z op is a single long-row GEMV over all its inputs [u_b..., y_t...]
+        w = pos
         for t in bct.row_map[s]:
             bid = bct.block_of[(s, t)]
-            if not factorized[bid]:
-                alloc(("S", bid), rank_r[s] * rank_c[t], rank_c[t])
+            if not factorized[bid] and rank_c[t] > 0:
+                spos[bid] = w
+                w += rank_c[t]
+        cwidth[s] = w
+        alloc(("C", s), rank_r[s] * w, w)
+        offs[("F", s)] = offs[("C", s)]
+        for t in bct.row_map[s]:
+            bid = bct.block_of[(s, t)]
+            if bid in spos:
+                offs[("S", bid)] = offs[("C", s)] + spos[bid]
     ycols = {}  # t -> ([(bid, s, pos, k)], K')
     for t in sorted(bct.col_map):
         pos, cols = 0, []
@@ -363,16 +377,17 @@ def pack(
                 m = np.asarray(basis.matrices[c])
                 blk[:, c0 : c0 + m.shape[1]] = m[L.lo - nodes[c].lo : L.hi - nodes[c].lo]
     for s, (cols, kfac) in fcols.items():
-        ls = rank_r[s]
-        if ls and kfac:
-            fs = np.empty((ls, kfac), dtype=np.complex128)
+        ls, w = rank_r[s], cwidth[s]
+        if ls and w:
+            cs = np.empty((ls, w), dtype=np.complex128)
             for bid, t, pos, k in cols:
-                fs[:, pos : pos + k] = u.coeffs[bid].s_x
-            put(("F", s), fs)
-    for bid, s, t in adm:
-        if not factorized[bid]:
-            pair = u.coeffs[bid]
-            put(("S", bid), pair.s_x @ np.conj(pair.s_y).T)
+                cs[:, pos : pos + k] = u.coeffs[bid].s_x
+            for t in bct.row_map[s]:
+                bid = bct.block_of[(s, t)]
+                if bid in spos:
+                    pair = u.coeffs[bid]
+                    cs[:, spos[bid] : spos[bid] + rank_c[t]] = pair.s_x @ np.conj(pair.s_y).T
+            put(("C", s), cs)
     for t, (cols, ktot) in ycols.items():
         lt = rank_c[t]
         if lt and ktot:
@@ -392,7 +407,7 @@ def pack(
     geo = dict(
         bct=bct, rank_r=rank_r, rank_c=rank_c, kb=kb, factorized=factorized,
         fcols=fcols, ycols=ycols, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
-        vstack=vstack, ustack=ustack,
+        vstack=vstack, ustack=ustack, cwidth=cwidth, spos=spos,
     )
     if world > 1:
         rb = partition_bounds(bct.row_tree, world)
@@ -562,12 +577,28 @@ def _build_program(
             chunks_of[t].append(idx)
     # exchange region: per owner rank, its input clusters' [y_t | u_t] in position order, every
     # rank block padded to the same length (in-place all-gather target)
+    # u_t: forward, Y_t^H y_t (s_y of the factorized blocks); adjoint, u'_b = s_x^H y_s of the
+    # factorized blocks of row cluster s.  The adjoint U op of s runs over its whole coupling
+    # matrix C_s (packer arena) and also produces the partials S_b^H y_s of its product blocks,
+    # stored per output cluster t and producing rank, contiguous, summed by t's Z op.
     u_len = {t: (ycols[t][1] if not adjoint else fcols[t][1]) for t in in_map}
+    zparts = {}  # adjoint: (t, rank q) -> [product blocks (r, t) with owner_in(r) == q]
+    if adjoint:
+        for t in sorted(out_map, key=lambda t: out_nodes[t].lo):
+            if out_rank[t] == 0:
+                continue
+            for r in out_map[t]:
+                bid = bct.block_of[(r, t)]
+                if not factorized[bid] and in_rank[r] > 0:
+                    zparts.setdefault((t, owner_in(r)), []).append(bid)
     by_rank = [[] for _ in range(world)]
     for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
         by_rank[owner_in(t)].append(t)
-    ex_len = max([sum(in_rank[t] + u_len[t] for t in ts) for ts in by_rank] + [0])
-    y_off, u_off = {}, {}
+    zp_len = [0] * world
+    for (t, q), bids in zparts.items():
+        zp_len[q] += len(bids) * out_rank[t]
+    ex_len = max([sum(in_rank[t] + u_len[t] for t in ts) + zp_len[r] for r, ts in enumerate(by_rank)] + [0])
+    y_off, u_off, zp_off = {}, {}, {}
     for r, ts in enumerate(by_rank):
         cur = r * ex_len
         for t in ts:
@@ -575,6 +606,14 @@ def _build_program(
             cur += in_rank[t]
             u_off[t] = cur
             cur += u_len[t]
+        for (t, q), bids in sorted(zparts.items(), key=lambda kv: (out_nodes[kv[0][0]].lo, kv[0][1])):
+            if q == r:
+                zp_off[(t, q)] = cur
+                cur += len(bids) * out_rank[t]
+    zp_slot = {}  # product block -> its partial's work offset
+    for (t, q), bids in zparts.items():
+        for i, bid in enumerate(bids):
+            zp_slot[bid] = zp_off[(t, q)] + i * out_rank[t]
     walloc(world * ex_len)
     part_off = {}
     for t in sorted(in_map, key=lambda t: in_nodes[t].lo):
@@ -648,14 +687,23 @@ def _build_program(
     for t in in_map:
         n, lt = u_len[t], in_rank[t]
         u_wait[t] = []
-        if n == 0 or lt == 0 or owner_in(t) != rank:
+        if (n == 0 and not (adjoint and geo["cwidth"][t])) or lt == 0 or owner_in(t) != rank:
             continue
         u_wait[t] = [(c_u[t], 1)]
-        base = offs[("Y", t)] if not adjoint else offs[("F", t)]
+        if not adjoint:
+            base, ld, outs = offs[("Y", t)], n, [(BUF_WORK, u_off[t], n, 0, 0)]
+        else:  # the whole C_s: [F_s | S_b ...] -> [u'_b ... | partial slots of the product blocks]
+            base, ld = offs[("C", t)], geo["cwidth"][t]
+            outs = [(BUF_WORK, u_off[t], n, 0, 0)] if n else []
+            for r2 in bct.row_map[t]:
+                bid = bct.block_of[(t, r2)]
+                if bid in zp_slot:
+                    outs.append((BUF_WORK, zp_slot[bid], out_rank[r2], geo["spos"][bid], 0))
+            n = ld
         for c0, c1 in _chunks(0, n, split["u_cols"]):  # column panels: one op each
-            segs = [_seg(base + c0, BUF_ARENA, lt, c1 - c0, n, MODE_H, 0, 0)]
+            segs = [_seg(base + c0, BUF_ARENA, lt, c1 - c0, ld, MODE_H, 0, 0)]
             ops[KIND_U].append(
-                (KIND_U, lt, c1 - c0, [(BUF_WORK, y_off[t], lt, 0, 0)], segs, [(BUF_WORK, u_off[t] + c0, c1 - c0, 0, 0)],
+                (KIND_U, lt, c1 - c0, [(BUF_WORK, y_off[t], lt, 0, 0)], segs, _clip_runs(outs, c0, c1),
                  list(y_wait[t]), [c_u[t]], lt * (c1 - c0))
             )
     # Z: coupling, owned by the output cluster (row cluster forward, column cluster adjoint)
@@ -670,20 +718,19 @@ def _build_program(
                 if k:
                     in_runs.append((BUF_WORK, u_off[t] + u_pos[bid], k, pos, 0))
                     waits.extend(u_wait[t])
-            if kfac:
-                segs.append(_seg(offs[("F", s)], BUF_ARENA, ls, kfac, kfac, MODE_N, 0, 0))
             n_in = kfac
-            nbytes = ls * kfac
-            for t in out_map[s]:  # + S_b y_t for product blocks
+            for t in out_map[s]:  # + S_b y_t for product blocks (C_s columns after F_s)
                 bid = bct.block_of[(s, t)]
                 lt = in_rank[t]
                 if factorized[bid] or lt == 0:
                     continue
                 in_runs.append((BUF_WORK, y_off[t], lt, n_in, 0))
                 waits.extend(y_wait[t])
-                segs.append(_seg(offs[("S", bid)], BUF_ARENA, ls, lt, lt, MODE_N, n_in, 0))
                 n_in += lt
-                nbytes += ls * lt
+            assert n_in == geo["cwidth"][s]
+            if n_in:  # one segment: the whole C_s
+                segs.append(_seg(offs[("C", s)], BUF_ARENA, ls, n_in, n_in, MODE_N, 0, 0))
+            nbytes = ls * n_in
         else:
             cols, ktot = ycols[s]
             for bid, r, pos, k in cols:  # Y_t [u'_b ...]
@@ -694,16 +741,15 @@ def _build_program(
                 segs.append(_seg(offs[("Y", s)], BUF_ARENA, ls, ktot, ktot, MODE_N, 0, 0))
             n_in = ktot
             nbytes = ls * ktot
-            for r in out_map[s]:  # + S_b^H y'_r for product blocks
+            for r in out_map[s]:  # + S_b^H y'_r of product blocks: computed by U_r ...
                 bid = bct.block_of[(r, s)]
-                lr = in_rank[r]
-                if factorized[bid] or lr == 0:
-                    continue
-                in_runs.append((BUF_WORK, y_off[r], lr, n_in, 0))
-                waits.extend(y_wait[r])
-                segs.append(_seg(offs[("S", bid)], BUF_ARENA, lr, ls, ls, MODE_H, n_in, 0))
-                n_in += lr
-                nbytes += lr * ls
+                if bid in zp_slot:
+                    waits.extend(u_wait[r])
+            for q in range(world):  # ... and summed here, one contiguous run per producing rank
+                bids = zparts.get((s, q), [])
+                if bids:
+                    segs.append(_seg(zp_off[(s, q)], BUF_WORK, len(bids), ls, ls, MODE_S, 0, 0))
+                    nbytes += len(bids) * ls
         for o0, o1 in _chunks(0, ls, split["z_rows"]):  # output-row parts: one op each
             part = _restrict(segs, o0, o1)
             nb = sum(q[2] * q[3] for q in part)
@@ -807,6 +853,16 @@ def _build_program(
     return prog_a, work, ex
 
 
+def _clip_runs(runs, c0, c1):
+    """The output runs of vector positions [c0, c1), re-based to start at 0."""
+    out = []
+    for buf, off, ln, dst, fl in runs:
+        a, b = max(dst, c0), min(dst + ln, c1)
+        if a < b:
+            out.append((buf, off + (a - dst), b - a, a - c0, fl))
+    return out
+
+
 def _restrict(segs, o0, o1):
     """The part of an op's logical segments that produces output entries [o0, o1) (N: rows,
     H/S: columns), re-based so the part's outputs start at 0."""
@@ -873,6 +929,7 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS):
     for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in split:
         xs = x_off >= 0 and has_x
         if buf == BUF_WORK:  # coherent in-kernel data: no bulk copy, no stage
+            close()  # the open stage ends with the last staged piece
             out.append([m_off, ld, rows, cols, mode, in_off, out_off, PI_DIRECT])
             continue
         # elements a piece of n rows occupies in a stage (matrix + its x window)
@@ -1008,7 +1065,13 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
             segs.extend(_panel_split(s))
         seg_e = len(segs)
         pc_b = len(pieces)
-        pieces.extend(_pieces(ordered, has_x, stage_elems))
+        pcs = _pieces(ordered, has_x, stage_elems)
+        nsg = [q for q in ordered if q[5] == MODE_N]
+        if nsg and all(q[3] >= WIDE_COLS for q in nsg):  # long rows: few per piece
+            for pc in pcs:
+                if pc[4] == MODE_N:
+                    pc[4] = MODE_NW
+        pieces.extend(pcs)
         pc_e = len(pieces)
         mr_b = len(mr_segs)
         mr, mr_flags = _mr_groups(_resolve_inputs(ordered, in_runs), n_out)

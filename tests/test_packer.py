@@ -53,11 +53,11 @@ def test_pieces_tile_stages(golden):
             open_ = False
             fill = 0
             for m_off, ld, rows, cols, mode, in_off, out_off, info in pcs:
-                if mode != 0:
+                if mode in (1, 2):
                     assert cols <= BULK_HCOLS_MAX  # register slots of an H/S group
                 if info & PI_DIRECT:
                     continue
-                xw = (cols if mode == 0 else rows) if info & PI_XSTAGE else 0
+                xw = (cols if mode in (0, 3) else rows) if info & PI_XSTAGE else 0
                 if info & PI_BEGIN:
                     assert not open_
                     open_ = True
