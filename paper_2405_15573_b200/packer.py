@@ -80,6 +80,7 @@ MR_ROWS = 80  # multi-RHS programs: NEAR / FAR output rows per op (= mrtc kNP, o
 FAR_ROWS = 64  # output rows per FAR op (4 register slots of 16 row-groups)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
+BULK_NCOLS_MAX = 640  # widest N piece row (two rows + x window still fit a stage)
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 # work splitting of the farfield chain ops across CTAs (output entries per op)
 SPLIT_DEFAULTS = {"p1_out": 1 << 30, "u_cols": 1 << 30, "z_rows": 1 << 30, "far_rows": ROWS_PER_CHUNK}
@@ -921,9 +922,13 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS):
     split = []
     for sg in segs:  # H/S groups own at most BULK_HCOLS_MAX output columns: cut wider ones
         m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off = sg
-        if mode != MODE_N and cols > BULK_HCOLS_MAX:
-            for c0, c1 in _chunks(0, cols, BULK_HCOLS_MAX):
+        if mode != MODE_N and cols > min(BULK_HCOLS_MAX, stage_elems // 2):
+            for c0, c1 in _chunks(0, cols, min(BULK_HCOLS_MAX, stage_elems // 2)):
                 split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off))
+        elif mode == MODE_N and cols > min(BULK_NCOLS_MAX, stage_elems // 2):  # rows wider than a stage
+            for c0, c1 in _chunks(0, cols, min(BULK_NCOLS_MAX, stage_elems // 2)):  # -> column panels
+                split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off + c0, out_off,
+                              x_off + c0 if x_off >= 0 else x_off))
         else:
             split.append(sg)
     for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in split:

@@ -69,10 +69,17 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
         offs[key] = cursor
         cursor += _align(n)
 
-    for b in adm:
-        blk = bct.nodes[b]
-        alloc(("W", b), cnodes[blk.col].size * kb[b], kb[b])
-        alloc(("U", b), rnodes[blk.row].size * kb[b], kb[b])
+    # leaf-stacked factors (as packer.py stacks cluster bases): for every column leaf, the
+    # rows of W_b of all blocks whose column cluster contains it side by side; for every row
+    # leaf, the rows of U_b likewise -- P1 and FAR of a leaf chunk read one long-row matrix
+    cleaves, cspan = _leaves_under(bct.col_tree)
+    rleaves, rspan = _leaves_under(bct.row_tree)
+    wstack = _block_stacks(cleaves, cspan, adm, kb, lambda b: bct.nodes[b].col)
+    ustack = _block_stacks(rleaves, rspan, adm, kb, lambda b: bct.nodes[b].row)
+    for leaf, (w, _cols) in sorted(wstack.items()):
+        alloc(("WS", leaf), cnodes[leaf].size * w, w)
+    for leaf, (w, _cols) in sorted(ustack.items()):
+        alloc(("US", leaf), rnodes[leaf].size * w, w)
     dense_by_rleaf, dense_by_cleaf = {}, {}
     for bid in h.dense:
         blk = bct.nodes[bid]
@@ -88,18 +95,27 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
             alloc(("D", bid), rr * cc, cc)
     arena = np.zeros(max(cursor, 8), dtype=np.complex128)
     elems = 0
+    fac = {}
     for b in adm:
         f = h.admissible[b]
         wmat = np.asarray(f.V, dtype=np.complex128) * np.asarray(f.sigma, dtype=np.float64)[None, :]
-        arena[offs[("W", b)] : offs[("W", b)] + wmat.size] = wmat.reshape(-1)
         um = np.asarray(f.U, dtype=np.complex128)
-        arena[offs[("U", b)] : offs[("U", b)] + um.size] = um.reshape(-1)
+        fac[b] = (wmat, um)
         elems += wmat.size + um.size
+    for key, stacks, nodes, which, cl in (("WS", wstack, cnodes, 0, lambda b: bct.nodes[b].col),
+                                          ("US", ustack, rnodes, 1, lambda b: bct.nodes[b].row)):
+        for leaf, (w, cols) in stacks.items():
+            L = nodes[leaf]
+            blk = arena[offs[(key, leaf)] : offs[(key, leaf)] + L.size * w].reshape(L.size, w)
+            for b, c0 in cols:
+                lo = nodes[cl(b)].lo
+                blk[:, c0 : c0 + kb[b]] = fac[b][which][L.lo - lo : L.hi - lo]
     dense_elems = 0
     for bid, d in h.dense.items():
         arena[offs[("D", bid)] : offs[("D", bid)] + d.size] = np.asarray(d).reshape(-1)
         dense_elems += d.size
-    geo = dict(bct=bct, adm=adm, kb=kb, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf)
+    geo = dict(bct=bct, adm=adm, kb=kb, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
+               wstack=wstack, ustack=ustack)
     kw = dict(rows_per_chunk=rows_per_chunk, stage_elems=stage_elems, near_interleave=near_interleave)
     fwd, work_f = _build_h(geo, adjoint=False, **kw)
     adj, work_a = _build_h(geo, adjoint=True, **kw)
@@ -113,11 +129,31 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
     )
 
 
+def _block_stacks(leaves, span, adm, kb, clus):
+    """{leaf: (width, [(block, column offset)])}: blocks (in ``adm`` order) whose cluster
+    ``clus(b)`` contains the leaf."""
+    per = [[] for _ in leaves]
+    for b in adm:
+        a, e = span[clus(b)]
+        for p in range(a, e):
+            per[p].append(b)
+    out = {}
+    for p, leaf in enumerate(leaves):
+        cols, w = [], 0
+        for b in per[p]:
+            cols.append((b, w))
+            w += kb[b]
+        if w:
+            out[leaf] = (w, cols)
+    return out
+
+
 def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
     bct, adm, kb, offs = geo["bct"], geo["adm"], geo["kb"], geo["offs"]
     if adjoint:
         in_tree, out_tree = bct.row_tree, bct.col_tree
-        in_key, out_key = "U", "W"
+        in_key, out_key = "US", "WS"
+        in_stacks, out_stacks = geo["ustack"], geo["wstack"]
         dense_by_outleaf = geo["dense_by_cleaf"]
 
         def in_c(b):
@@ -127,7 +163,8 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
             return bct.nodes[b].col
     else:
         in_tree, out_tree = bct.col_tree, bct.row_tree
-        in_key, out_key = "W", "U"
+        in_key, out_key = "WS", "US"
+        in_stacks, out_stacks = geo["wstack"], geo["ustack"]
         dense_by_outleaf = geo["dense_by_rleaf"]
 
         def in_c(b):
@@ -196,13 +233,16 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
     for idx, (p, a, e, grp) in enumerate(items):
         segs, outs, sigs = [], [], []
         oo = 0
+        leaf = in_leaves[p]
+        W, cols = in_stacks[leaf]
+        c0 = dict(cols)[grp[0]]  # a group is a run of adjacent stack columns
         for b in grp:
             k = kb[b]
-            lo_c = in_nodes[in_c(b)].lo
-            segs.append(_seg(offs[(in_key, b)] + (a - lo_c) * k, BUF_ARENA, e - a, k, k, MODE_H, 0, oo, a))
             outs.append((BUF_WORK, part_off[b] + chunks_of[b].index(idx) * k, k, oo, 0))
             sigs.append(c_part[b])
             oo += k
+        base = offs[(in_key, leaf)] + (a - in_nodes[leaf].lo) * W
+        segs.append(_seg(base + c0, BUF_ARENA, e - a, oo, W, MODE_H, 0, 0, a))
         ops[KIND_P1].append((KIND_P1, e - a, oo, [(BUF_X, a, e - a, 0, 0)], segs, outs, [], sigs, (e - a) * oo))
     y_wait = {}
     for b in adm:
@@ -248,11 +288,12 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
             in_runs, segs, waits, pos = [], [], [], 0
             for b in bl:
                 k = kb[b]
-                lo_c = out_nodes[out_c(b)].lo
                 in_runs.append((BUF_WORK, y_off[b], k, pos, 0))
-                segs.append(_seg(offs[(out_key, b)] + (a - lo_c) * k, BUF_ARENA, rows, k, k, MODE_N, pos, 0))
                 waits.append(y_wait[b])
                 pos += k
+            W, _cols = out_stacks[leaf]
+            assert W == pos
+            segs.append(_seg(offs[(out_key, leaf)] + (a - n.lo) * W, BUF_ARENA, rows, W, W, MODE_N, 0, 0))
             ops[KIND_FAR].append(
                 (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], sorted(set(waits)), [], rows * pos)
             )

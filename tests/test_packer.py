@@ -221,3 +221,17 @@ def test_mr_segments_fit_tma_rows(name):
                 continue
             assert m_off % ld + cols <= ld, (m_off, ld, cols)
             assert prog.mr_lds[mode >> MR_TMAP_SHIFT] == ld
+
+
+@pytest.mark.parametrize("name", ["helm400", "ico2_helm_compress", "rect_sphere"])
+def test_small_stages_split_wide_rows(name):
+    """With tiny stages every wide N row is cut into column panels and every wide H piece into
+    column groups; the pieces program still computes the reference's outputs."""
+    u, ex = load_golden(name)
+    p = pack(u, stage_elems=96)
+    for prog in (p.fwd, p.adj):
+        pcs = prog.pieces
+        assert (pcs[:, 3][np.isin(pcs[:, 4], (0, 3))] <= 48).all()
+    for adjoint, vk, rk in ((False, "vf_0", "ref_fwd_0"), (True, "va_0", "ref_adj_0")):
+        w = vm_matvec(p, ex[vk], adjoint=adjoint, order="fused", engine="pieces")
+        assert rel(w, ex[rk]) <= TOL
