@@ -305,17 +305,29 @@ class DeviceOperator:
         """End-to-end C-ABI call with host buffers (H2D, kernels, D2H, sync)."""
         p = self.packed
         n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
-        x_host = np.ascontiguousarray(x_host, dtype=np.complex128)
+        if x_host.dtype != np.complex128 or not x_host.flags.c_contiguous:
+            x_host = np.ascontiguousarray(x_host, dtype=np.complex128)
         if x_host.shape != (n_in,):
             raise ValueError(f"x must have shape ({n_in},)")
         if out is None:
             out = np.empty(n_out, dtype=np.complex128)
+        elif out.dtype != np.complex128 or not out.flags.c_contiguous or out.shape != (n_out,):
+            raise ValueError(f"out must be a contiguous complex128 array of shape ({n_out},)")
         mode = mode or default_mode()
-        with self._lock, self.torch.cuda.device(self.device):
-            rc = _lib.lib().uhmv_matvec_host(
-                self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data), int(adjoint),
-                _MODES[mode], self._stream(stream),
-            )
+        torch = self.torch
+        with self._lock:
+            # (the device switch costs ~10 us of host time per call: only when needed)
+            if torch.cuda.current_device() == self.device.index:
+                rc = _lib.lib().uhmv_matvec_host(
+                    self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+                    int(adjoint), _MODES[mode], self._stream(stream),
+                )
+            else:
+                with torch.cuda.device(self.device):
+                    rc = _lib.lib().uhmv_matvec_host(
+                        self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+                        int(adjoint), _MODES[mode], self._stream(stream),
+                    )
         _lib.check(rc, "uhmv_matvec_host")
         return out
 
