@@ -41,6 +41,12 @@ def parse():
     ap.add_argument("--view", default="full", choices=["full", "far", "near"], help="diagnostics: parity view")
     ap.add_argument("--format", default="uh", choices=["uh", "h"],
                     help="uh: uniform H-matrix (the hot path); h: the source H-matrix (matvec_h)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+                    help="multi-GPU y/u exchange: NCCL all-gather between two launches, or peer stores "
+                         "over NVLink inside one launch per rank")
+    ap.add_argument("--emulate-ranks", type=int, default=0,
+                    help="diagnostics (1 GPU): run a W-rank peer-exchange partition in one launch, "
+                         "each rank on 1/W of the SMs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     return ap.parse_args()
@@ -179,6 +185,11 @@ def main():
         "adjoint": bool(args.adjoint),
         "parallelism": f"row-partition x{args.gpus}" if args.gpus > 1 else "single GPU",
     }
+    if args.gpus > 1:
+        config["exchange"] = args.exchange
+    if args.emulate_ranks > 1:
+        config["parallelism"] = (f"peer-exchange partition of {args.emulate_ranks} ranks emulated in one launch "
+                                 f"on one GPU (1/{args.emulate_ranks} of the SMs each)")
 
     if args.impl == "reference":
         run_reference(args, rank, world, config)
@@ -210,8 +221,13 @@ def main():
     if world > 1:
         from paper_2405_15573_b200.dist import DistributedOperator
 
-        op = DistributedOperator(u, rank, world, device=dev)
+        op = DistributedOperator(u, rank, world, device=dev, exchange=args.exchange)
         packed = op.packed_local
+    elif args.emulate_ranks > 1:
+        from paper_2405_15573_b200.dist import PeerEmulation
+
+        op = PeerEmulation(u, args.emulate_ranks, device=dev)
+        packed = op.packs[0]
     else:
         from paper_2405_15573_b200.device import DeviceOperator
 
@@ -330,7 +346,8 @@ def main():
         "frac_vs_8000_nominal": achieved / 8000.0,
         "traffic": traffic,
         "algorithmic_bytes_per_launch": int(alg_bytes_total / world),
-        "kernel": {"bulk": "bulk::uhmv_bulk_kernel", "fused": "uhmv_fused_kernel"}.get(args.mode, "uhmv_phase_kernel (5 launches)"),
+        "kernel": "bulk::uhmv_bulk_peer_kernel" if (args.emulate_ranks > 1 or args.exchange == "peer") else
+        {"bulk": "bulk::uhmv_bulk_kernel", "fused": "uhmv_fused_kernel"}.get(args.mode, "uhmv_phase_kernel (5 launches)"),
     }
     if rank != 0:
         if world > 1:

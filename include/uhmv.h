@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 7
+#define UHMV_ABI_VERSION 8
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -123,6 +123,34 @@ int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjo
  * rejects 2-D input).  Asynchronous. */
 int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs,
                       int adjoint, void* stream);
+
+/* One rank of a peer-exchange partition (packer pack(peer=True)), as mapped in the calling
+ * process: its own buffers, or a peer's NVLink-mapped ones (CUDA IPC / symmetric memory). */
+typedef struct uhmv_peer_rank {
+    void* work;          /* complex128 work buffer of 2 x work_len elements: epoch e uses half e & 1 */
+    int64_t work_len;    /* that rank's program work length (uhmv_desc.work_len of its plan)     */
+    uint32_t* counters;  /* >= n_counters uint32, zero before epoch 1 (monotonic afterwards)       */
+    uint32_t* done;      /* world uint32, zero before epoch 1: done[q] = last epoch rank q finished */
+} uhmv_peer_rank;
+
+/* Multi-GPU matvec with the y/u exchange fused into the kernel: ONE launch per rank, whose
+ * producer ops store this rank's y_t / u_t into every rank's work buffer over NVLink and
+ * signal the peers' dependency counters (system-scope release); Z ops wait on them.  Replaces
+ * the launch A / NCCL all-gather / launch B sequence of the partitioned path.
+ * plans[0..nplans): the plans of ranks rank0 .. rank0+nplans-1 (nplans = 1 on a real multi-GPU
+ * rank; nplans = world emulates the whole partition in one launch on one GPU, each rank on
+ * its share of the SMs).  ranks[0..world): every rank's buffers.  w[i]: rank rank0+i's output
+ * (zeroed here; ranks write disjoint rows, so the emulation may pass one vector for all).
+ * epoch: 1, 2, ... consecutive per partition.  Asynchronous. */
+int uhmv_execute_peer(uhmv_plan* const* plans, int nplans, int rank0, int world,
+                      const uhmv_peer_rank* ranks, const void* x, void* const* w, int adjoint,
+                      uint32_t epoch, void* stream);
+
+/* Diagnostics of uhmv_execute_peer: a peer wait polls 2^spin_log2 times (default 28, ~10 s)
+ * before trapping; host_mapped (pinned, device-visible, 512 uint32, zeroed, or NULL) receives
+ * [0] the number of timed-out waits and, from [8], up to 63 records of 8 uint32: {rank,
+ * counter (or 0x80000000 | peer for a done flag), value, need, epoch, block, 1, 0}. */
+int uhmv_peer_set_diag(void* host_mapped, int spin_log2);
 
 /* Launch geometry chosen for a mode (grid CTAs, dynamic shared memory bytes, threads per CTA,
  * shared-memory stages of the bulk engine). */

@@ -21,14 +21,16 @@ from paper_2405_15573_b200.packer import (
     MODE_S,
     MR_FIRST,
     MR_ZERO,
+    OP_PEER,
     PI_DIRECT,
     PI_XGLOBAL,
     PI_XSTAGE,
     RUN_ADD,
     RUN_ATOMIC,
+    RUN_PEER,
 )
 
-__all__ = ["run_program", "vm_matvec"]
+__all__ = ["run_program", "vm_matvec", "vm_peer_matvec"]
 
 
 def _segments(prog, i, engine):
@@ -43,7 +45,9 @@ def _segments(prog, i, engine):
             yield (m_off, buf, rows, cols, ld, mode, in_off, out_off, bool(info & (PI_XGLOBAL | PI_XSTAGE)))
 
 
-def run_op(prog, i, bufs, engine="segs"):
+def run_op(prog, i, bufs, engine="segs", peers=()):
+    """One op; ``peers``: the other ranks' work buffers (peer-exchange programs store their
+    RUN_PEER outputs there too)."""
     n_in, n_out, in_b, in_e = (int(v) for v in prog.ops[i, :4])
     out_b, out_e = (int(v) for v in prog.ops[i, 6:8])
     xin = np.zeros(n_in, dtype=np.complex128)
@@ -68,6 +72,9 @@ def run_op(prog, i, bufs, engine="segs"):
             bufs[buf][off : off + ln] += out[dst : dst + ln]
         else:
             bufs[buf][off : off + ln] = out[dst : dst + ln]
+        if flags & RUN_PEER:
+            for pw in peers:
+                pw[off : off + ln] = out[dst : dst + ln]
 
 
 def run_program(prog, arena, work, x, w, order="phased", op_range=None, engine="segs"):
@@ -96,6 +103,47 @@ def vm_matvec(packed, v, adjoint=False, order="phased", engine="segs"):
     w = np.zeros(n_out, dtype=np.complex128)  # the launcher zeroes w (NEAR/FAR add atomically)
     work = np.zeros(packed.work_len, dtype=np.complex128)
     run_program(prog, packed.arena, work, x, w, order=order, engine=engine)
+    return w
+
+
+def vm_peer_matvec(packs, v, adjoint=False, engine="pieces", epochs=1):
+    """Emulate the W ranks of a peer-exchange partition (``pack(..., peer=True)``) in one
+    process: each rank walks its fused ticket order in turn, running ops while their waits
+    are met (counters are monotonic: epoch e waits for e x count, as on the device); RUN_PEER
+    outputs are stored into every rank's work buffer and OP_PEER ops signal every rank's
+    counters.  A round with no progress is a deadlock (assertion).  Returns w (every rank
+    adds its own rows into one zeroed vector) after ``epochs`` consecutive matvecs."""
+    W = len(packs)
+    progs = [p.adj if adjoint else p.fwd for p in packs]
+    assert all(pr.peer for pr in progs)
+    p0 = packs[0]
+    n_in, n_out = (p0.n_rows, p0.n_cols) if adjoint else (p0.n_cols, p0.n_rows)
+    x = np.asarray(v, dtype=np.complex128)
+    assert x.shape == (n_in,)
+    works = [np.zeros(p.work_len, dtype=np.complex128) for p in packs]
+    ctr = [np.zeros(max(pr.n_counters, 1), dtype=np.int64) for pr in progs]
+    for epoch in range(1, epochs + 1):
+        w = np.zeros(n_out, dtype=np.complex128)
+        seqs = [pr.fused_order.tolist() for pr in progs]
+        pos = [0] * W
+        while any(pos[r] < len(seqs[r]) for r in range(W)):
+            progressed = False
+            for r in range(W):
+                pr = progs[r]
+                while pos[r] < len(seqs[r]):
+                    i = seqs[r][pos[r]]
+                    wb, we, sb, se = (int(q) for q in pr.ops[i, 8:12])
+                    if any(ctr[r][c] < epoch * cnt for c, cnt in pr.waits[wb:we]):
+                        break
+                    bufs = {BUF_ARENA: packs[r].arena, BUF_WORK: works[r], BUF_X: x, BUF_W: w}
+                    run_op(pr, i, bufs, engine, peers=[works[q] for q in range(W) if q != r])
+                    targets = range(W) if pr.ops[i, 12] & OP_PEER else (r,)
+                    for c in pr.sigs[sb:se]:
+                        for q in targets:
+                            ctr[q][c] += 1
+                    pos[r] += 1
+                    progressed = True
+            assert progressed, f"peer programs deadlock at tickets {pos}"
     return w
 
 

@@ -10,11 +10,11 @@ from __future__ import annotations
 import ctypes
 import os
 
-__all__ = ["lib", "UhmvProgram", "UhmvDesc", "check", "LIB_PATH", "MAX_PHASES"]
+__all__ = ["lib", "UhmvProgram", "UhmvDesc", "UhmvPeerRank", "check", "LIB_PATH", "MAX_PHASES"]
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 7
+ABI_VERSION = 8
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -65,6 +65,15 @@ class UhmvDesc(ctypes.Structure):
     ]
 
 
+class UhmvPeerRank(ctypes.Structure):
+    _fields_ = [
+        ("work", ctypes.c_void_p),
+        ("work_len", ctypes.c_int64),
+        ("counters", ctypes.c_void_p),
+        ("done", ctypes.c_void_p),
+    ]
+
+
 _lib = None
 
 EXPORTS = (
@@ -74,6 +83,8 @@ EXPORTS = (
     "uhmv_execute_phases",
     "uhmv_matvec_host",
     "uhmv_execute_mrhs",
+    "uhmv_execute_peer",
+    "uhmv_peer_set_diag",
     "uhmv_plan_info",
     "uhmv_plan_set_profile",
     "uhmv_dmma_peak",
@@ -104,6 +115,10 @@ def lib():
     L.uhmv_matvec_host.argtypes = [vp, vp, vp, i32, i32, vp]
     L.uhmv_execute_mrhs.argtypes = [vp, vp, vp, vp, i32, i32, vp]
     L.uhmv_execute_mrhs.restype = i32
+    L.uhmv_execute_peer.argtypes = [vp, i32, i32, i32, ctypes.POINTER(UhmvPeerRank), vp, vp, i32, ctypes.c_uint32, vp]
+    L.uhmv_execute_peer.restype = i32
+    L.uhmv_peer_set_diag.argtypes = [vp, i32]
+    L.uhmv_peer_set_diag.restype = i32
     L.uhmv_matvec_host.restype = i32
     pi = ctypes.POINTER(i32)
     L.uhmv_plan_info.argtypes = [vp, i32, i32, pi, pi, pi, pi]

@@ -431,6 +431,7 @@ struct uhmv_plan {
     int fused_grid[2];
     int smem[2];
     int bulk_grid[2];
+    int bulk_full_grid[2];  // resident CTAs per SM x SMs (the peer launch splits it over ranks)
     int bulk_smem[2];
     int bulk_nstage[2];
     int sm_count;
@@ -595,6 +596,9 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem_optin);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(bulk::uhmv_bulk_peer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_optin);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel<true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
     if (e != cudaSuccess) {
@@ -611,6 +615,7 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         }
         if (per_sm < 1) per_sm = 1;
         int grid = per_sm * p->sm_count;
+        p->bulk_full_grid[k] = grid;
         if (grid > progs[k]->n_ops) grid = progs[k]->n_ops > 0 ? progs[k]->n_ops : 1;
         p->bulk_grid[k] = grid;
     }
@@ -757,6 +762,78 @@ int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode,
                         static_cast<cudaStream_t>(stream)>>>(ep);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "uhmv_fused_kernel launch");
+    return UHMV_OK;
+}
+
+static uint32_t* g_peer_diag = nullptr;
+static int g_peer_spin_log2 = 28;
+
+int uhmv_peer_set_diag(void* host_mapped, int spin_log2) {
+    g_peer_diag = static_cast<uint32_t*>(host_mapped);
+    g_peer_spin_log2 = (spin_log2 >= 10 && spin_log2 <= 40) ? spin_log2 : 28;
+    return UHMV_OK;
+}
+
+int uhmv_execute_peer(uhmv_plan* const* plans, int nplans, int rank0, int world,
+                      const uhmv_peer_rank* ranks, const void* x, void* const* w, int adjoint,
+                      uint32_t epoch, void* stream) {
+    if (!plans || !ranks || !w || !x) return fail(UHMV_EINVAL, "uhmv_execute_peer: null argument");
+    if (world < 1 || world > bulk::kMaxRanks || nplans < 1 || rank0 < 0 || rank0 + nplans > world)
+        return fail(UHMV_EINVAL, "uhmv_execute_peer: bad rank range");
+    if (epoch == 0) return fail(UHMV_EINVAL, "uhmv_execute_peer: epochs start at 1");
+    for (int q = 0; q < world; ++q)
+        if (!ranks[q].work || !ranks[q].counters || !ranks[q].done || ranks[q].work_len < 0)
+            return fail(UHMV_EINVAL, "uhmv_execute_peer: null peer buffer");
+    const int k = adjoint ? 1 : 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int grid = 0, smem = 0;
+    for (int i = 0; i < nplans; ++i) {
+        if (!plans[i]) return fail(UHMV_EINVAL, "uhmv_execute_peer: null plan");
+        const uhmv_program& pr = adjoint ? plans[i]->d.adj : plans[i]->d.fwd;
+        if (pr.n_ops > 0 && !pr.pieces) return fail(UHMV_EINVAL, "peer execution needs the piece table");
+        if (plans[i]->bulk_smem[k] > smem) smem = plans[i]->bulk_smem[k];
+        // every CTA must be resident (ranks wait on one another inside the launch): the
+        // smallest full grid, i.e. the one of the largest shared-memory footprint
+        if (i == 0 || plans[i]->bulk_full_grid[k] < grid) grid = plans[i]->bulk_full_grid[k];
+        if (!w[i]) return fail(UHMV_EINVAL, "uhmv_execute_peer: null output");
+        bool seen = false;  // zero every distinct output once (NEAR/FAR add into it)
+        for (int j = 0; j < i; ++j) seen = seen || (w[j] == w[i]);
+        const int64_t n_out = adjoint ? plans[i]->d.n_cols : plans[i]->d.n_rows;
+        if (!seen && n_out > 0) {
+            cudaError_t e0 = cudaMemsetAsync(w[i], 0, (size_t)n_out * 16, st);
+            if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
+        }
+    }
+    if (grid < nplans) return fail(UHMV_EINVAL, "uhmv_execute_peer: fewer CTAs than ranks");
+    bulk::PeerLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.nranks = nplans;
+    for (int i = 0; i < nplans; ++i) {
+        const int r = rank0 + i;
+        const uhmv_program& pr = adjoint ? plans[i]->d.adj : plans[i]->d.fwd;
+        bulk::Params bp = make_bulk_params(plans[i], pr, k, x, w[i]);
+        bp.prof = nullptr;
+        bp.rank = r;
+        bp.world = world;
+        bp.epoch = epoch;
+        const long long lo = ((long long)i * grid + nplans - 1) / nplans;
+        const long long hi = ((long long)(i + 1) * grid + nplans - 1) / nplans;
+        bp.n_ctas = (int32_t)(hi - lo);
+        for (int q = 0; q < world; ++q) {
+            bp.peer_work[q] = static_cast<double2*>(ranks[q].work) + (epoch & 1u) * ranks[q].work_len;
+            bp.peer_counters[q] = ranks[q].counters;
+            bp.peer_done[q] = ranks[q].done;
+        }
+        bp.diag = g_peer_diag;
+        bp.spin_log2 = g_peer_spin_log2;
+        bp.work = bp.peer_work[r];
+        bp.counters = ranks[r].counters;
+        bp.done = ranks[r].done;
+        L.r[i] = bp;
+    }
+    bulk::uhmv_bulk_peer_kernel<<<grid, bulk::kThreads, smem, st>>>(L);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "uhmv_bulk_peer_kernel launch");
     return UHMV_OK;
 }
 

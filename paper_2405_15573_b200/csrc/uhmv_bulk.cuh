@@ -33,6 +33,9 @@ constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
 
 constexpr int kOpSlots = 2;
+constexpr int kMaxRanks = 8;      // peer-exchange programs: ranks of one NVLink domain
+constexpr int kOpPeer = 16;       // op field 12 flag (packer.OP_PEER)
+constexpr int kRunPeer = 4;       // out-run flag (packer.RUN_PEER)
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
 static_assert((kRowGroups & (kRowGroups - 1)) == 0 && (kConsumers & (kConsumers - 1)) == 0,
@@ -84,6 +87,24 @@ struct Params {
     int32_t skip_waits;        // diagnostics: ignore dependencies (results are wrong)
     int32_t dbg;               // diagnostics: 1 skip compute, 2 skip gather/scatter (wrong results)
     unsigned long long* prof;  // optional [grid][64] cycle counters, else null
+    // ---- peer-exchange programs only (PEER kernels, packer pack(peer=True)) ----
+    int32_t rank, world;
+    uint32_t epoch;     // 1, 2, ...: counters are monotonic, a wait for n arrivals needs n x epoch
+    int32_t n_ctas;     // CTAs running this rank's program (the self-reset's exit count)
+    double2* peer_work[kMaxRanks];       // every rank's work buffer, this epoch's half ([rank] = work)
+    uint32_t* peer_counters[kMaxRanks];  // every rank's dependency counters
+    uint32_t* peer_done[kMaxRanks];      // every rank's done-epoch array (world uint32 each)
+    uint32_t* done;                      // this rank's done-epoch array: done[q] = last epoch q finished
+    uint32_t* diag;     // optional host-mapped record of a timed-out wait (rank, what, value, need)
+    int32_t spin_log2;  // bounded spin of the peer waits: 2^spin_log2 polls, then trap
+};
+
+// One launch running the programs of several ranks (peer-exchange emulation of a multi-GPU
+// partition on one GPU: CTAs [r*G/n, (r+1)*G/n) run rank r).  A real multi-GPU rank launches it
+// with n = 1 and its peers' NVLink-mapped pointers.
+struct PeerLaunch {
+    Params r[kMaxRanks];
+    int32_t nranks;
 };
 
 // prof layout per CTA (64 x u64): [kind * 8 + c] for op kinds 0..6 with c = 0 consumer waiting
@@ -147,6 +168,50 @@ __device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
 }
 __device__ __forceinline__ void red_relaxed_add(uint32_t* p, uint32_t v) {
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// system scope (peer-exchange programs: counters and flags another GPU writes over NVLink)
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_relaxed_add_sys(uint32_t* p, uint32_t v) {
+    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Bounded spin of the peer-exchange waits: a peer that never arrives (a dead rank) traps the
+// kernel after ~20 s instead of hanging the GPU.
+template <bool PEER>
+__device__ __forceinline__ void wait_count(const uint32_t* c, uint32_t need, const Params& p, uint32_t what) {
+    if (!PEER) {
+        while (ld_acquire(c) < need) __nanosleep(20);
+        return;
+    }
+    long long spins = 0;
+    uint32_t v;
+    while ((int32_t)((v = ld_acquire_sys(c)) - need) < 0) {  // wrap-safe: counters grow monotonically
+        __nanosleep(32);
+        if (++spins > (1ll << p.spin_log2)) {
+            if (p.diag) {  // record (up to 63 waits), then give the others time to record too
+                const uint32_t i = atomicAdd(p.diag, 1u);
+                if (i < 63) {
+                    uint32_t* rec = p.diag + 8 + 8 * i;
+                    rec[0] = (uint32_t)p.rank;
+                    rec[1] = what;
+                    rec[2] = v;
+                    rec[3] = need;
+                    rec[4] = p.epoch;
+                    rec[5] = blockIdx.x;
+                    rec[6] = 1;
+                }
+                __threadfence_system();
+                for (int k = 0; k < 4096; ++k) __nanosleep(1000000);
+            }
+            __trap();
+        }
+    }
 }
 // Signal counters sigs[b..e) once every prior write of the CTA (ordered before the caller by
 // a bar.sync) is visible: ONE release fence, then relaxed adds (a release pattern each).
@@ -341,7 +406,7 @@ __device__ __forceinline__ int4 get_piece(const Params& p, const OpSlot* S, int 
                           __ldg(d + 7));
 }
 
-template <bool PROF>
+template <bool PROF, bool PEER>
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
                                          double2* outv, uint64_t* full, uint64_t* empty,
                                          uint64_t* opfull, uint64_t* opempty, OpSlot* slots,
@@ -374,6 +439,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         const int out_e = S->hdr[7];
         const int pc_b = S->hdr[13], pc_e = S->hdr[14];
         const int kind = S->hdr[12] & 7;
+        const bool peer_op = PEER && (S->hdr[12] & kOpPeer);  // (read while the slot is held)
         const int n_in_runs = in_e - in_b;
         const int n_runs = out_e - in_b;
         if (!p.skip_waits) {  // every consumer thread polls one dependency counter in parallel
@@ -381,8 +447,12 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             for (int i = wb + tid; i < we; i += kConsumers) {
                 const int c = __ldg(p.waits + 2 * i);
                 const uint32_t need = (uint32_t)__ldg(p.waits + 2 * i + 1);
-                while (ld_acquire(p.counters + c) < need) __nanosleep(20);
+                wait_count<PEER>(p.counters + c, PEER ? need * p.epoch : need, p, (uint32_t)c);
             }
+            // peer data of epoch e lands in the peers' work half e & 1, which peer q last read
+            // in epoch e - 2: wait until q has finished it (almost always long done)
+            if (peer_op && tid < p.world && tid != p.rank && p.epoch > 2)
+                wait_count<true>(p.done + tid, p.epoch - 2, p, 0x80000000u | tid);
         }
         consumer_sync();
         if (prof) {
@@ -669,7 +739,10 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             const int buf = R.bf & 0xFF, flags = R.bf >> 8;
             double2* dp = (buf == kBufW ? p.w : p.work) + R.off + (pos - R.dst);
             const double2 v = outv[pos];
-            if (flags & 2) {  // fp64 red.add into the pre-zeroed output (<= 2 addends per entry)
+            if (PEER && (flags & kRunPeer)) {  // y/u of this rank: every rank gets a copy
+                const int64_t o = R.off + (pos - R.dst);
+                for (int q = 0; q < p.world; ++q) __stcg(p.peer_work[q] + o, v);
+            } else if (flags & 2) {  // fp64 red.add into the pre-zeroed output (<= 2 addends per entry)
                 atomicAdd(&dp->x, v.x);
                 atomicAdd(&dp->y, v.y);
             } else if (flags & 1) {
@@ -683,10 +756,20 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         consumer_sync();  // all outputs issued; the slot is no longer read
         if (lane == 0) mbar_arrive(&opempty[q]);
         if (tid == 0 && !p.skip_waits && se > sb) {
-            // red.release.gpu orders every output store of the CTA before the signal: the
-            // stores happen-before this thread's release through the bar.sync above
-            // (release cumulativity), so no separate fence is needed
-            signal_counters(p.counters, p.sigs, sb, se);
+            if (peer_op) {  // (the slot may already hold another op: flag read at op start)
+                // the CTA's local and peer stores precede the system-scope fence through the
+                // bar.sync above; then one relaxed add per counter and rank
+                asm volatile("fence.acq_rel.sys;" ::: "memory");
+                for (int i = sb; i < se; ++i) {
+                    const int c = __ldg(p.sigs + i);
+                    for (int q = 0; q < p.world; ++q) red_relaxed_add_sys(p.peer_counters[q] + c, 1u);
+                }
+            } else {
+                // red.release.gpu orders every output store of the CTA before the signal: the
+                // stores happen-before this thread's release through the bar.sync above
+                // (release cumulativity), so no separate fence is needed
+                signal_counters(p.counters, p.sigs, sb, se);
+            }
         }
         if (++q == kOpSlots) {
             q = 0;
@@ -696,8 +779,8 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     }
 }
 
-template <bool PROF>
-__global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
+template <bool PROF, bool PEER>
+__device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.stage_bytes, p.xin_max, p.out_max);
     unsigned char* stages = smem + L.stage_off;
@@ -727,25 +810,47 @@ __global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
     if (warp == kConsumerWarps) {
         producer<PROF>(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer<PROF>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
+        consumer<PROF, PEER>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch
+    // (peer programs keep their counters: monotonic, every wait scaled by the epoch)
     if (threadIdx.x == 0) {
         __threadfence();
         const uint32_t prev = atomicAdd(p.exit_count, 1u);
-        flag[0] = (prev == gridDim.x - 1) ? 1 : 0;
+        flag[0] = (prev == (uint32_t)n_ctas - 1) ? 1 : 0;
     }
     __syncthreads();
     if (flag[0]) {
         __threadfence();
-        for (int i = threadIdx.x; i < p.n_counters; i += kThreads) p.counters[i] = 0u;
+        if (!PEER)
+            for (int i = threadIdx.x; i < p.n_counters; i += kThreads) p.counters[i] = 0u;
         if (threadIdx.x == 0) {
             *p.ticket = 0ull;
             *p.exit_count = 0u;
         }
         __threadfence();
+        if (PEER && threadIdx.x == 0) {
+            // every CTA of this rank is done with the epoch's work half: tell every rank
+            __threadfence_system();
+            for (int q = 0; q < p.world; ++q) st_release_sys(p.peer_done[q] + p.rank, p.epoch);
+        }
     }
+    (void)cta;
+}
+
+template <bool PROF>
+__global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
+    run_cta<PROF, false>(p, blockIdx.x, gridDim.x);
+}
+
+// Peer-exchange programs: L.nranks ranks share the grid (n = 1 on a real multi-GPU rank).
+__global__ void __maxnreg__(128) uhmv_bulk_peer_kernel(const __grid_constant__ PeerLaunch L) {
+    const int n = L.nranks;
+    const int r = (int)(((long long)blockIdx.x * n) / gridDim.x);
+    const int lo = (int)(((long long)r * gridDim.x + n - 1) / n);
+    const int hi = (int)(((long long)(r + 1) * gridDim.x + n - 1) / n);
+    run_cta<false, true>(L.r[r], blockIdx.x - lo, hi - lo);
 }
 
 }  // namespace bulk

@@ -91,9 +91,10 @@ class _DeviceProgram:
 class DeviceOperator:
     """A packed uniform H-matrix resident in HBM, with its C-ABI plan."""
 
-    def __init__(self, packed: PackedOperator, device=None, programs=None, share_with=None):
+    def __init__(self, packed: PackedOperator, device=None, programs=None, share_with=None, share_arena_with=None):
         """``programs=(fwd, adj)`` overrides the packed programs; ``share_with`` reuses another
-        DeviceOperator's arena / work / counter buffers (multi-GPU launch B)."""
+        DeviceOperator's arena / work / counter buffers (multi-GPU launch B);
+        ``share_arena_with`` reuses only its arena (the ranks of a peer-exchange emulation)."""
         torch = _torch()
         L = _lib.lib()
         self.torch = torch
@@ -117,9 +118,15 @@ class DeviceOperator:
         else:
             # padded by the largest leading dimension: TMA rows of the last matrix may overhang
             pad = max([int(q.mr_lds.max()) for q in (fwd_p, adj_p) if q.mr_lds is not None and len(q.mr_lds)] + [0])
-            self._arena_pad = pad
-            self.arena = torch.zeros(len(packed.arena) + pad + 16, dtype=torch.complex128, device=dev)
-            self.arena[: len(packed.arena)].copy_(torch.from_numpy(packed.arena))
+            if share_arena_with is not None:
+                if share_arena_with._arena_pad < pad or share_arena_with.packed.arena.shape != packed.arena.shape:
+                    raise ValueError("arena layouts differ")
+                self._arena_pad = share_arena_with._arena_pad
+                self.arena = share_arena_with.arena
+            else:
+                self._arena_pad = pad
+                self.arena = torch.zeros(len(packed.arena) + pad + 16, dtype=torch.complex128, device=dev)
+                self.arena[: len(packed.arena)].copy_(torch.from_numpy(packed.arena))
             self.work = torch.zeros(packed.work_len, dtype=torch.complex128, device=dev)
             n_ctr = max(packed.fwd.n_counters, packed.adj.n_counters, 1)
             self.counters = torch.zeros(n_ctr, dtype=torch.int32, device=dev)

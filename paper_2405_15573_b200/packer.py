@@ -52,6 +52,9 @@ WIDE_COLS = 288  # an op whose N segments all have rows this long (<= 4 rows per
 BUF_ARENA, BUF_WORK, BUF_X, BUF_W = 0, 1, 2, 3
 RUN_ADD = 1  # out run: read-modify-write add (single writer)
 RUN_ATOMIC = 2  # out run: fp64 red.add -- w is zeroed first; <= 2 addends per entry
+RUN_PEER = 4  # out run (peer-exchange programs): y/u data also stored into every peer's work
+OP_PEER = 16  # op field 12 flag (peer-exchange programs): the op writes peer data and
+#               signals its counters on every rank (kind = field 12 & 7)
 
 OP_FIELDS = 16  # int32 per op
 # op layout: n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, wait_b, wait_e,
@@ -114,6 +117,8 @@ class Program:
     mr_segs: np.ndarray | None = None  # (n, MR_FIELDS) int64: multi-RHS segments, one input source each
     mr_ranges: np.ndarray | None = None  # (n_ops, 3) int32: mr_segs range + MR_ZERO flag of every op
     mr_lds: np.ndarray | None = None  # int64 leading dimensions the mr segments read (one TMA map each)
+    peer: bool = False  # multi-GPU peer-exchange program: ONE launch per rank, y/u stored into
+    #                     the peers' work buffers and counters signalled across ranks (RUN_PEER)
 
     @property
     def n_ops(self) -> int:
@@ -141,6 +146,28 @@ class PackedOperator:
     geo: dict | None = field(default=None, repr=False)  # index structure, for re-chunked programs
     build_kw: dict | None = field(default=None, repr=False)
     rechunked: dict = field(default_factory=dict, repr=False)  # (rows, far_rows) -> (fwd, adj, work_len)
+
+    def for_rank(self, rank: int, world: int, peer: bool = False) -> "PackedOperator":
+        """The same arena with the programs of one rank of a ``world``-way partition (what
+        ``pack(u, rank=, world=, peer=)`` returns, without re-copying the slabs)."""
+        import dataclasses
+
+        if self.geo is None:
+            raise ValueError("re-partitioning needs the pack's index structure")
+        bct = self.geo["bct"]
+        part = None
+        if world > 1:
+            rb = partition_bounds(bct.row_tree, world)
+            cb = rb if bct.col_tree is bct.row_tree else partition_bounds(bct.col_tree, world)
+            part = dict(rank=rank, world=world, row_bounds=rb, col_bounds=cb)
+        kw = dict(self.build_kw, part=part, peer=bool(peer and world > 1))
+        fwd, work_f, ex_f = _build_program(self.geo, adjoint=False, **kw)
+        adj, work_a, ex_a = _build_program(self.geo, adjoint=True, **kw)
+        _assign_tmaps([fwd, adj] + [q.part_b for q in (fwd, adj) if q.part_b is not None])
+        return dataclasses.replace(
+            self, fwd=fwd, adj=adj, work_len=max(work_f, work_a, 1), rank=rank, world=world, part=part,
+            exchange={"fwd": ex_f, "adj": ex_a}, build_kw=kw, rechunked={},
+        )
 
     def programs(self, *, rows_per_chunk: int, far_rows: int):
         """(fwd, adj, work_len): the same operator and arena with NEAR / FAR ops re-chunked
@@ -253,6 +280,7 @@ def pack(
     rank: int = 0,
     world: int = 1,
     stage_elems: int | None = None,
+    peer: bool = False,
 ) -> PackedOperator:
     """Pack a UniformHMatrix (reference object or mirror) into arena + programs.
 
@@ -262,7 +290,13 @@ def pack(
     NEAR/FAR for its output rows and Z for every output cluster touching its rows.  y/u live
     in an exchange region of the work buffer, one block per rank padded to ``ex_len``, filled
     for everyone by one in-place all-gather between launch A (P1, RED, U, NEAR) and launch B
-    (Z, NEAR, FAR)."""
+    (Z, NEAR, FAR).
+
+    ``peer=True`` (world > 1): ONE program per rank and direction instead of the A / B pair.
+    The producers of this rank's y/u (P1 of single-chunk clusters, RED, U) also store them into
+    every peer's exchange region (RUN_PEER) and signal their counters on every rank (OP_PEER);
+    Z ops wait on remote counters with the owner's producer count.  The exchange rides the
+    NVLink peer mappings inside the one kernel (csrc/uhmv_bulk.cuh, PEER)."""
     import os
 
     if rows_per_chunk is None:
@@ -421,7 +455,7 @@ def pack(
         near_interleave = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE"].split(","))
     split["far_rows"] = int(os.environ.get("UHMV_FAR_ROWS", FAR_ROWS))
     kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems,
-              split=split)
+              split=split, peer=bool(peer and world > 1))
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
     adj, work_a, ex_a = _build_program(geo, adjoint=True, **kw)
     _assign_tmaps([fwd, adj] + [q.part_b for q in (fwd, adj) if q.part_b is not None])
@@ -481,9 +515,11 @@ def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
 
 
 def _build_program(
-    geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS, split=None
+    geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS, split=None,
+    peer=False,
 ):
     split = dict(SPLIT_DEFAULTS, **(split or {}))
+    peer = bool(peer and part is not None)
     bct = geo["bct"]
     offs = geo["offs"]
     fcols, ycols = geo["fcols"], geo["ycols"]
@@ -674,9 +710,24 @@ def _build_program(
         ops[KIND_RED].append(
             (KIND_RED, 0, lt, [], segs, [(BUF_WORK, y_off[t], lt, 0, 0)], [(c_part[t], nchunk)], [c_y[t]], nchunk * lt)
         )
+    # peer exchange: waits on counters another rank signals carry that owner's producer
+    # count (every rank derives it from the same structure: P1 chunks under t, U panels)
+    remote_ctr = set()
+    n_chunks_all = {}
+    if peer:
+        for t in in_map:
+            a_, b_ = in_span[t]
+            n_chunks_all[t] = sum(
+                len(_chunks(in_nodes[in_leaves[q]].lo, in_nodes[in_leaves[q]].hi, P1_CHUNK)) for q in range(a_, b_)
+            )
+            if owner_in(t) == rank and in_rank[t]:
+                assert n_chunks_all[t] == len(chunks_of[t])
     y_wait = {}
     for t in in_map:
-        if in_rank[t] == 0 or owner_in(t) != rank:
+        if in_rank[t] and owner_in(t) != rank and peer:
+            y_wait[t] = [(c_part[t], 1)] if n_chunks_all[t] <= 1 else [(c_y[t], 1)]
+            remote_ctr.add(y_wait[t][0][0])
+        elif in_rank[t] == 0 or owner_in(t) != rank:
             y_wait[t] = []  # zero-width, or produced by another rank (ordered by the exchange)
         elif len(chunks_of[t]) <= 1:
             y_wait[t] = [(c_part[t], len(chunks_of[t]))]
@@ -688,7 +739,12 @@ def _build_program(
     for t in in_map:
         n, lt = u_len[t], in_rank[t]
         u_wait[t] = []
-        if (n == 0 and not (adjoint and geo["cwidth"][t])) or lt == 0 or owner_in(t) != rank:
+        if (n == 0 and not (adjoint and geo["cwidth"][t])) or lt == 0:
+            continue
+        if owner_in(t) != rank:
+            if peer:  # the owner's U panels of t, signalled across ranks
+                u_wait[t] = [(c_u[t], len(_chunks(0, geo["cwidth"][t] if adjoint else n, split["u_cols"])))]
+                remote_ctr.add(c_u[t])
             continue
         u_wait[t] = [(c_u[t], 1)]
         if not adjoint:
@@ -818,7 +874,8 @@ def _build_program(
                 producers[c] = producers.get(c, 0) + 1
     for k in ops:
         ops[k] = [
-            o[:6] + ([(c, producers.get(c, 0)) for c, _n in o[6]],) + o[7:] for o in ops[k]
+            o[:6] + ([(c, producers.get(c, _n if c in remote_ctr else 0)) for c, _n in o[6]],) + o[7:]
+            for o in ops[k]
         ]
     # ---- order: largest first inside each kind (reference uniform.py:505-506) ----
     for k in ops:
@@ -834,14 +891,15 @@ def _build_program(
     phased = [ops[KIND_P1] + near]
     phased += [ops[k] for k in (KIND_RED, KIND_U, KIND_Z, KIND_FAR)]
     ex = (0, ex_len)
-    if world == 1:
+    if world == 1 or peer:
         # fused persistent order: every op waits only on ops that come earlier; nearfield ops
         # (no dependencies) are spread between the dependent farfield phases to cover latency
         fused = (
             ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
             + ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
         )
-        return _finish(phased, fused, n_ctr, stage_elems=stage_elems), work, ex
+        prog = _finish(phased, fused, n_ctr, stage_elems=stage_elems, peer_limit=world * ex_len if peer else None)
+        return prog, work, ex
     # multi-GPU: launch A produces this rank's y/u (+ nearfield), the exchange fills every
     # rank's y/u, launch B consumes them.  Waits on ops outside a launch are dropped: they are
     # ordered by the launch boundary and the all-gather.
@@ -1027,10 +1085,12 @@ def _mr_groups(mr, n_out):
     return out, (0 if covered.all() else MR_ZERO)
 
 
-def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
+def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, peer_limit=None):
     """Flatten op tuples into arrays in the phased order; the fused order is a
     permutation (``fused_order[ticket] = op index``).  ``keep_waits_on``: in a partial program
-    keep only waits on counters signalled by ops of this kind inside the program."""
+    keep only waits on counters signalled by ops of this kind inside the program.
+    ``peer_limit``: peer-exchange program -- work outputs below this offset (the y/u exchange
+    region) are RUN_PEER runs and their ops are flagged OP_PEER."""
     order = [o for ph in phased for o in ph]
     bounds = []
     a = 0
@@ -1058,6 +1118,16 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
         has_x = any(r[0] == BUF_X for r in in_runs)
         has_w = any(r[0] == BUF_WORK for r in in_runs)
         assert not (has_x and has_w), "an op reads x or work inputs, never both"
+        op_flags = 0
+        if peer_limit is not None:
+            marked = []
+            for buf, off, ln, dst, fl in out_runs:
+                if buf == BUF_WORK and off < peer_limit:
+                    assert off + ln <= peer_limit and not fl & (RUN_ADD | RUN_ATOMIC)
+                    fl |= RUN_PEER
+                    op_flags = OP_PEER
+                marked.append((buf, off, ln, dst, fl))
+            out_runs = marked
         in_b = len(runs)
         runs.extend(in_runs)
         in_e = len(runs)
@@ -1089,7 +1159,8 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
         sigs.extend(sgn)
         s_e = len(sigs)
         xin_len = 0 if has_x else n_in  # x windows travel in the stages (bulk kernel)
-        ops[i] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind, pc_b, pc_e, xin_len)
+        ops[i] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind | op_flags, pc_b, pc_e,
+                  xin_len)
         in_max = max(in_max, n_in)
         xin_max = max(xin_max, xin_len)
         out_max = max(out_max, n_out)
@@ -1106,7 +1177,8 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS):
         xin_max=xin_max,
         out_max=out_max,
         n_counters=n_ctr,
-        kinds=ops[:, 12].copy(),
+        kinds=ops[:, 12] & 7,
+        peer=peer_limit is not None,
         arena_elems=arena_elems,
         stage_elems=stage_elems,
         mr_segs=np.asarray(mr_segs, dtype=np.int64).reshape(-1, MR_FIELDS),

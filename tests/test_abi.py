@@ -23,7 +23,7 @@ def test_library_exports_all_header_symbols():
     L = ensure_built()
     for s in header_symbols():
         assert hasattr(L, s), s
-    assert L.uhmv_abi_version() == 7
+    assert L.uhmv_abi_version() == 8
     assert L.uhmv_last_error() == b""
 
 
@@ -51,3 +51,17 @@ def test_plan_create_rejects_bad_descriptor():
     assert L.uhmv_plan_create(None, ctypes.byref(h)) == -1
     assert L.uhmv_execute(None, None, None, 0, 0, None) == -1
     assert L.uhmv_plan_destroy(None) == 0
+
+
+def test_execute_peer_rejects_bad_arguments():
+    from paper_2405_15573_b200 import _lib
+
+    L = ensure_built()
+    ranks = (_lib.UhmvPeerRank * 2)()
+    plans = (ctypes.c_void_p * 1)(None)
+    ws = (ctypes.c_void_p * 1)(None)
+    assert L.uhmv_execute_peer(None, 1, 0, 2, ranks, None, ws, 0, 1, None) == -1
+    assert L.uhmv_execute_peer(plans, 1, 0, 9, ranks, ctypes.c_void_p(16), ws, 0, 1, None) == -1
+    assert b"rank range" in L.uhmv_last_error()
+    assert L.uhmv_execute_peer(plans, 1, 0, 2, ranks, ctypes.c_void_p(16), ws, 0, 0, None) == -1
+    assert b"epoch" in L.uhmv_last_error()
