@@ -173,8 +173,11 @@ class DistributedOperator:
         self.device = self.a.device
         self.n_rows, self.n_cols = packed.n_rows, packed.n_cols
         part = packed.part
-        self.row_slice = (part["row_bounds"][rank], part["row_bounds"][rank + 1])
-        self.col_slice = (part["col_bounds"][rank], part["col_bounds"][rank + 1])
+        if part is None:  # world 1
+            self.row_slice, self.col_slice = (0, self.n_rows), (0, self.n_cols)
+        else:
+            self.row_slice = (part["row_bounds"][rank], part["row_bounds"][rank + 1])
+            self.col_slice = (part["col_bounds"][rank], part["col_bounds"][rank + 1])
 
     def _setup_peer(self):
         """One symmetric-memory allocation per rank holds its peer-visible buffers: work (two
@@ -198,7 +201,11 @@ class DistributedOperator:
         self._symm_buf.zero_()
         torch.cuda.synchronize(dev)
         grp = self.group if self.group is not None else dist.group.WORLD
-        self._symm = symm.rendezvous(self._symm_buf, grp)
+        try:
+            self._symm = symm.rendezvous(self._symm_buf, grp.group_name)
+        except RuntimeError:  # older releases: symmetric memory is enabled per group first
+            symm.enable_symm_mem_for_group(grp.group_name)
+            self._symm = symm.rendezvous(self._symm_buf, grp.group_name)
         ptrs = list(self._symm.buffer_ptrs)
         self.ranks = {
             adjoint: [_peer_rank(ptrs[q] + b, work_lens[q], ptrs[q] + b + off_c, ptrs[q] + b + off_d)
@@ -261,6 +268,8 @@ class DistributedOperator:
         """All-gather the ranks' output slices into the full vector (padded blocks)."""
         import torch
 
+        if self.world == 1:
+            return w
         bounds = self.packed_local.part["col_bounds" if adjoint else "row_bounds"]
         lens = np.diff(bounds)
         blk = int(lens.max())

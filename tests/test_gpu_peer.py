@@ -67,3 +67,54 @@ def test_peer_emulation_config2(world):
         ref = one.matvec(x, adjoint=adjoint)
         w = em.matvec(x, adjoint=adjoint)
         assert (torch.linalg.norm(w - ref) / torch.linalg.norm(ref)).item() <= 1e-13
+
+
+def _symm_worker(name, q):
+    import sys
+
+    from conftest import GOLDEN, ROOT
+
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        from paper_2405_15573_b200.dist import DistributedOperator
+        from paper_2405_15573_b200.uh_io import load_uh
+
+        u, ex = load_uh(os.path.join(GOLDEN, f"{name}.npz"))
+        op = DistributedOperator(u, 0, 1, device=torch.device("cuda", 0), exchange="peer")
+        errs = []
+        for rep in range(3):
+            for adjoint, vk, rk in ((False, "vf_0", "ref_fwd_0"), (True, "va_0", "ref_adj_0")):
+                w = op.matvec_host(ex[vk], adjoint=adjoint)
+                errs.append(float(np.linalg.norm(w - ex[rk]) / np.linalg.norm(ex[rk])))
+        q.put(("ok", max(errs)))
+    except Exception as e:  # noqa: BLE001
+        q.put(("error", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_peer_exchange_symmetric_memory_single_rank():
+    """The real multi-GPU plumbing (NCCL group, torch symmetric-memory rendezvous, peer
+    pointer table, per-direction epochs) on the one GPU of the pool: world 1."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    pr = ctx.Process(target=_symm_worker, args=("helm400", q))
+    pr.start()
+    pr.join(timeout=300)
+    status, val = q.get(timeout=5)
+    assert status == "ok", val
+    assert val <= 1e-12
