@@ -310,7 +310,7 @@ def main():
         xh = torch.from_numpy(x.cpu().numpy()).pin_memory()
         wh = torch.empty(u.shape[1 if args.adjoint else 0], dtype=torch.complex128).pin_memory()
         xh_np, wh_np = xh.numpy(), wh.numpy()
-        for _ in range(3):
+        for _ in range(10):  # includes the host-I/O vs copy-path choice (4 calls each)
             op.matvec_host(xh_np, adjoint=args.adjoint, out=wh_np, mode=args.mode)
         k_e2e = max(10, min(args.steps, 200))
         if world > 1:
@@ -330,6 +330,11 @@ def main():
             "d2h_bytes_per_step": int(16 * (u.shape[1] if args.adjoint else u.shape[0])),
             "api": "uhmv_matvec_host (C ABI, pinned host x/w, H2D + kernels + D2H + sync, wall clock)",
         }
+        choice = op.host_io_choice(args.adjoint) if hasattr(op, "host_io_choice") else None
+        if choice is not None:
+            e2e["path"] = ("host-I/O launch: x read over PCIe by the P1 ops, finished output leaves drained "
+                           "to the pinned host buffer inside the kernel" if choice
+                           else "H2D copy + launch + D2H copy (faster than the host-I/O launch here)")
 
     peak, peak_kind = measured_peaks()
     alg_bytes_total = workloads.algorithmic_bytes(packed)

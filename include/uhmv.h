@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 8
+#define UHMV_ABI_VERSION 9
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -116,6 +116,15 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
  * Replaces: the whole matvec_uh call as a caller sees it (uniform.py:476-556). */
 int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
                      void* stream);
+
+/* Attach the host-I/O variant of the plan's programs (packer io_programs(); counters: a
+ * zeroed uint32 buffer of max(n_counters) of the two).  Afterwards uhmv_matvec_host with
+ * PINNED host buffers runs ONE bulk launch whose P1 ops read x over PCIe (publishing it to
+ * the device copy the NEAR ops read) and whose NEAR / FAR ops copy every finished output leaf
+ * to w_host as soon as its last contribution lands: the transfers overlap the kernel instead
+ * of bracketing it.  Pageable buffers keep the copy / launch / copy path.  A direction whose
+ * program has n_ops = 0 keeps the copy path; fwd = adj = NULL detaches. */
+int uhmv_plan_set_io(uhmv_plan* plan, const uhmv_program* fwd, const uhmv_program* adj, uint32_t* counters);
 
 /* Multi-RHS product on FP64 tensor cores (DMMA): W = A X or A^H X, X (n_in x nrhs), W
  * (n_out x nrhs) and work_mr (work_len x nrhs) device complex128, row-major, nrhs a

@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "UhmvPeerRank", "check", "LIB_PATH"
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 8
+ABI_VERSION = 9
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -85,6 +85,7 @@ EXPORTS = (
     "uhmv_execute_mrhs",
     "uhmv_execute_peer",
     "uhmv_peer_set_diag",
+    "uhmv_plan_set_io",
     "uhmv_plan_info",
     "uhmv_plan_set_profile",
     "uhmv_dmma_peak",
@@ -119,6 +120,8 @@ def lib():
     L.uhmv_execute_peer.restype = i32
     L.uhmv_peer_set_diag.argtypes = [vp, i32]
     L.uhmv_peer_set_diag.restype = i32
+    L.uhmv_plan_set_io.argtypes = [vp, ctypes.POINTER(UhmvProgram), ctypes.POINTER(UhmvProgram), vp]
+    L.uhmv_plan_set_io.restype = i32
     L.uhmv_matvec_host.restype = i32
     pi = ctypes.POINTER(i32)
     L.uhmv_plan_info.argtypes = [vp, i32, i32, pi, pi, pi, pi]

@@ -432,6 +432,15 @@ struct uhmv_plan {
     int smem[2];
     int bulk_grid[2];
     int bulk_full_grid[2];  // resident CTAs per SM x SMs (the peer launch splits it over ranks)
+    // host-I/O programs (uhmv_plan_set_io): x read from / w drained to pinned host buffers
+    bool has_io;
+    uhmv_program io[2];
+    uint32_t* io_counters;
+    int io_grid[2], io_smem[2], io_nstage[2];
+    const void* io_x_host;  // last mapped pointers (cudaPointerGetAttributes is ~1 us a call)
+    void* io_x_dev;
+    const void* io_w_host;
+    void* io_w_dev;
     int bulk_smem[2];
     int bulk_nstage[2];
     int sm_count;
@@ -501,6 +510,39 @@ static int encode_tmaps(const uhmv_desc* d, const uhmv_program& pr, const char* 
     }
     cudaError_t e = cudaMemcpy(pr.tmaps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(tensor maps)");
+    return UHMV_OK;
+}
+
+// Shared-memory stages, dynamic shared memory and persistent grid of the bulk engine for one
+// program (as many stages as fit with the requested CTAs per SM).
+static int size_bulk(int device, int sm_count, const uhmv_program* pr, int* nstage, int* smem, int* grid,
+                     int* full_grid) {
+    int smem_sm = 0, smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    int want_ctas = 3;
+    if (const char* ev = getenv("UHMV_BULK_CTAS")) want_ctas = atoi(ev) > 0 ? atoi(ev) : 3;
+    int want_stages = 0;
+    if (const char* ev = getenv("UHMV_NSTAGE")) want_stages = atoi(ev);
+    int budget = smem_sm / want_ctas - 1024;
+    if (budget > smem_optin) budget = smem_optin;
+    const int sbytes = (pr->stage_elems > 0 ? pr->stage_elems : 1408) * 16;
+    const int fixed = bulk::layout(0, sbytes, pr->xin_max, pr->out_max).total;
+    int ns = (budget - fixed) / sbytes;
+    if (want_stages > 0) ns = want_stages;
+    if (ns > 12) ns = 12;
+    if (ns < 2) ns = 2;
+    *nstage = ns;
+    *smem = bulk::layout(ns, sbytes, pr->xin_max, pr->out_max).total;
+    if (*smem > smem_optin) return fail(UHMV_EINVAL, "bulk engine shared memory exceeds the opt-in limit");
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk::uhmv_bulk_kernel<false>,
+                                                                  bulk::kThreads, *smem);
+    if (e != cudaSuccess) return cuda_fail(e, "occupancy(bulk)");
+    if (per_sm < 1) per_sm = 1;
+    *full_grid = per_sm * sm_count;
+    *grid = *full_grid;
+    if (*grid > pr->n_ops) *grid = pr->n_ops > 0 ? pr->n_ops : 1;
     return UHMV_OK;
 }
 
@@ -599,6 +641,9 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         e = cudaFuncSetAttribute(bulk::uhmv_bulk_peer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem_optin);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(bulk::uhmv_bulk_io_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_optin);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel<true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
     if (e != cudaSuccess) {
@@ -675,6 +720,9 @@ static bulk::Params make_bulk_params(const uhmv_plan* plan, const uhmv_program& 
     bp.skip_waits = plan->debug_skip_waits;
     bp.prof = plan->prof;
     bp.dbg = plan->debug_flags;
+    bp.x_host = nullptr;
+    bp.w_host = nullptr;
+    bp.diag = nullptr;
     return bp;
 }
 
@@ -772,6 +820,42 @@ int uhmv_peer_set_diag(void* host_mapped, int spin_log2) {
     g_peer_diag = static_cast<uint32_t*>(host_mapped);
     g_peer_spin_log2 = (spin_log2 >= 10 && spin_log2 <= 40) ? spin_log2 : 28;
     return UHMV_OK;
+}
+
+int uhmv_plan_set_io(uhmv_plan* plan, const uhmv_program* fwd, const uhmv_program* adj, uint32_t* counters) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_set_io: null plan");
+    if (!fwd && !adj) {  // detach
+        plan->has_io = false;
+        return UHMV_OK;
+    }
+    if (!fwd || !adj || !counters) return fail(UHMV_EINVAL, "uhmv_plan_set_io: null argument");
+    int rc = check_program(*fwd, "io fwd");
+    if (rc || (rc = check_program(*adj, "io adj"))) return rc;
+    cudaError_t e = cudaSetDevice(plan->d.device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    const uhmv_program* progs[2] = {fwd, adj};
+    for (int k = 0; k < 2; ++k) {
+        if (progs[k]->n_ops > 0 && !progs[k]->pieces) return fail(UHMV_EINVAL, "io program without pieces");
+        int full = 0;
+        if ((rc = size_bulk(plan->d.device, plan->sm_count, progs[k], &plan->io_nstage[k], &plan->io_smem[k],
+                            &plan->io_grid[k], &full)))
+            return rc;
+        plan->io[k] = *progs[k];
+    }
+    plan->io_counters = counters;
+    plan->has_io = true;
+    plan->io_x_host = plan->io_w_host = nullptr;
+    return UHMV_OK;
+}
+
+// Device pointer of a pinned (page-locked) host buffer, or null for pageable memory.
+static void* mapped_ptr(const void* host) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, host) != cudaSuccess) {
+        cudaGetLastError();  // clear the sticky-free error of an unregistered pointer
+        return nullptr;
+    }
+    return (a.type == cudaMemoryTypeHost && a.devicePointer) ? a.devicePointer : nullptr;
 }
 
 int uhmv_execute_peer(uhmv_plan* const* plans, int nplans, int rank0, int world,
@@ -897,6 +981,36 @@ int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjo
     const int64_t n_in = adjoint ? plan->d.n_rows : plan->d.n_cols;
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int k = adjoint ? 1 : 0;
+    if (plan->has_io && mode == UHMV_MODE_BULK && plan->io[k].n_ops > 0) {
+        // pinned host buffers: ONE launch reads x over PCIe (P1 ops) and drains finished
+        // output leaves to w_host as they complete -- no separate H2D / D2H copies
+        if (x_host != plan->io_x_host) {
+            plan->io_x_dev = mapped_ptr(x_host);
+            plan->io_x_host = x_host;
+        }
+        if (w_host != plan->io_w_host) {
+            plan->io_w_dev = mapped_ptr(w_host);
+            plan->io_w_host = w_host;
+        }
+        if (plan->io_x_dev && plan->io_w_dev) {
+            cudaError_t e0 = cudaMemsetAsync(plan->d.w_scratch, 0, (size_t)n_out * 16, st);
+            if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
+            const uhmv_program& pr = plan->io[k];
+            bulk::Params bp = make_bulk_params(plan, pr, k, plan->d.x_scratch, plan->d.w_scratch);
+            bp.nstage = plan->io_nstage[k];
+            bp.counters = plan->io_counters;
+            bp.prof = nullptr;
+            bp.x_host = static_cast<const double2*>(plan->io_x_dev);
+            bp.w_host = static_cast<double2*>(plan->io_w_dev);
+            bulk::uhmv_bulk_io_kernel<<<plan->io_grid[k], bulk::kThreads, plan->io_smem[k], st>>>(bp);
+            e0 = cudaGetLastError();
+            if (e0 != cudaSuccess) return cuda_fail(e0, "uhmv_bulk_kernel (host I/O) launch");
+            e0 = cudaStreamSynchronize(st);
+            if (e0 != cudaSuccess) return cuda_fail(e0, "uhmv_matvec_host synchronize");
+            return UHMV_OK;
+        }
+    }
     cudaError_t e = cudaMemcpyAsync(plan->d.x_scratch, x_host, (size_t)n_in * 16,
                                     cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");

@@ -36,6 +36,10 @@ constexpr int kOpSlots = 2;
 constexpr int kMaxRanks = 8;      // peer-exchange programs: ranks of one NVLink domain
 constexpr int kOpPeer = 16;       // op field 12 flag (packer.OP_PEER)
 constexpr int kRunPeer = 4;       // out-run flag (packer.RUN_PEER)
+// host-I/O programs (packer OP_XHOST / OP_XWAIT / OP_DRAIN, uhmv_matvec_host with pinned buffers)
+constexpr int kOpXHost = 32;  // P1: gather x from the host buffer, publish it to device x
+constexpr int kOpXWait = 64;  // NEAR: the producer waits for the op's x windows in device x
+constexpr int kOpDrain = 128; // NEAR/FAR: the last op of an output leaf copies w[leaf] to the host
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
 static_assert((kRowGroups & (kRowGroups - 1)) == 0 && (kConsumers & (kConsumers - 1)) == 0,
@@ -96,6 +100,8 @@ struct Params {
     uint32_t* peer_done[kMaxRanks];      // every rank's done-epoch array (world uint32 each)
     uint32_t* done;                      // this rank's done-epoch array: done[q] = last epoch q finished
     uint32_t* diag;     // optional host-mapped record of a timed-out wait (rank, what, value, need)
+    const double2* x_host;  // host-I/O programs: device-visible pointers of the pinned host x / w
+    double2* w_host;
     int32_t spin_log2;  // bounded spin of the peer waits: 2^spin_log2 polls, then trap
 };
 
@@ -244,7 +250,7 @@ __device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64
 // are reduced by shuffles at the flush.  (P = 4 up to 128 columns measured slower.)
 __device__ __forceinline__ int h_lanes(int cols) { return cols <= 32 ? 4 : (cols <= 64 ? 2 : 1); }
 
-template <bool PROF>
+template <bool PROF, bool IO>
 __device__ __forceinline__ void producer(const Params& p, unsigned char* stages, uint64_t* full,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
                                          OpSlot* slots) {
@@ -297,6 +303,18 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&opfull[q]);  // release: the slot writes above are visible
+        if (IO && op >= 0 && (__shfl_sync(0xffffffffu, hv, 12) & kOpXWait)) {
+            // host-I/O NEAR op: its x windows are published to device x by P1 ops (generic
+            // stores); wait for them, then order the bulk copies (async proxy) after the acquire
+            const int wb = __shfl_sync(0xffffffffu, hv, 8), we = __shfl_sync(0xffffffffu, hv, 9);
+            for (int i = wb + lane; i < we; i += 32) {
+                const int c = __ldg(p.waits + 2 * i);
+                const uint32_t need = (uint32_t)__ldg(p.waits + 2 * i + 1);
+                while (ld_acquire(p.counters + c) < need) __nanosleep(32);
+            }
+            __syncwarp();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
         if (++q == kOpSlots) {
             q = 0;
             qphase ^= 1u;
@@ -406,7 +424,7 @@ __device__ __forceinline__ int4 get_piece(const Params& p, const OpSlot* S, int 
                           __ldg(d + 7));
 }
 
-template <bool PROF, bool PEER>
+template <bool PROF, bool PEER, bool IO>
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
                                          double2* outv, uint64_t* full, uint64_t* empty,
                                          uint64_t* opfull, uint64_t* opempty, OpSlot* slots,
@@ -440,6 +458,8 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         const int pc_b = S->hdr[13], pc_e = S->hdr[14];
         const int kind = S->hdr[12] & 7;
         const bool peer_op = PEER && (S->hdr[12] & kOpPeer);  // (read while the slot is held)
+        const bool xhost = IO && (S->hdr[12] & kOpXHost) != 0;
+        const bool drain_op = IO && (S->hdr[12] & kOpDrain) != 0;
         const int n_in_runs = in_e - in_b;
         const int n_runs = out_e - in_b;
         if (!p.skip_waits) {  // every consumer thread polls one dependency counter in parallel
@@ -471,13 +491,18 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 if (pos < n_in) {
                     const RunRef R = get_run(p, S, in_b, find_run(p, S, in_b, 0, n_in_runs, pos));
                     const int64_t src = R.off + (pos - R.dst);
-                    v[k] = ((R.bf & 0xFF) == kBufX) ? __ldg(p.x + src) : __ldcg(p.work + src);
+                    if ((R.bf & 0xFF) != kBufX) v[k] = __ldcg(p.work + src);
+                    else v[k] = xhost ? __ldcg(p.x_host + src) : __ldg(p.x + src);  // host: over PCIe
                 }
             }
 #pragma unroll
             for (int k = 0; k < kGatherBatch; ++k) {
                 const int pos = base + tid + k * kConsumers;
-                if (pos < n_in) xin[pos] = v[k];
+                if (pos < n_in) {
+                    xin[pos] = v[k];
+                    // host-I/O P1 op: its one input run is x[a:b] -- publish it for the NEAR ops
+                    if (xhost) __stcg(const_cast<double2*>(p.x) + S->roff[0] + pos, v[k]);
+                }
             }
         }
         for (int i = tid; i < n_out; i += kConsumers) outv[i] = make_double2(0.0, 0.0);
@@ -771,6 +796,24 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 signal_counters(p.counters, p.sigs, sb, se);
             }
         }
+        if (drain_op) {
+            // host-I/O: count this op's contribution to its output leaf; the last one copies the
+            // finished w[leaf] to the host buffer (PCIe writes overlap the rest of the kernel)
+            int* dflag = reinterpret_cast<int*>(opempty + kOpSlots) + 1;
+            const int64_t* dr = p.runs + (int64_t)(in_b + n_runs) * kRunFields;
+            if (tid == 0) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");  // this CTA's w adds first
+                const uint32_t old = atomicAdd(p.counters + (int)__ldg(dr + 3), 1u);
+                const int last = (old + 1u == (uint32_t)__ldg(dr + 4));
+                if (last) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // every CTA's w adds
+                *dflag = last;
+            }
+            consumer_sync();
+            if (*dflag) {
+                const int64_t lo = __ldg(dr + 1), len = __ldg(dr + 2);
+                for (int64_t i = tid; i < len; i += kConsumers) __stcg(p.w_host + lo + i, __ldcg(p.w + lo + i));
+            }
+        }
         if (++q == kOpSlots) {
             q = 0;
             qphase ^= 1u;
@@ -779,7 +822,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     }
 }
 
-template <bool PROF, bool PEER>
+template <bool PROF, bool PEER, bool IO = false>
 __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.stage_bytes, p.xin_max, p.out_max);
@@ -808,9 +851,9 @@ __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
     __syncthreads();
     const int warp = threadIdx.x >> 5;
     if (warp == kConsumerWarps) {
-        producer<PROF>(p, stages, full, empty, opfull, opempty, slots);
+        producer<PROF, IO>(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer<PROF, PEER>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
+        consumer<PROF, PEER, IO>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch
@@ -842,6 +885,12 @@ __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
 template <bool PROF>
 __global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
     run_cta<PROF, false>(p, blockIdx.x, gridDim.x);
+}
+
+// Host-I/O programs (uhmv_matvec_host with pinned buffers): x gathered over PCIe by the P1
+// ops, finished output leaves drained to the host by their last NEAR / FAR op.
+__global__ void __maxnreg__(128) uhmv_bulk_io_kernel(const Params p) {
+    run_cta<false, false, true>(p, blockIdx.x, gridDim.x);
 }
 
 // Peer-exchange programs: L.nranks ranks share the grid (n = 1 on a real multi-GPU rank).

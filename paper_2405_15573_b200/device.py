@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import time
 
 import numpy as np
 
@@ -308,8 +309,50 @@ class DeviceOperator:
         )
         _lib.check(rc, "uhmv_execute_phases")
 
-    def matvec_host(self, x_host: np.ndarray, adjoint=False, out: np.ndarray | None = None, mode=None, stream=None):
-        """End-to-end C-ABI call with host buffers (H2D, kernels, D2H, sync)."""
+    def attach_io(self) -> bool:
+        """Build and upload the host-I/O programs (packer ``io_programs``) once: with them
+        ``matvec_host`` on pinned buffers can run ONE launch that reads x and writes w over
+        PCIe itself.  False when the operator has none (or this is a partitioned / re-chunked
+        plan)."""
+        if getattr(self, "_io", None) is not None:
+            return bool(self._io)
+        self._io = ()
+        p = self.packed
+        if p.world != 1 or self.progs != (p.fwd, p.adj) or os.environ.get("UHMV_HOST_IO", "1") == "0":
+            return False
+        fwd, adj = p.io_programs()
+        if fwd is None and adj is None:
+            return False
+        torch = self.torch
+        dev = [_DeviceProgram(torch, q, self.device) if q is not None else None for q in (fwd, adj)]
+        n_ctr = max([q.n_counters for q in (fwd, adj) if q is not None] + [1])
+        ctr = torch.zeros(n_ctr, dtype=torch.int32, device=self.device)
+        self._io = (dev, ctr, [d.struct() if d is not None else None for d in dev])
+        self._io_on = None
+        self._io_tune = {False: ([], []), True: ([], [])}  # per direction: (io times, copy times)
+        self._io_use = {}
+        return True
+
+    def _set_io(self, fwd_on: bool, adj_on: bool):
+        """Enable the host-I/O program of each direction (an empty program = copy path)."""
+        if self._io_on == (fwd_on, adj_on):
+            return
+        _dev, ctr, structs = self._io
+        sf = structs[0] if (fwd_on and structs[0] is not None) else _lib.UhmvProgram()
+        sa = structs[1] if (adj_on and structs[1] is not None) else _lib.UhmvProgram()
+        with self.torch.cuda.device(self.device):
+            _lib.check(_lib.lib().uhmv_plan_set_io(self._plan, ctypes.byref(sf), ctypes.byref(sa),
+                                                   ctypes.c_void_p(ctr.data_ptr())), "uhmv_plan_set_io")
+        self._io_on = (fwd_on, adj_on)
+
+    def matvec_host(self, x_host: np.ndarray, adjoint=False, out: np.ndarray | None = None, mode=None, stream=None,
+                    host_io=None):
+        """End-to-end C-ABI call with host buffers, then a stream synchronize.
+        Pinned buffers (e.g. ``tensor.pin_memory().numpy()``) can take the host-I/O launch (x read
+        and w written over PCIe inside the kernel, overlapping it); pageable ones always take
+        H2D copy, kernel, D2H copy.  ``host_io``: None = measure both on the first calls of each
+        direction and keep the faster (the host-I/O launch pays PCIe latency at the start of
+        the kernel, which loses on small operators), True / False = force."""
         p = self.packed
         n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
         if x_host.dtype != np.complex128 or not x_host.flags.c_contiguous:
@@ -322,7 +365,25 @@ class DeviceOperator:
             raise ValueError(f"out must be a contiguous complex128 array of shape ({n_out},)")
         mode = mode or default_mode()
         torch = self.torch
+        adjoint = bool(adjoint)
+        use, tuning = False, False
+        if mode == "bulk" and host_io is not False and self.attach_io() and self._io[2][int(adjoint)] is not None:
+            if host_io:
+                use = True
+            elif adjoint in self._io_use:
+                use = self._io_use[adjoint]
+            else:
+                t_io, t_cp = self._io_tune[adjoint]
+                use, tuning = len(t_io) <= len(t_cp), True
+            on = list(self._io_on or (False, False))
+            on[int(adjoint)] = use
+            self._set_io(*on)
+        elif getattr(self, "_io", None):
+            on = list(self._io_on or (False, False))
+            on[int(adjoint)] = False
+            self._set_io(*on)
         with self._lock:
+            t0 = time.perf_counter()
             # (the device switch costs ~10 us of host time per call: only when needed)
             if torch.cuda.current_device() == self.device.index:
                 rc = _lib.lib().uhmv_matvec_host(
@@ -335,8 +396,19 @@ class DeviceOperator:
                         self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
                         int(adjoint), _MODES[mode], self._stream(stream),
                     )
+            dt = time.perf_counter() - t0
         _lib.check(rc, "uhmv_matvec_host")
+        if tuning:
+            t_io, t_cp = self._io_tune[adjoint]
+            (t_io if use else t_cp).append(dt)
+            if len(t_io) >= 4 and len(t_cp) >= 4:  # first call of each is a warm-up
+                self._io_use[adjoint] = min(t_io[1:]) < min(t_cp[1:])
         return out
+
+    def host_io_choice(self, adjoint=False):
+        """Which path matvec_host settled on for pinned buffers: True host-I/O, False copy,
+        None not decided (or unavailable)."""
+        return getattr(self, "_io_use", {}).get(bool(adjoint))
 
     def close(self):
         mr = getattr(self, "_mr", None)

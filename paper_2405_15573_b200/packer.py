@@ -55,6 +55,12 @@ RUN_ATOMIC = 2  # out run: fp64 red.add -- w is zeroed first; <= 2 addends per e
 RUN_PEER = 4  # out run (peer-exchange programs): y/u data also stored into every peer's work
 OP_PEER = 16  # op field 12 flag (peer-exchange programs): the op writes peer data and
 #               signals its counters on every rank (kind = field 12 & 7)
+# host-I/O programs (uhmv_matvec_host with pinned buffers: x read and w written over PCIe
+# inside the kernel, no separate H2D / D2H copies)
+OP_XHOST = 32  # P1 op: gathers its x window from the host buffer and stores it into device x
+OP_XWAIT = 64  # NEAR op: its x windows come from device x -> the producer waits for them first
+OP_DRAIN = 128  # NEAR / FAR op: the last op finishing an output leaf copies w[leaf] to the host
+BUF_HOSTW = 4  # drain descriptor run (after the op's out runs): lo, len, counter, expected count
 
 OP_FIELDS = 16  # int32 per op
 # op layout: n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, wait_b, wait_e,
@@ -119,6 +125,7 @@ class Program:
     mr_lds: np.ndarray | None = None  # int64 leading dimensions the mr segments read (one TMA map each)
     peer: bool = False  # multi-GPU peer-exchange program: ONE launch per rank, y/u stored into
     #                     the peers' work buffers and counters signalled across ranks (RUN_PEER)
+    host_io: bool = False  # host-I/O program (OP_XHOST / OP_XWAIT / OP_DRAIN ops)
 
     @property
     def n_ops(self) -> int:
@@ -146,6 +153,23 @@ class PackedOperator:
     geo: dict | None = field(default=None, repr=False)  # index structure, for re-chunked programs
     build_kw: dict | None = field(default=None, repr=False)
     rechunked: dict = field(default_factory=dict, repr=False)  # (rows, far_rows) -> (fwd, adj, work_len)
+    io: tuple | None = field(default=None, repr=False)  # cached io_programs()
+
+    def io_programs(self):
+        """(fwd, adj) host-I/O programs of this single-GPU pack (``_build_program(host_io=True)``:
+        x read from / w drained to pinned host buffers inside the kernel), cached; (None, None)
+        when the operator's structure does not allow it (an input leaf without a P1 op, an
+        output leaf without NEAR / FAR ops)."""
+        if self.io is None:
+            if self.geo is None or self.world != 1:
+                self.io = (None, None)
+            else:
+                kw = dict(self.build_kw, host_io=True)
+                fwd, work_f, _ = _build_program(self.geo, adjoint=False, **kw)
+                adj, work_a, _ = _build_program(self.geo, adjoint=True, **kw)
+                assert max(work_f, work_a, 1) <= self.work_len
+                self.io = (fwd, adj)
+        return self.io
 
     def for_rank(self, rank: int, world: int, peer: bool = False) -> "PackedOperator":
         """The same arena with the programs of one rank of a ``world``-way partition (what
@@ -166,7 +190,7 @@ class PackedOperator:
         _assign_tmaps([fwd, adj] + [q.part_b for q in (fwd, adj) if q.part_b is not None])
         return dataclasses.replace(
             self, fwd=fwd, adj=adj, work_len=max(work_f, work_a, 1), rank=rank, world=world, part=part,
-            exchange={"fwd": ex_f, "adj": ex_a}, build_kw=kw, rechunked={},
+            exchange={"fwd": ex_f, "adj": ex_a}, build_kw=kw, rechunked={}, io=None,
         )
 
     def programs(self, *, rows_per_chunk: int, far_rows: int):
@@ -516,10 +540,16 @@ def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
 
 def _build_program(
     geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS, split=None,
-    peer=False,
+    peer=False, host_io=False,
 ):
+    """Returns (program, work length, exchange layout).  ``host_io``: the single-GPU variant
+    whose P1 ops read x from the caller's pinned host buffer (and publish it to device x for
+    the NEAR ops, which wait for it) and whose NEAR / FAR ops drain finished output leaves
+    to the host buffer; (None, ...) when some input leaf has no P1 op or some output leaf
+    no NEAR / FAR op (the caller then copies x and w around a plain launch)."""
     split = dict(SPLIT_DEFAULTS, **(split or {}))
     peer = bool(peer and part is not None)
+    host_io = bool(host_io and part is None)
     bct = geo["bct"]
     offs = geo["offs"]
     fcols, ycols = geo["fcols"], geo["ycols"]
@@ -608,6 +638,8 @@ def _build_program(
         n = in_nodes[leaf]
         for a, b in _chunks(n.lo, n.hi, P1_CHUNK):
             p1_items.append((p, a, b))
+    if host_io and {q for q, _a, _b in p1_items} != set(range(len(in_leaves))):
+        return None, 0, (0, 0)
     chunks_of = {t: [] for t in in_map}
     for idx, (p, a, b) in enumerate(p1_items):
         for t in in_anc[p]:
@@ -676,6 +708,9 @@ def _build_program(
     c_y = {t: ctr() for t in in_map}
     c_u = {t: ctr() for t in in_map}
     c_z = {s: ctr() for s in out_map}
+    in_pos = {leaf: q for q, leaf in enumerate(in_leaves)}
+    c_x = {q: ctr() for q in range(len(in_leaves))} if host_io else {}  # x[leaf] is in device x
+    c_w = {q: ctr() for q in range(len(out_leaves))} if host_io else {}  # contributions to w[leaf]
     ops = {k: [] for k in range(7)}
 
     # P1: partial_t = B_t[chunk rows]^H x[chunk]; the ancestors of a chunk are grouped into
@@ -699,8 +734,13 @@ def _build_program(
                 outs.append((BUF_WORK, part_off[t] + chunks_of[t].index(idx) * lt, lt, oo, 0))
                 sigs.append(c_part[t])
                 oo += lt
-            segs = stack_segs(in_stack_key, in_stacks, leaf, in_nodes[leaf].lo, a, b, grp, in_rank, MODE_H, a)
-            ops[KIND_P1].append((KIND_P1, b - a, oo, [(BUF_X, a, b - a, 0, 0)], segs, outs, [], sigs, (b - a) * oo))
+            segs = stack_segs(in_stack_key, in_stacks, leaf, in_nodes[leaf].lo, a, b, grp, in_rank, MODE_H,
+                              -1 if host_io else a)
+            kind = KIND_P1
+            if host_io:  # x[a:b] gathered from the host, published to device x
+                kind |= OP_XHOST
+                sigs.append(c_x[p])
+            ops[KIND_P1].append((kind, b - a, oo, [(BUF_X, a, b - a, 0, 0)], segs, outs, [], sigs, (b - a) * oo))
     # RED: y_t = sum of chunk partials (skipped when the single partial is y_t itself)
     for t in in_map:
         lt, nchunk = in_rank[t], len(chunks_of[t])
@@ -848,7 +888,13 @@ def _build_program(
                     segs.append(_seg(offs[("D", bid)], BUF_ARENA, r.size, n.size, n.size, MODE_H, pos, 0, r.lo))
                     pos += r.size
                     nbytes += r.size * n.size
-            ops[KIND_NEAR].append((KIND_NEAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], [], [], nbytes))
+            kind, waits_n, outs_n = KIND_NEAR, [], [(BUF_W, a, rows, 0, RUN_ATOMIC)]
+            if host_io:
+                kind |= OP_XWAIT | OP_DRAIN
+                leaves_in = sorted({in_pos[bct.nodes[bid].col if not adjoint else bct.nodes[bid].row] for bid in dlist})
+                waits_n = [(c_x[q], 0) for q in leaves_in]
+                outs_n.append((BUF_HOSTW, n.lo, n.size, c_w[p], 0))
+            ops[KIND_NEAR].append((kind, pos, rows, in_runs, segs, outs_n, waits_n, [], nbytes))
         anc = out_anc[p]
         if not anc:
             continue
@@ -862,9 +908,11 @@ def _build_program(
                 waits.append((c_z[s], 1))
                 pos += ls
             segs = stack_segs(out_stack_key, out_stacks, leaf, n.lo, a, b, anc, out_rank, MODE_N, -1)
-            ops[KIND_FAR].append(
-                (KIND_FAR, pos, rows, in_runs, segs, [(BUF_W, a, rows, 0, RUN_ATOMIC)], waits, [], rows * pos)
-            )
+            kind, outs_f = KIND_FAR, [(BUF_W, a, rows, 0, RUN_ATOMIC)]
+            if host_io:
+                kind |= OP_DRAIN
+                outs_f.append((BUF_HOSTW, n.lo, n.size, c_w[p], 0))
+            ops[KIND_FAR].append((kind, pos, rows, in_runs, segs, outs_f, waits, [], rows * pos))
 
     # ---- a wait means "every op signalling this counter is done": count the producers ----
     producers = {}
@@ -877,6 +925,20 @@ def _build_program(
             o[:6] + ([(c, producers.get(c, _n if c in remote_ctr else 0)) for c, _n in o[6]],) + o[7:]
             for o in ops[k]
         ]
+    if host_io:  # every output leaf drains once: its NEAR + FAR op count is the drain target
+        n_contrib = {}
+        for k in (KIND_NEAR, KIND_FAR):
+            for o in ops[k]:
+                for r in o[5]:
+                    if r[0] == BUF_HOSTW:
+                        n_contrib[r[3]] = n_contrib.get(r[3], 0) + 1
+        if set(n_contrib) != set(c_w.values()):
+            return None, 0, (0, 0)
+        for k in (KIND_NEAR, KIND_FAR):
+            ops[k] = [
+                o[:5] + ([r if r[0] != BUF_HOSTW else r[:4] + (n_contrib[r[3]],) for r in o[5]],) + o[6:]
+                for o in ops[k]
+            ]
     # ---- order: largest first inside each kind (reference uniform.py:505-506) ----
     for k in ops:
         ops[k].sort(key=lambda o: -o[-1])
@@ -1092,6 +1154,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
     ``peer_limit``: peer-exchange program -- work outputs below this offset (the y/u exchange
     region) are RUN_PEER runs and their ops are flagged OP_PEER."""
     order = [o for ph in phased for o in ph]
+    host_io = False
     bounds = []
     a = 0
     for ph in phased:
@@ -1128,12 +1191,16 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
                     op_flags = OP_PEER
                 marked.append((buf, off, ln, dst, fl))
             out_runs = marked
+        drain = [r for r in out_runs if r[0] == BUF_HOSTW]
+        out_runs = [r for r in out_runs if r[0] != BUF_HOSTW]
         in_b = len(runs)
         runs.extend(in_runs)
         in_e = len(runs)
         out_b = len(runs)
         runs.extend(out_runs)
         out_e = len(runs)
+        runs.extend(drain)  # read by OP_DRAIN ops at index out_e, outside the output cover
+        host_io = host_io or bool(kind & (OP_XHOST | OP_XWAIT | OP_DRAIN))
         ordered = _order_segments(sg)
         seg_b = len(segs)
         for s in ordered:
@@ -1158,7 +1225,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         s_b = len(sigs)
         sigs.extend(sgn)
         s_e = len(sigs)
-        xin_len = 0 if has_x else n_in  # x windows travel in the stages (bulk kernel)
+        xin_len = 0 if (has_x and not kind & OP_XHOST) else n_in  # x windows travel in the stages
         ops[i] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind | op_flags, pc_b, pc_e,
                   xin_len)
         in_max = max(in_max, n_in)
@@ -1179,6 +1246,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         n_counters=n_ctr,
         kinds=ops[:, 12] & 7,
         peer=peer_limit is not None,
+        host_io=host_io,
         arena_elems=arena_elems,
         stage_elems=stage_elems,
         mr_segs=np.asarray(mr_segs, dtype=np.int64).reshape(-1, MR_FIELDS),

@@ -23,7 +23,7 @@ def test_library_exports_all_header_symbols():
     L = ensure_built()
     for s in header_symbols():
         assert hasattr(L, s), s
-    assert L.uhmv_abi_version() == 8
+    assert L.uhmv_abi_version() == 9
     assert L.uhmv_last_error() == b""
 
 

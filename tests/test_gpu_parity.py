@@ -197,3 +197,31 @@ def test_loaded_packed_operator(golden, tmp_path):
         X = torch.stack([x, 2 * x], dim=1)
         W = dop.matmat(X, adjoint=adjoint).cpu().numpy()
         assert rel(W[:, 0], ex[rk]) <= TOL and rel(W[:, 1], 2 * ex[rk]) <= TOL
+
+
+@pytest.mark.parametrize("name", ["helm400", "ico2_helm_compress", "rect_sphere", "uh800_laplace", "two_cloud",
+                                  "degenerate", "no_admissible"])
+def test_host_io_pinned_buffers(name):
+    """uhmv_matvec_host with pinned buffers: the host-I/O launch (x over PCIe in the P1 ops,
+    finished output leaves drained to the host by their last NEAR / FAR op) vs the reference,
+    repeated (counters self-reset) and interleaved with the pageable path."""
+    import torch
+
+    from conftest import load_golden
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer import pack
+
+    u, ex = load_golden(name)
+    dop = DeviceOperator(pack(u), device="cuda:0")
+    for rep in range(3):
+        for adjoint, vk, rk in ((False, "vf_0", "ref_fwd_0"), (True, "va_0", "ref_adj_0")):
+            xv = np.asarray(ex[vk], dtype=np.complex128)
+            xh = torch.from_numpy(xv.copy()).pin_memory()
+            n_out = len(ex[rk])
+            wh = torch.full((n_out,), complex(np.nan, np.nan), dtype=torch.complex128).pin_memory()
+            for host_io in (True, None):
+                w = dop.matvec_host(xh.numpy(), adjoint=adjoint, out=wh.numpy(), host_io=host_io)
+                assert rel(w, ex[rk]) <= 1e-12, (name, adjoint, rep)
+            wp = dop.matvec_host(xv, adjoint=adjoint)  # pageable: copy path
+            assert rel(wp, ex[rk]) <= 1e-12
+    assert dop.attach_io() == any(q is not None for q in dop.packed.io_programs())
