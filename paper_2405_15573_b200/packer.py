@@ -942,6 +942,11 @@ def _build_program(
     # ---- order: largest first inside each kind (reference uniform.py:505-506) ----
     for k in ops:
         ops[k].sort(key=lambda o: -o[-1])
+    if host_io:
+        # x arrives over PCIe through the P1 ops: run them in tree order, and the NEAR ops
+        # (which wait for the x of their column leaves, mostly tree neighbours) likewise
+        ops[KIND_P1].sort(key=lambda o: o[3][0][1])
+        ops[KIND_NEAR].sort(key=lambda o: [r for r in o[5] if r[0] == BUF_W][0][1])
     near = ops[KIND_NEAR]
     f = np.cumsum([0.0] + list(near_interleave))
     f = f / f[-1]
