@@ -171,6 +171,11 @@ int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int*
  * producer waiting for a free stage / an op slot, ops, pieces. */
 int uhmv_plan_set_profile(uhmv_plan* plan, void* counters);
 
+/* Diagnostics: op timeline of the profiled bulk engine (with uhmv_plan_set_profile on):
+ * trace is a [n_ops][4] uint64 device buffer receiving {start, dependencies met, end, CTA} per
+ * op, times from %globaltimer in ns (NULL disables). */
+int uhmv_plan_set_trace(uhmv_plan* plan, void* trace);
+
 /* Diagnostics: measured FP64 tensor-core (DMMA m16n8k16) throughput of the device, TFLOP/s
  * (the roofline denominator of the multi-RHS product; MEASURED_PEAKS.json has no FP64 entry). */
 int uhmv_dmma_peak(int device, double* tflops);

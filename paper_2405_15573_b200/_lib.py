@@ -88,6 +88,7 @@ EXPORTS = (
     "uhmv_plan_set_io",
     "uhmv_plan_info",
     "uhmv_plan_set_profile",
+    "uhmv_plan_set_trace",
     "uhmv_dmma_peak",
     "uhmv_plan_destroy",
     "uhmv_last_error",
@@ -130,6 +131,8 @@ def lib():
     L.uhmv_dmma_peak.restype = i32
     L.uhmv_plan_set_profile.argtypes = [vp, vp]
     L.uhmv_plan_set_profile.restype = i32
+    L.uhmv_plan_set_trace.argtypes = [vp, vp]
+    L.uhmv_plan_set_trace.restype = i32
     L.uhmv_plan_destroy.argtypes = [vp]
     L.uhmv_plan_destroy.restype = i32
     L.uhmv_last_error.restype = ctypes.c_char_p

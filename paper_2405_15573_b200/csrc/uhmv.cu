@@ -446,6 +446,7 @@ struct uhmv_plan {
     int sm_count;
     int debug_skip_waits;  // diagnostics only (UHMV_DEBUG_SKIP_WAITS): results are wrong
     unsigned long long* prof;  // diagnostics only (uhmv_plan_set_profile)
+    unsigned long long* trace;  // diagnostics only (uhmv_plan_set_trace)
     int debug_flags;           // diagnostics only (UHMV_DEBUG_FLAGS): results are wrong
     int mrhs_grid;
     int mrtc_grid;
@@ -719,6 +720,7 @@ static bulk::Params make_bulk_params(const uhmv_plan* plan, const uhmv_program& 
     bp.out_max = pr.out_max;
     bp.skip_waits = plan->debug_skip_waits;
     bp.prof = plan->prof;
+    bp.trace = plan->prof ? plan->trace : nullptr;
     bp.dbg = plan->debug_flags;
     bp.x_host = nullptr;
     bp.w_host = nullptr;
@@ -1033,6 +1035,12 @@ int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int*
     if (smem_bytes) *smem_bytes = b ? plan->bulk_smem[k] : plan->smem[k];
     if (threads_per_cta) *threads_per_cta = b ? bulk::kThreads : kThreads;
     if (stages) *stages = b ? plan->bulk_nstage[k] : 0;
+    return UHMV_OK;
+}
+
+int uhmv_plan_set_trace(uhmv_plan* plan, void* trace) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_set_trace: null plan");
+    plan->trace = static_cast<unsigned long long*>(trace);
     return UHMV_OK;
 }
 

@@ -102,6 +102,7 @@ struct Params {
     uint32_t* diag;     // optional host-mapped record of a timed-out wait (rank, what, value, need)
     const double2* x_host;  // host-I/O programs: device-visible pointers of the pinned host x / w
     double2* w_host;
+    unsigned long long* trace;  // diagnostics (PROF kernels): per op {start, deps ready, end, cta} ns
     int32_t spin_log2;  // bounded spin of the peer waits: 2^spin_log2 polls, then trap
 };
 
@@ -228,6 +229,11 @@ __device__ __forceinline__ void signal_counters(uint32_t* counters, const int32_
     }
     asm volatile("fence.acq_rel.gpu;" ::: "memory");
     for (int i = b; i < e; ++i) red_relaxed_add(counters + __ldg(sigs + i), 1u);
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
@@ -452,6 +458,10 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             if (PROF && lane == 0) p.prof[(size_t)blockIdx.x * 64 + 58 + (tid >> 5)] = sprof[58 + (tid >> 5)];
             break;
         }
+        if (PROF && tid == 0 && p.trace) {
+            p.trace[(size_t)op * 4 + 0] = globaltimer_ns();
+            p.trace[(size_t)op * 4 + 3] = blockIdx.x;
+        }
         const int n_out = S->hdr[1];
         const int in_b = S->hdr[2], in_e = S->hdr[3];
         const int out_e = S->hdr[7];
@@ -480,6 +490,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             pr[kind * 8 + 1] += t1 - t0;
             t0 = t1;
             pr[kind * 8 + 5] += 1;
+            if (p.trace) p.trace[(size_t)op * 4 + 1] = globaltimer_ns();
         }
         // gather the input vector: all loads of a batch issued before any smem store
         const int n_in = (p.dbg & 2) ? 0 : S->hdr[15];  // work inputs only (x rides in stages)
@@ -732,11 +743,20 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     } else {
                         const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
                         int r = pp;
-                        for (; r + P < rows; r += 2 * P) {  // two independent chains
-                            cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
-                            cmac_conj(br, bi, tile[(r + P) * cols + j], xv[r + P]);
+                        double cr = 0.0, ci = 0.0, dr = 0.0, di = 0.0;
+                        for (; r + 3 * P < rows; r += 4 * P) {  // four independent chains
+                            const double2 m0 = tile[r * cols + j], m1 = tile[(r + P) * cols + j];
+                            const double2 m2 = tile[(r + 2 * P) * cols + j], m3 = tile[(r + 3 * P) * cols + j];
+                            cmac_conj(ar, ai, m0, xv[r]);
+                            cmac_conj(br, bi, m1, xv[r + P]);
+                            cmac_conj(cr, ci, m2, xv[r + 2 * P]);
+                            cmac_conj(dr, di, m3, xv[r + 3 * P]);
                         }
-                        if (r < rows) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
+                        for (; r < rows; r += P) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
+                        ar += cr;
+                        ai += ci;
+                        br += dr;
+                        bi += di;
                     }
                     accr[k] += ar + br;
                     acci[k] += ai + bi;
@@ -818,7 +838,10 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             q = 0;
             qphase ^= 1u;
         }
-        if (prof) pr[kind * 8 + 3] += clock64() - t0;
+        if (prof) {
+            pr[kind * 8 + 3] += clock64() - t0;
+            if (p.trace) p.trace[(size_t)op * 4 + 2] = globaltimer_ns();
+        }
     }
 }
 

@@ -206,6 +206,33 @@ class DeviceOperator:
                 out["kinds"][name] = dict(zip(cats, row))
         return out
 
+    def trace(self, adjoint=False, x=None):
+        """Diagnostics: one profiled bulk matvec with the op timeline on.  Returns a
+        (n_ops, 4) int64 array {start, dependencies met, end, CTA} per op (ns, %globaltimer,
+        relative to the first start) and the program's kinds."""
+        torch = self.torch
+        prog = self.progs[1] if adjoint else self.progs[0]
+        grid = self.launch_info(adjoint, "bulk")["grid"]
+        buf = torch.zeros((grid, 64), dtype=torch.int64, device=self.device)
+        tr = torch.zeros((max(prog.n_ops, 1), 4), dtype=torch.int64, device=self.device)
+        L = _lib.lib()
+        _lib.check(L.uhmv_plan_set_profile(self._plan, ctypes.c_void_p(buf.data_ptr())), "set_profile")
+        _lib.check(L.uhmv_plan_set_trace(self._plan, ctypes.c_void_p(tr.data_ptr())), "set_trace")
+        p = self.packed
+        n_in = p.n_rows if adjoint else p.n_cols
+        if x is None:
+            x = torch.ones(n_in, dtype=torch.complex128, device=self.device)
+        try:
+            self.matvec(x, adjoint=adjoint, mode="bulk")
+            torch.cuda.synchronize(self.device)
+        finally:
+            L.uhmv_plan_set_trace(self._plan, None)
+            L.uhmv_plan_set_profile(self._plan, None)
+        t = tr.cpu().numpy()
+        t0 = t[:, 0][t[:, 0] > 0].min()
+        t[:, :3] -= t0
+        return t, prog.kinds.copy()
+
     def profile_mr(self, R=64, adjoint=False):
         """Diagnostics: one multi-RHS block product with the staged engine's per-CTA cycle
         counters on (csrc/uhmv_mrtc.cuh), summed over CTAs."""
