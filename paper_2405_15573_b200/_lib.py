@@ -12,7 +12,7 @@ import os
 
 __all__ = ["lib", "UhmvProgram", "UhmvDesc", "UhmvPeerRank", "check", "LIB_PATH", "MAX_PHASES"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
+LIB_PATH = os.environ.get("UHMV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
 ABI_VERSION = 9
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2

@@ -743,20 +743,11 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     } else {
                         const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
                         int r = pp;
-                        double cr = 0.0, ci = 0.0, dr = 0.0, di = 0.0;
-                        for (; r + 3 * P < rows; r += 4 * P) {  // four independent chains
-                            const double2 m0 = tile[r * cols + j], m1 = tile[(r + P) * cols + j];
-                            const double2 m2 = tile[(r + 2 * P) * cols + j], m3 = tile[(r + 3 * P) * cols + j];
-                            cmac_conj(ar, ai, m0, xv[r]);
-                            cmac_conj(br, bi, m1, xv[r + P]);
-                            cmac_conj(cr, ci, m2, xv[r + 2 * P]);
-                            cmac_conj(dr, di, m3, xv[r + 3 * P]);
+                        for (; r + P < rows; r += 2 * P) {  // two independent chains
+                            cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
+                            cmac_conj(br, bi, tile[(r + P) * cols + j], xv[r + P]);
                         }
-                        for (; r < rows; r += P) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
-                        ar += cr;
-                        ai += ci;
-                        br += dr;
-                        bi += di;
+                        if (r < rows) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
                     }
                     accr[k] += ar + br;
                     acci[k] += ai + bi;

@@ -90,6 +90,7 @@ FAR_ROWS = 64  # output rows per FAR op (4 register slots of 16 row-groups)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_NCOLS_MAX = 640  # widest N piece row (two rows + x window still fit a stage)
+NW_COLS = int(__import__("os").environ.get("UHMV_NW_COLS", 640))  # widest panel of a warp-per-row op
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 # work splitting of the farfield chain ops across CTAs (output entries per op)
 SPLIT_DEFAULTS = {"p1_out": 1 << 30, "u_cols": 1 << 30, "z_rows": 1 << 30, "far_rows": ROWS_PER_CHUNK}
@@ -301,6 +302,7 @@ def pack(
     *,
     rows_per_chunk: int | None = None,
     near_interleave=(0.35, 0.1, 0.2, 0.35),
+    near_interleave_adj=(0.4, 0.15, 0.3, 0.15),
     rank: int = 0,
     world: int = 1,
     stage_elems: int | None = None,
@@ -477,9 +479,11 @@ def pack(
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in SPLIT_DEFAULTS.items()}
     if os.environ.get("UHMV_NEAR_INTERLEAVE"):
         near_interleave = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE"].split(","))
+    if os.environ.get("UHMV_NEAR_INTERLEAVE_ADJ"):
+        near_interleave_adj = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE_ADJ"].split(","))
     split["far_rows"] = int(os.environ.get("UHMV_FAR_ROWS", FAR_ROWS))
     kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems,
-              split=split, peer=bool(peer and world > 1))
+              split=split, peer=bool(peer and world > 1), near_interleave_adj=near_interleave_adj)
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
     adj, work_a, ex_a = _build_program(geo, adjoint=True, **kw)
     _assign_tmaps([fwd, adj] + [q.part_b for q in (fwd, adj) if q.part_b is not None])
@@ -540,7 +544,7 @@ def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
 
 def _build_program(
     geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS, split=None,
-    peer=False, host_io=False,
+    peer=False, host_io=False, near_interleave_adj=None,
 ):
     """Returns (program, work length, exchange layout).  ``host_io``: the single-GPU variant
     whose P1 ops read x from the caller's pinned host buffer (and publish it to device x for
@@ -550,6 +554,8 @@ def _build_program(
     split = dict(SPLIT_DEFAULTS, **(split or {}))
     peer = bool(peer and part is not None)
     host_io = bool(host_io and part is None)
+    if adjoint and near_interleave_adj is not None:
+        near_interleave = near_interleave_adj
     bct = geo["bct"]
     offs = geo["offs"]
     fcols, ycols = geo["fcols"], geo["ycols"]
@@ -1026,7 +1032,7 @@ def _order_segments(segs):
     return n + h
 
 
-def _pieces(segs, has_x, stage_elems=STAGE_ELEMS):
+def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX):
     """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages.
 
     Pieces whose input is a window of x (P1 and NEAR ops) carry that window inside the stage,
@@ -1050,8 +1056,8 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS):
         if mode != MODE_N and cols > min(BULK_HCOLS_MAX, stage_elems // 2):
             for c0, c1 in _chunks(0, cols, min(BULK_HCOLS_MAX, stage_elems // 2)):
                 split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off))
-        elif mode == MODE_N and cols > min(BULK_NCOLS_MAX, stage_elems // 2):  # rows wider than a stage
-            for c0, c1 in _chunks(0, cols, min(BULK_NCOLS_MAX, stage_elems // 2)):  # -> column panels
+        elif mode == MODE_N and cols > min(ncols_max, stage_elems // 2):  # rows wider than a stage
+            for c0, c1 in _chunks(0, cols, min(ncols_max, stage_elems // 2)):  # -> column panels
                 split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off + c0, out_off,
                               x_off + c0 if x_off >= 0 else x_off))
         else:
@@ -1212,9 +1218,11 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
             segs.extend(_panel_split(s))
         seg_e = len(segs)
         pc_b = len(pieces)
-        pcs = _pieces(ordered, has_x, stage_elems)
         nsg = [q for q in ordered if q[5] == MODE_N]
-        if nsg and all(q[3] >= WIDE_COLS for q in nsg):  # long rows: few per piece
+        wide = bool(nsg) and all(q[3] >= WIDE_COLS for q in nsg)
+        # warp-per-row ops: panels narrow enough that a stage holds a row for every warp
+        pcs = _pieces(ordered, has_x, stage_elems, NW_COLS if wide else BULK_NCOLS_MAX)
+        if wide:  # long rows: few per piece
             for pc in pcs:
                 if pc[4] == MODE_N:
                     pc[4] = MODE_NW
