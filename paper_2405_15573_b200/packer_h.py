@@ -74,8 +74,8 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
     # leaf, the rows of U_b likewise -- P1 and FAR of a leaf chunk read one long-row matrix
     cleaves, cspan = _leaves_under(bct.col_tree)
     rleaves, rspan = _leaves_under(bct.row_tree)
-    wstack = _block_stacks(cleaves, cspan, adm, kb, lambda b: bct.nodes[b].col)
-    ustack = _block_stacks(rleaves, rspan, adm, kb, lambda b: bct.nodes[b].row)
+    wstack = _block_stacks(cleaves, cspan, adm, kb, lambda b: bct.nodes[b].col, lambda c: cnodes[c].level)
+    ustack = _block_stacks(rleaves, rspan, adm, kb, lambda b: bct.nodes[b].row, lambda c: rnodes[c].level)
     for leaf, (w, _cols) in sorted(wstack.items()):
         alloc(("WS", leaf), cnodes[leaf].size * w, w)
     for leaf, (w, _cols) in sorted(ustack.items()):
@@ -116,7 +116,8 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
         dense_elems += d.size
     geo = dict(bct=bct, adm=adm, kb=kb, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
                wstack=wstack, ustack=ustack)
-    kw = dict(rows_per_chunk=rows_per_chunk, stage_elems=stage_elems, near_interleave=near_interleave)
+    kw = dict(rows_per_chunk=rows_per_chunk, stage_elems=stage_elems, near_interleave=near_interleave,
+              far_rows=int(os.environ.get("UHMV_FAR_ROWS_H", 64)))
     fwd, work_f = _build_h(geo, adjoint=False, **kw)
     adj, work_a = _build_h(geo, adjoint=True, **kw)
     _assign_tmaps([fwd, adj])
@@ -129,11 +130,12 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
     )
 
 
-def _block_stacks(leaves, span, adm, kb, clus):
-    """{leaf: (width, [(block, column offset)])}: blocks (in ``adm`` order) whose cluster
-    ``clus(b)`` contains the leaf."""
+def _block_stacks(leaves, span, adm, kb, clus, level):
+    """{leaf: (width, [(block, column offset)])}: blocks whose cluster ``clus(b)`` contains the
+    leaf, grouped by that cluster (root to leaf, blocks of one cluster in ``adm`` order) -- so
+    the per-cluster vectors of all its blocks are contiguous in every stack."""
     per = [[] for _ in leaves]
-    for b in adm:
+    for b in sorted(adm, key=lambda b: (level(clus(b)), clus(b), b)):
         a, e = span[clus(b)]
         for p in range(a, e):
             per[p].append(b)
@@ -148,7 +150,7 @@ def _block_stacks(leaves, span, adm, kb, clus):
     return out
 
 
-def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
+def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave, far_rows=64):
     bct, adm, kb, offs = geo["bct"], geo["adm"], geo["kb"], geo["offs"]
     if adjoint:
         in_tree, out_tree = bct.row_tree, bct.col_tree
@@ -200,10 +202,29 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
         n_ctr += 1
         return n_ctr - 1
 
-    # P1 items: (leafpos, lo, hi, block group)
+    # Per-cluster vectors: the blocks of an input cluster t (col(t) forward) are one group of
+    # adjacent stack columns, so P1 writes each multi-chunk t's partials as ONE run
+    # (part_base[t] + chunk * K_t) and RED sums them per cluster (one S op of nchunk x K_t);
+    # y is laid out grouped by OUTPUT cluster s, so a FAR op gathers one run per ancestor s.
+    in_groups, out_groups = {}, {}
+    for b in sorted(adm):
+        in_groups.setdefault(in_c(b), []).append(b)
+        out_groups.setdefault(out_c(b), []).append(b)
+    y_off = {}
+    for sc in sorted(out_groups, key=lambda c: (out_nodes[c].level, c)):
+        for b in out_groups[sc]:
+            y_off[b] = walloc(kb[b])
+    K = {t: sum(kb[b] for b in bl) for t, bl in in_groups.items()}
+    boff = {}  # block -> offset inside its input cluster's vector
+    for t, bl in in_groups.items():
+        o = 0
+        for b in bl:
+            boff[b] = o
+            o += kb[b]
+    # P1 items: (leafpos, lo, hi, block group); groups are runs of adjacent stack columns
     items = []
     for p, leaf in enumerate(in_leaves):
-        bl = in_blocks[p]
+        bl = [b for b, _c in in_stacks[leaf][1]] if leaf in in_stacks else []
         if not bl:
             continue
         n = in_nodes[leaf]
@@ -218,44 +239,55 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
         for a, e in _chunks(n.lo, n.hi, P1_CHUNK):
             for grp in groups:
                 items.append((p, a, e, grp))
-    chunks_of = {b: [] for b in adm}
-    for idx, (p, a, e, grp) in enumerate(items):
-        for b in grp:
-            chunks_of[b].append(idx)
-    y_off, part_off = {}, {}
-    for b in adm:
-        y_off[b] = walloc(kb[b])
-    for b in adm:
-        part_off[b] = y_off[b] if len(chunks_of[b]) == 1 else walloc(len(chunks_of[b]) * kb[b])
-    c_part = {b: ctr() for b in adm}
-    c_y = {b: ctr() for b in adm}
+    chunk_sets = {t: set() for t in in_groups}
+    for p, a, e, grp in items:
+        for t in {in_c(b) for b in grp}:
+            chunk_sets[t].add((a, e))
+    chunks = {t: sorted(cs) for t, cs in chunk_sets.items()}
+    chunk_idx = {t: {ae: i for i, ae in enumerate(cs)} for t, cs in chunks.items()}
+    part_base = {t: walloc(len(cs) * K[t]) for t, cs in sorted(chunks.items()) if len(cs) > 1}
+    c_part = {t: ctr() for t in in_groups}  # P1 ops touching t (its partials / its single-chunk y)
+    c_y = {t: ctr() for t in in_groups}  # RED of a multi-chunk t
+    n_touch = {t: 0 for t in in_groups}
     ops = {k: [] for k in range(7)}
     for idx, (p, a, e, grp) in enumerate(items):
         segs, outs, sigs = [], [], []
         oo = 0
         leaf = in_leaves[p]
         W, cols = in_stacks[leaf]
-        c0 = dict(cols)[grp[0]]  # a group is a run of adjacent stack columns
-        for b in grp:
-            k = kb[b]
-            outs.append((BUF_WORK, part_off[b] + chunks_of[b].index(idx) * k, k, oo, 0))
-            sigs.append(c_part[b])
-            oo += k
+        c0 = dict(cols)[grp[0]]
+        i = 0
+        while i < len(grp):  # one run per (cluster, partial row), or per block into y
+            t = in_c(grp[i])
+            j = i
+            while j < len(grp) and in_c(grp[j]) == t:
+                j += 1
+            if t in part_base:
+                k_run = sum(kb[b] for b in grp[i:j])
+                outs.append((BUF_WORK, part_base[t] + chunk_idx[t][(a, e)] * K[t] + boff[grp[i]], k_run, oo, 0))
+                oo += k_run
+            else:
+                for b in grp[i:j]:
+                    outs.append((BUF_WORK, y_off[b], kb[b], oo, 0))
+                    oo += kb[b]
+            sigs.append(c_part[t])
+            n_touch[t] += 1
+            i = j
         base = offs[(in_key, leaf)] + (a - in_nodes[leaf].lo) * W
         segs.append(_seg(base + c0, BUF_ARENA, e - a, oo, W, MODE_H, 0, 0, a))
         ops[KIND_P1].append((KIND_P1, e - a, oo, [(BUF_X, a, e - a, 0, 0)], segs, outs, [], sigs, (e - a) * oo))
     y_wait = {}
-    for b in adm:
-        nchunk = len(chunks_of[b])
-        if nchunk <= 1:
-            y_wait[b] = (c_part[b], nchunk)
+    for t, bl in in_groups.items():
+        if t not in part_base:
+            y_wait[t] = (c_part[t], n_touch[t])
             continue
-        k = kb[b]
+        nchunk = len(chunks[t])
+        outs = [(BUF_WORK, y_off[b], kb[b], boff[b], 0) for b in bl]
         ops[KIND_RED].append(
-            (KIND_RED, 0, k, [], [_seg(part_off[b], BUF_WORK, nchunk, k, k, MODE_S, 0, 0)],
-             [(BUF_WORK, y_off[b], k, 0, 0)], [(c_part[b], nchunk)], [c_y[b]], nchunk * k)
+            (KIND_RED, 0, K[t], [], [_seg(part_base[t], BUF_WORK, nchunk, K[t], K[t], MODE_S, 0, 0)],
+             outs, [(c_part[t], n_touch[t])], [c_y[t]], nchunk * K[t])
         )
-        y_wait[b] = (c_y[b], 1)
+        y_wait[t] = (c_y[t], 1)
     for p, leaf in enumerate(out_leaves):
         n = out_nodes[leaf]
         dlist = dense_by_outleaf.get(leaf, [])
@@ -283,15 +315,19 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave):
         bl = out_blocks[p]
         if not bl:
             continue
-        for a, e in _chunks(n.lo, n.hi, rows_per_chunk):
+        for a, e in _chunks(n.lo, n.hi, far_rows):  # each FAR op gathers the whole y stack once
             rows = e - a
             in_runs, segs, waits, pos = [], [], [], 0
-            for b in bl:
+            W, cols = out_stacks[leaf]
+            for b, _c in cols:  # stack order: grouped by output cluster, y grouped alike
                 k = kb[b]
-                in_runs.append((BUF_WORK, y_off[b], k, pos, 0))
-                waits.append(y_wait[b])
+                if in_runs and in_runs[-1][1] + in_runs[-1][2] == y_off[b]:
+                    r0 = in_runs[-1]
+                    in_runs[-1] = (r0[0], r0[1], r0[2] + k, r0[3], r0[4])
+                else:
+                    in_runs.append((BUF_WORK, y_off[b], k, pos, 0))
+                waits.append(y_wait[in_c(b)])
                 pos += k
-            W, _cols = out_stacks[leaf]
             assert W == pos
             segs.append(_seg(offs[(out_key, leaf)] + (a - n.lo) * W, BUF_ARENA, rows, W, W, MODE_N, 0, 0))
             ops[KIND_FAR].append(

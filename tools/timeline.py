@@ -1,5 +1,5 @@
 """Diagnostics: op timeline of one profiled bulk matvec (usage: python tools/timeline.py CFG
-[fwd|adj] [full|far|near]).  Prints, per op kind, when its ops start / get their
+[fwd|adj] [full|far|near] [uh|h]).  Prints, per op kind, when its ops start / get their
 dependencies / end, how long they wait for dependencies vs compute, and the kernel span;
 saves the raw timeline to gpurun_out/timeline_cfgN.npz."""
 import os
@@ -17,12 +17,18 @@ from paper_2405_15573_b200.packer import KIND_NAMES, pack
 cfg = int(sys.argv[1])
 adj = len(sys.argv) > 2 and sys.argv[2] == "adj"
 view = sys.argv[3] if len(sys.argv) > 3 else "full"
-u = workloads.build_operator(cfg)
+fmt = sys.argv[4] if len(sys.argv) > 4 else "uh"
+u = workloads.build_operator(cfg) if fmt == "uh" else workloads.build_h_operator(cfg)
 if view != "full":
     from matvec_oracle import farfield_only, nearfield_only
 
     u = farfield_only(u) if view == "far" else nearfield_only(u)
-op = DeviceOperator(pack(u), device="cuda:0")
+if fmt == "h":
+    from paper_2405_15573_b200.packer_h import pack_h
+
+    op = DeviceOperator(pack_h(u), device="cuda:0")
+else:
+    op = DeviceOperator(pack(u), device="cuda:0")
 x = torch.from_numpy(workloads.seeded_vector(u.shape[0] if adj else u.shape[1], 0)).cuda()
 for _ in range(3):
     op.matvec(x, adjoint=adj)
