@@ -1032,7 +1032,7 @@ def _order_segments(segs):
     return n + h
 
 
-def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX):
+def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_panel=BULK_HCOLS_MAX):
     """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages.
 
     Pieces whose input is a window of x (P1 and NEAR ops) carry that window inside the stage,
@@ -1053,8 +1053,8 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX):
     split = []
     for sg in segs:  # H/S groups own at most BULK_HCOLS_MAX output columns: cut wider ones
         m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off = sg
-        if mode != MODE_N and cols > min(BULK_HCOLS_MAX, stage_elems // 2):
-            for c0, c1 in _chunks(0, cols, min(BULK_HCOLS_MAX, stage_elems // 2)):
+        if mode != MODE_N and cols > min(h_panel, stage_elems // 2):
+            for c0, c1 in _chunks(0, cols, min(h_panel, stage_elems // 2)):
                 split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off))
         elif mode == MODE_N and cols > min(ncols_max, stage_elems // 2):  # rows wider than a stage
             for c0, c1 in _chunks(0, cols, min(ncols_max, stage_elems // 2)):  # -> column panels
@@ -1158,7 +1158,8 @@ def _mr_groups(mr, n_out):
     return out, (0 if covered.all() else MR_ZERO)
 
 
-def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, peer_limit=None):
+def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, peer_limit=None,
+            h_panel=BULK_HCOLS_MAX):
     """Flatten op tuples into arrays in the phased order; the fused order is a
     permutation (``fused_order[ticket] = op index``).  ``keep_waits_on``: in a partial program
     keep only waits on counters signalled by ops of this kind inside the program.
@@ -1221,7 +1222,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         nsg = [q for q in ordered if q[5] == MODE_N]
         wide = bool(nsg) and all(q[3] >= WIDE_COLS for q in nsg)
         # warp-per-row ops: panels narrow enough that a stage holds a row for every warp
-        pcs = _pieces(ordered, has_x, stage_elems, NW_COLS if wide else BULK_NCOLS_MAX)
+        pcs = _pieces(ordered, has_x, stage_elems, NW_COLS if wide else BULK_NCOLS_MAX, h_panel)
         if wide:  # long rows: few per piece
             for pc in pcs:
                 if pc[4] == MODE_N:

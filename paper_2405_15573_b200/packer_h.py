@@ -45,6 +45,7 @@ from .packer import (
 __all__ = ["pack_h"]
 
 P1_MAX_OUT = 512  # output entries per P1 op (bounds the consumers' shared-memory vector)
+H_PANEL = 256  # H/S column panel of the bulk pieces (config 3: 1.24 ms at 512, 1.15 ms at 256)
 
 
 def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = None,
@@ -344,4 +345,5 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave, far_
         parts.append([])
     phased = [ops[KIND_P1] + near, ops[KIND_RED], ops[KIND_FAR]]
     fused = ops[KIND_P1] + parts[0] + ops[KIND_RED] + parts[1] + parts[2] + parts[3] + ops[KIND_FAR]
-    return _finish(phased, fused, n_ctr, stage_elems=stage_elems), work
+    # 256-column H panels (more rows per stage) measured best for the wide per-block stacks
+    return _finish(phased, fused, n_ctr, stage_elems=stage_elems, h_panel=H_PANEL), work
