@@ -301,7 +301,7 @@ def pack(
     u,
     *,
     rows_per_chunk: int | None = None,
-    near_interleave=(0.35, 0.1, 0.2, 0.35),
+    near_interleave=None,
     near_interleave_adj=(0.4, 0.15, 0.3, 0.15),
     rank: int = 0,
     world: int = 1,
@@ -477,6 +477,11 @@ def pack(
     else:
         part = None
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in SPLIT_DEFAULTS.items()}
+    if near_interleave is None:
+        # forward nearfield shares between the farfield phases (measured): operators under
+        # ~1 GB are chain-latency-bound and want the chain started early (configs 1-2: -3..4%)
+        small = 16 * (bytes_bases + bytes_coupling + bytes_dense) < 1e9
+        near_interleave = (0.2, 0.1, 0.2, 0.5) if small else (0.35, 0.1, 0.2, 0.35)
     if os.environ.get("UHMV_NEAR_INTERLEAVE"):
         near_interleave = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE"].split(","))
     if os.environ.get("UHMV_NEAR_INTERLEAVE_ADJ"):
