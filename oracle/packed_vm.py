@@ -214,3 +214,64 @@ def vm_matmat(packed, V, adjoint=False, programs=None):
     for i in prog.fused_order.tolist():
         run_op_mr(prog, i, bufs, R)
     return W
+
+
+def run_peer_rank(pack, rank, world, work, counters, done, x, w, adjoint=False, epochs=1, lock=None,
+                  jitter=None, engine="pieces", timeout_s=60.0, scale=None):
+    """One rank of a peer-exchange partition, run CONCURRENTLY with the other ranks (each in
+    its own process) over shared memory -- the multi-process CPU model of the device protocol
+    (csrc/uhmv_bulk.cuh, PEER):
+      work[q]      every rank's work buffer, shape (2, work_len_q): epoch e uses half e & 1
+      counters[q]  every rank's dependency counters (monotonic: a wait for n needs n * e)
+      done[q]      every rank's done-epoch flags (done[q][r] = last epoch rank r finished)
+    The rank walks its fused ticket order, polling each op's waits (and, for OP_PEER ops,
+    done[rank][q] >= e - 2 for every peer q, so no store lands in a half a peer still reads);
+    RUN_PEER outputs go to every rank's current half; OP_PEER ops signal every rank's
+    counters (under ``lock``: the device uses atomics).  ``w`` receives this rank's rows.
+    ``scale(e)``: epoch e multiplies x by it (stale data of an earlier epoch then shows in
+    the result); returns the list of per-epoch outputs."""
+    outs = []
+    import time
+
+    prog = pack.adj if adjoint else pack.fwd
+    assert prog.peer
+
+    def wait_until(pred):
+        t0 = time.time()
+        while not pred():
+            if time.time() - t0 > timeout_s:
+                raise TimeoutError(f"rank {rank}: peer wait timed out")
+            time.sleep(0.0002)
+
+    for epoch in range(1, epochs + 1):
+        half = epoch & 1
+        w[:] = 0
+        xe = x * scale(epoch) if scale is not None else x
+        for i in prog.fused_order.tolist():
+            wb, we, sb, se = (int(q) for q in prog.ops[i, 8:12])
+            peer_op = bool(prog.ops[i, 12] & OP_PEER)
+            for c, cnt in prog.waits[wb:we]:
+                wait_until(lambda c=int(c), cnt=int(cnt): counters[rank][c] >= epoch * cnt)
+            if peer_op and epoch > 2:
+                for q in range(world):
+                    if q != rank:
+                        wait_until(lambda q=q: done[rank][q] >= epoch - 2)
+            if jitter is not None:
+                time.sleep(jitter.random() * 1e-4)
+            bufs = {BUF_ARENA: pack.arena, BUF_WORK: work[rank][half], BUF_X: xe, BUF_W: w}
+            run_op(prog, i, bufs, engine, peers=[work[q][half] for q in range(world) if q != rank])
+            targets = range(world) if peer_op else (rank,)
+            if se > sb:
+                if lock is not None:
+                    lock.acquire()
+                try:
+                    for c in prog.sigs[sb:se]:
+                        for q in targets:
+                            counters[q][int(c)] += 1
+                finally:
+                    if lock is not None:
+                        lock.release()
+        for q in range(world):
+            done[q][rank] = epoch
+        outs.append(w.copy())
+    return outs
