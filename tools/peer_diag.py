@@ -26,13 +26,16 @@ _lib.lib().uhmv_peer_set_diag(ctypes.c_void_p(diag.data_ptr()), int(os.environ.g
 out = torch.empty_like(ref)
 for i in range(n):
     mode = i % 3
+    sc = 1.0 + 0.37j * (i % 5)  # a different x each epoch: stale exchange data would show
+    xs = x * sc
+    ref = one.matvec(xs)
     t = time.time()
     if mode == 0:
-        w = em.matvec(x, out=out)
+        w = em.matvec(xs, out=out)
     elif mode == 1:
-        w = em.matvec(x.clone())
+        w = em.matvec(xs.clone())
     else:
-        w = torch.from_numpy(em.matvec_host(x.cpu().numpy())).cuda()
+        w = torch.from_numpy(em.matvec_host(xs.cpu().numpy())).cuda()
     try:
         torch.cuda.synchronize()
     except Exception as e:
