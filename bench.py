@@ -8,8 +8,10 @@ BASELINE config (default: config 3, N=81920 -- the config BASELINE.json quotes a
   python bench.py --impl reference ...   # the reference algorithm on the host CPU
 
 Under torchrun (N>1) every rank owns a contiguous slice of output leaves (row-cluster
-partition); the y/u coefficients are exchanged with one NCCL
-all-gather; time = max over ranks; value = whole-job matvecs/s.
+partition); the y/u coefficients are exchanged inside the one kernel per
+rank over NVLink peer mappings (``--exchange auto``: when every rank can map its peers and
+the first matvecs agree with the NCCL path; else one NCCL all-gather between two launches);
+time = max over ranks; value = whole-job matvecs/s.
 """
 
 from __future__ import annotations
@@ -41,7 +43,7 @@ def parse():
     ap.add_argument("--view", default="full", choices=["full", "far", "near"], help="diagnostics: parity view")
     ap.add_argument("--format", default="uh", choices=["uh", "h"],
                     help="uh: uniform H-matrix (the hot path); h: the source H-matrix (matvec_h)")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "peer"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer"],
                     help="multi-GPU y/u exchange: NCCL all-gather between two launches, or peer stores "
                          "over NVLink inside one launch per rank")
     ap.add_argument("--emulate-ranks", type=int, default=0,
@@ -185,8 +187,6 @@ def main():
         "adjoint": bool(args.adjoint),
         "parallelism": f"row-partition x{args.gpus}" if args.gpus > 1 else "single GPU",
     }
-    if args.gpus > 1:
-        config["exchange"] = args.exchange
     if args.emulate_ranks > 1:
         config["parallelism"] = (f"peer-exchange partition of {args.emulate_ranks} ranks emulated in one launch "
                                  f"on one GPU (1/{args.emulate_ranks} of the SMs each)")
@@ -221,7 +221,11 @@ def main():
     if world > 1:
         from paper_2405_15573_b200.dist import DistributedOperator
 
-        op = DistributedOperator(u, rank, world, device=dev, exchange=args.exchange)
+        from paper_2405_15573_b200.dist import make_distributed
+
+        op, why = make_distributed(u, rank, world, device=dev, exchange=args.exchange)
+        config["exchange"] = op.exchange
+        config["exchange_choice"] = why
         packed = op.packed_local
     elif args.emulate_ranks > 1:
         from paper_2405_15573_b200.dist import PeerEmulation
@@ -351,7 +355,7 @@ def main():
         "frac_vs_8000_nominal": achieved / 8000.0,
         "traffic": traffic,
         "algorithmic_bytes_per_launch": int(alg_bytes_total / world),
-        "kernel": "bulk::uhmv_bulk_peer_kernel" if (args.emulate_ranks > 1 or args.exchange == "peer") else
+        "kernel": "bulk::uhmv_bulk_peer_kernel" if (args.emulate_ranks > 1 or getattr(op, "exchange", "") == "peer") else
         {"bulk": "bulk::uhmv_bulk_kernel", "fused": "uhmv_fused_kernel"}.get(args.mode, "uhmv_phase_kernel (5 launches)"),
     }
     if rank != 0:

@@ -29,7 +29,7 @@ import numpy as np
 
 from .packer import pack
 
-__all__ = ["DistributedOperator", "PeerEmulation", "exchange_views"]
+__all__ = ["DistributedOperator", "PeerEmulation", "exchange_views", "make_distributed"]
 
 
 def exchange_views(work, packed, adjoint: bool):
@@ -155,17 +155,21 @@ class DistributedOperator:
     ``exchange="peer"``: one launch per rank, y/u stored into the peers' work buffers inside
     the kernel (NVLink peer mappings from torch symmetric memory)."""
 
-    def __init__(self, u, rank: int, world: int, device=None, group=None, exchange: str = "nccl"):
+    def __init__(self, u, rank: int, world: int, device=None, group=None, exchange: str = "nccl", packed=None):
         from .device import DeviceOperator
 
         if exchange not in ("nccl", "peer"):
             raise ValueError("exchange is 'nccl' or 'peer'")
         self.rank, self.world, self.group, self.exchange = rank, world, group, exchange
-        self.packed_local = packed = pack(u, rank=rank, world=world, peer=exchange == "peer")
+        if packed is None:
+            packed = pack(u, rank=rank, world=world, peer=exchange == "peer")
+        self.packed_local = packed
         self.a = DeviceOperator(packed, device=device)
         if exchange == "peer":
             self.b = None
             self._setup_peer()
+        elif packed.fwd.part_b is None:  # world 1: nothing to exchange
+            self.b = None
         else:
             self.b = DeviceOperator(
                 packed, device=device, programs=(packed.fwd.part_b, packed.adj.part_b), share_with=self.a
@@ -226,7 +230,7 @@ class DistributedOperator:
     def kernel_launches(self, adjoint=False, mode=None) -> int:
         if self.exchange == "peer":
             return 1
-        return self.a.kernel_launches(adjoint, mode) + self.b.kernel_launches(adjoint, mode)
+        return self.a.kernel_launches(adjoint, mode) + (self.b.kernel_launches(adjoint, mode) if self.b else 0)
 
     def launch_info(self, adjoint=False, mode=None):
         return self.a.launch_info(adjoint, mode)
@@ -243,6 +247,8 @@ class DistributedOperator:
                           self.epoch[adjoint], torch.cuda.current_stream(self.device))
             return self.gather_output(out, adjoint) if gather else out
         out = self.a.matvec(x, adjoint=adjoint, out=out, mode=mode)
+        if self.b is None:  # world 1
+            return out
         region, mine = exchange_views(self.a.work, self.packed_local, adjoint)
         if region.numel():
             self._all_gather(region, mine)
@@ -292,3 +298,47 @@ class DistributedOperator:
             out[...] = w
             return out
         return w
+
+
+def make_distributed(u, rank: int, world: int, device=None, group=None, exchange: str = "auto", check_tol=1e-12):
+    """The rank's DistributedOperator.  ``exchange="auto"``: the fused peer exchange when every
+    rank can map every other's buffers (torch symmetric memory) AND its first forward and
+    adjoint matvecs on a seeded vector agree with the NCCL path within ``check_tol`` on every
+    rank; the NCCL path otherwise.  Returns (operator, reason)."""
+    import torch
+    import torch.distributed as dist
+
+    if exchange in ("nccl", "peer"):
+        return DistributedOperator(u, rank, world, device=device, group=group, exchange=exchange), "requested"
+    base = pack(u, rank=rank, world=world, peer=True)
+    nccl = DistributedOperator(u, rank, world, device=device, group=group, exchange="nccl",
+                               packed=base.for_rank(rank, world, peer=False))
+    dev = nccl.device
+    peer, why = None, ""
+    try:
+        peer = DistributedOperator(u, rank, world, device=device, group=group, exchange="peer", packed=base)
+        ok = 1
+    except Exception as e:  # noqa: BLE001 -- any rank unable to map its peers: NCCL everywhere
+        ok, why = 0, f"peer setup failed: {type(e).__name__}: {e}"[:200]
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    if int(flag.item()) == 1:
+        g = torch.Generator(device="cpu").manual_seed(1234)
+        err = 0.0
+        for adjoint in (False, True):
+            n_in = u.shape[0] if adjoint else u.shape[1]
+            x = torch.complex(torch.randn(n_in, generator=g, dtype=torch.float64),
+                              torch.randn(n_in, generator=g, dtype=torch.float64)).to(dev)
+            a = nccl.matvec(x, adjoint=adjoint, gather=True)
+            b = peer.matvec(x, adjoint=adjoint, gather=True)
+            err = max(err, float(torch.linalg.norm(a - b) / torch.linalg.norm(a)))
+        e = torch.tensor([err], dtype=torch.float64, device=dev)
+        dist.all_reduce(e, op=dist.ReduceOp.MAX, group=group)
+        if float(e.item()) <= check_tol:
+            del nccl
+            return peer, f"peer exchange (agrees with the NCCL path to {float(e.item()):.1e})"
+        why = f"peer result differs from the NCCL path ({float(e.item()):.1e})"
+    elif not why:
+        why = "a peer rank could not map its buffers"
+    del peer
+    return nccl, "NCCL all-gather: " + why

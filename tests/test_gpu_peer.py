@@ -88,11 +88,17 @@ def _symm_worker(name, q):
 
         u, ex = load_uh(os.path.join(GOLDEN, f"{name}.npz"))
         op = DistributedOperator(u, 0, 1, device=torch.device("cuda", 0), exchange="peer")
+        from paper_2405_15573_b200.dist import make_distributed
+
+        auto, why = make_distributed(u, 0, 1, device=torch.device("cuda", 0), exchange="auto")
+        if auto.exchange != "peer":
+            raise AssertionError(f"auto exchange fell back: {why}")
         errs = []
         for rep in range(3):
             for adjoint, vk, rk in ((False, "vf_0", "ref_fwd_0"), (True, "va_0", "ref_adj_0")):
-                w = op.matvec_host(ex[vk], adjoint=adjoint)
-                errs.append(float(np.linalg.norm(w - ex[rk]) / np.linalg.norm(ex[rk])))
+                for o in (op, auto):
+                    w = o.matvec_host(ex[vk], adjoint=adjoint)
+                    errs.append(float(np.linalg.norm(w - ex[rk]) / np.linalg.norm(ex[rk])))
         q.put(("ok", max(errs)))
     except Exception as e:  # noqa: BLE001
         q.put(("error", repr(e)))
