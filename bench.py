@@ -416,16 +416,18 @@ def run_multi_rhs(args, world, rank, local_rank):
     from paper_2405_15573_b200.device import DeviceOperator
     from paper_2405_15573_b200.packer import pack
 
-    if world > 1 and rank != 0:
-        return  # multi-RHS is single-GPU in this round
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    if world > 1:  # every rank applies the operator to its own block of right-hand sides
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
     R = args.nrhs
     u = workloads.build_operator(3)
     packed = pack(u)
     op = DeviceOperator(packed, device=dev)
     n = u.shape[1]
-    rng = np.random.default_rng(0)
+    rng = np.random.default_rng(0 if world == 1 else [0, rank])
     Xh = rng.standard_normal((n, R)) + 1j * rng.standard_normal((n, R))
     X = torch.from_numpy(Xh).to(dev)
     op.matmat(X)
@@ -437,14 +439,22 @@ def run_multi_rhs(args, world, rank, local_rank):
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
     torch.cuda.synchronize(dev)
     for a, b in ev:
         a.record()
         op.matmat(X)
         b.record()
     torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
     clk = clocks.stop()
     t = float(np.mean([a.elapsed_time(b) for a, b in ev])) * 1e-3
+    if world > 1:  # time = max over ranks
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
     flops = 8.0 * R * packed.bytes_alg / 16  # 4 real mul + 4 add per complex MAC
     peak = dmma_peak(dev.index)
     # e2e: pinned host block in, pinned host block out (H2D + kernel + D2H + sync, wall clock)
@@ -464,26 +474,35 @@ def run_multi_rhs(args, world, rank, local_rank):
     for _ in range(ke):
         e2e_step()
     te = (time.perf_counter() - te) / ke
+    if world > 1:
+        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        te = float(tt.item())
+        if rank != 0:
+            dist.destroy_process_group()
+            return
     line = {
         "metric": "uniform-H matvecs/sec (multi-RHS block, config 5)",
-        "value": R / t,
+        "value": world * R / t,
         "unit": "matvec/s",
-        "n_gpus": 1,
+        "n_gpus": world,
         "steps": steps,
         "warmup": max(args.warmup, 3),
         "ms_per_step": t * 1e3,
         "higher_is_better": True,
-        "scaling": "strong",
+        "scaling": "weak" if world > 1 else "strong",
         "vs_baseline": None,
         "dtype": "c128 (f64 complex)",
         "data": "synthetic",
         "config": {"workload": "cfg5_cfg3_operator_x_%d_rhs" % R, "N": n, "nrhs": R,
+                   "parallelism": (f"{world} GPUs, each its own block of {R} right-hand sides (no exchange)"
+                                   if world > 1 else "single GPU"),
                    "values": "seeded synthetic on the reference-built cfg3 structure and ranks"},
         "roofline": {"bound": "tensor", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
                      "frac": flops / t / 1e12 / peak,
                      "peak_source": "uhmv_dmma_peak: measured DMMA m16n8k16 f64 throughput on this GPU",
                      "traffic": None, "flops_per_launch": flops, "kernel": "mrtc::uhmv_mrtc_kernel"},
-        "e2e": {"value": R / te, "unit": "matvec/s", "h2d_bytes_per_step": int(16 * n * R),
+        "e2e": {"value": world * R / te, "unit": "matvec/s", "h2d_bytes_per_step": int(16 * n * R),
                 "d2h_bytes_per_step": int(16 * n * R)},
         "gpu_launches": steps,
         "clocks": clk,
@@ -491,6 +510,8 @@ def run_multi_rhs(args, world, rank, local_rank):
     if os.environ.get("UHMV_PROFILE"):
         line["engine_cycles"] = op.profile_mr(R)
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def load_traffic(cfg):

@@ -40,6 +40,7 @@ Two device encodings of the same segments are emitted:
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -90,7 +91,7 @@ FAR_ROWS = 64  # output rows per FAR op (4 register slots of 16 row-groups)
 P1_CHUNK = 256  # max input rows per P1 op
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_NCOLS_MAX = 640  # widest N piece row (two rows + x window still fit a stage)
-NW_COLS = int(__import__("os").environ.get("UHMV_NW_COLS", 640))  # widest panel of a warp-per-row op
+NW_COLS = int(os.environ.get("UHMV_NW_COLS", 640))  # widest panel of a warp-per-row op (sweeps: 352/176 slower)
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 # work splitting of the farfield chain ops across CTAs (output entries per op)
 SPLIT_DEFAULTS = {"p1_out": 1 << 30, "u_cols": 1 << 30, "z_rows": 1 << 30, "far_rows": ROWS_PER_CHUNK}
