@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--emulate-ranks", type=int, default=0,
                     help="diagnostics (1 GPU): run a W-rank peer-exchange partition in one launch, "
                          "each rank on 1/W of the SMs")
+    ap.add_argument("--l2", default="auto", choices=["auto", "hot"],
+                    help="auto: flush L2 between steps when the operator fits in ~4x L2; hot: never "
+                         "(the L2-resident number SURVEY §8d asks for at config 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     return ap.parse_args()
@@ -123,6 +126,17 @@ class ClockSampler:
         }
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(u, x, sample_s: float):
     """The oracle port (restating uniform.py:476-556) on the host cores: best of BLAS threads
     {1, all}, bounded to ~sample_s seconds of CPU work."""
@@ -156,6 +170,8 @@ def cpu_baseline(u, x, sample_s: float):
         "value": 1.0 / t,
         "unit": "matvec/s",
         "cores": threads,
+        "cpu_model": cpu_model(),
+        "host_cpus": ncpu,
         "kind": "port",
         "sample": f"{reps} full matvecs (min of reps; median {med * 1e3:.1f} ms) after 1 warm-up, "
         f"oracle/matvec_oracle.py (restates uniform.py:476-556), BLAS threads best of {{1,{ncpu}}}",
@@ -255,7 +271,7 @@ def main():
     # L2 policy: operator bytes vs the 126 MB L2
     full_bytes = workloads.algorithmic_bytes(packed)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = full_bytes / max(world, 1) < 4 * l2_bytes
+    flush = full_bytes / max(world, 1) < 4 * l2_bytes and args.l2 == "auto"
     flush_buf = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev) if flush else None
     flush_rd = torch.zeros(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev) if flush else None
 
@@ -267,7 +283,8 @@ def main():
 
     config["l2"] = (
         f"L2 flushed between steps ({flush_buf.numel() * 4 / 1e6:.0f} MB write + read, untimed)" if flush
-        else f"operator {full_bytes / max(world, 1) / 1e9:.2f} GB per GPU >> L2 {l2_bytes / 1e6:.0f} MB, no flush"
+        else (f"L2-hot: no flush (operator {full_bytes / 1e6:.0f} MB, L2 {l2_bytes / 1e6:.0f} MB)" if args.l2 == "hot"
+              else f"operator {full_bytes / max(world, 1) / 1e9:.2f} GB per GPU >> L2 {l2_bytes / 1e6:.0f} MB, no flush")
     )
     for _ in range(max(args.warmup, 3)):
         if flush:
