@@ -235,3 +235,52 @@ def test_small_stages_split_wide_rows(name):
     for adjoint, vk, rk in ((False, "vf_0", "ref_fwd_0"), (True, "va_0", "ref_adj_0")):
         w = vm_matvec(p, ex[vk], adjoint=adjoint, order="fused", engine="pieces")
         assert rel(w, ex[rk]) <= TOL
+
+
+def test_host_io_programs():
+    """Host-I/O variant (uhmv_matvec_host with pinned buffers): same results as the plain
+    program in the VM; P1 ops publish x (OP_XHOST, one input run), NEAR ops wait for it
+    (OP_XWAIT), and every output leaf is drained exactly once -- its drain descriptor (the run
+    after the op's output cover) carries the leaf's NEAR + FAR op count."""
+    from conftest import GOLDEN_NAMES, load_golden, rel
+    from packed_vm import run_program
+    from paper_2405_15573_b200.packer import (
+        BUF_HOSTW, BUF_X, KIND_FAR, KIND_NEAR, KIND_P1, OP_DRAIN, OP_XHOST, OP_XWAIT, pack,
+    )
+
+    n_checked = 0
+    for name in GOLDEN_NAMES:
+        u, ex = load_golden(name)
+        p = pack(u)
+        for adjoint, prog, vk, rk in zip((False, True), p.io_programs(), ("vf_0", "va_0"), ("ref_fwd_0", "ref_adj_0")):
+            if prog is None:
+                continue
+            n_checked += 1
+            assert prog.host_io
+            x = np.asarray(ex[vk], dtype=np.complex128)
+            n_out = p.n_cols if adjoint else p.n_rows
+            w = np.zeros(n_out, dtype=np.complex128)
+            run_program(prog, p.arena, np.zeros(p.work_len, dtype=np.complex128), x, w, order="fused", engine="pieces")
+            assert rel(w, ex[rk]) <= 1e-12
+            drains = {}
+            covered = np.zeros(p.n_rows if not adjoint else p.n_cols, dtype=int)
+            for i in range(prog.n_ops):
+                f, k = int(prog.ops[i, 12]), int(prog.kinds[i])
+                if k == KIND_P1:
+                    assert f & OP_XHOST
+                    rr = prog.runs[prog.ops[i, 2] : prog.ops[i, 3]]
+                    assert len(rr) == 1 and rr[0][0] == BUF_X
+                if k == KIND_NEAR:
+                    assert f & OP_XWAIT and f & OP_DRAIN
+                if k in (KIND_NEAR, KIND_FAR):
+                    assert f & OP_DRAIN
+                    d = prog.runs[prog.ops[i, 7]]
+                    assert d[0] == BUF_HOSTW
+                    key = (int(d[1]), int(d[2]), int(d[3]))
+                    drains.setdefault(key, [int(d[4]), 0])[1] += 1
+            for (lo, ln, _c), (expect, seen) in drains.items():
+                assert expect == seen
+                covered[lo : lo + ln] += 1
+            n_out_rows = p.n_cols if adjoint else p.n_rows
+            assert (covered[:n_out_rows] == 1).all()
+    assert n_checked >= 8
