@@ -113,6 +113,9 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
 
 /* End-to-end call with HOST buffers: H2D copy of x, execute, D2H copy of w, stream sync.
  * x_host / w_host: complex128 (interleaved re,im doubles), length n_in / n_out.
+ * With pinned (page-locked) buffers the whole call is captured once per direction and buffer
+ * pair into a CUDA graph and replayed (UHMV_HOST_GRAPH=0 disables), and -- after
+ * uhmv_plan_set_io -- runs as one host-I/O launch instead of copy / launch / copy.
  * Replaces: the whole matvec_uh call as a caller sees it (uniform.py:476-556). */
 int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
                      void* stream);

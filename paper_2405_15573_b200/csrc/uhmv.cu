@@ -441,6 +441,15 @@ struct uhmv_plan {
     void* io_x_dev;
     const void* io_w_host;
     void* io_w_dev;
+    // CUDA graphs of the whole host call (copies / memset / kernel) per direction, for pinned
+    // buffers: one graph launch replaces four API calls (UHMV_HOST_GRAPH=0 disables)
+    cudaGraphExec_t hg_exec[2];
+    const void* hg_x[2];
+    void* hg_w[2];
+    int hg_mode[2];
+    int hg_io[2];
+    cudaStream_t cap_stream;  // capture stream (the caller's may be the legacy default stream)
+    int no_graphs;
     int bulk_smem[2];
     int bulk_nstage[2];
     int sm_count;
@@ -692,6 +701,7 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     }
     if (const char* ev = getenv("UHMV_DEBUG_SKIP_WAITS")) p->debug_skip_waits = atoi(ev);
     if (const char* ev = getenv("UHMV_DEBUG_FLAGS")) p->debug_flags = atoi(ev);
+    if (const char* ev = getenv("UHMV_HOST_GRAPH")) p->no_graphs = (atoi(ev) == 0);
     *out = p;
     return UHMV_OK;
 }
@@ -824,10 +834,13 @@ int uhmv_peer_set_diag(void* host_mapped, int spin_log2) {
     return UHMV_OK;
 }
 
+static void drop_host_graphs(uhmv_plan* plan);
+
 int uhmv_plan_set_io(uhmv_plan* plan, const uhmv_program* fwd, const uhmv_program* adj, uint32_t* counters) {
     if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_set_io: null plan");
     if (!fwd && !adj) {  // detach
         plan->has_io = false;
+        drop_host_graphs(plan);
         return UHMV_OK;
     }
     if (!fwd || !adj || !counters) return fail(UHMV_EINVAL, "uhmv_plan_set_io: null argument");
@@ -846,7 +859,7 @@ int uhmv_plan_set_io(uhmv_plan* plan, const uhmv_program* fwd, const uhmv_progra
     }
     plan->io_counters = counters;
     plan->has_io = true;
-    plan->io_x_host = plan->io_w_host = nullptr;
+    drop_host_graphs(plan);  // captured graphs hold the previous programs
     return UHMV_OK;
 }
 
@@ -974,53 +987,104 @@ int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, in
     return UHMV_OK;
 }
 
+// Enqueue one host-buffer matvec on st (no synchronize): the host-I/O launch (io = true;
+// x_dev / w_dev are the device-visible pointers of the pinned buffers) or H2D copy + execute
+// + D2H copy.
+static int enqueue_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode, cudaStream_t st,
+                        bool io, const void* x_dev, void* w_dev) {
+    const int64_t n_in = adjoint ? plan->d.n_rows : plan->d.n_cols;
+    const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
+    const int k = adjoint ? 1 : 0;
+    if (io) {
+        // ONE launch reads x over PCIe (P1 ops) and drains finished output leaves to w_host
+        // as they complete -- no separate H2D / D2H copies
+        cudaError_t e0 = cudaMemsetAsync(plan->d.w_scratch, 0, (size_t)n_out * 16, st);
+        if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
+        const uhmv_program& pr = plan->io[k];
+        bulk::Params bp = make_bulk_params(plan, pr, k, plan->d.x_scratch, plan->d.w_scratch);
+        bp.nstage = plan->io_nstage[k];
+        bp.counters = plan->io_counters;
+        bp.prof = nullptr;
+        bp.trace = nullptr;
+        bp.x_host = static_cast<const double2*>(x_dev);
+        bp.w_host = static_cast<double2*>(w_dev);
+        bulk::uhmv_bulk_io_kernel<<<plan->io_grid[k], bulk::kThreads, plan->io_smem[k], st>>>(bp);
+        e0 = cudaGetLastError();
+        if (e0 != cudaSuccess) return cuda_fail(e0, "uhmv_bulk_kernel (host I/O) launch");
+        return UHMV_OK;
+    }
+    cudaError_t e = cudaMemcpyAsync(plan->d.x_scratch, x_host, (size_t)n_in * 16, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");
+    int rc = uhmv_execute(plan, plan->d.x_scratch, plan->d.w_scratch, adjoint, mode, st);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(w_host, plan->d.w_scratch, (size_t)n_out * 16, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H copy of w");
+    return UHMV_OK;
+}
+
+static void drop_host_graphs(uhmv_plan* plan) {
+    for (int k = 0; k < 2; ++k) {
+        if (plan->hg_exec[k]) cudaGraphExecDestroy(plan->hg_exec[k]);
+        plan->hg_exec[k] = nullptr;
+    }
+}
+
 int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
                      void* stream) {
     if (!plan) return fail(UHMV_EINVAL, "uhmv_matvec_host: null plan");
     if (!plan->d.x_scratch || !plan->d.w_scratch)
         return fail(UHMV_EINVAL, "uhmv_matvec_host: plan has no scratch vectors");
     if (!x_host || !w_host) return fail(UHMV_EINVAL, "uhmv_matvec_host: null host pointer");
-    const int64_t n_in = adjoint ? plan->d.n_rows : plan->d.n_cols;
-    const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int k = adjoint ? 1 : 0;
-    if (plan->has_io && mode == UHMV_MODE_BULK && plan->io[k].n_ops > 0) {
-        // pinned host buffers: ONE launch reads x over PCIe (P1 ops) and drains finished
-        // output leaves to w_host as they complete -- no separate H2D / D2H copies
-        if (x_host != plan->io_x_host) {
-            plan->io_x_dev = mapped_ptr(x_host);
-            plan->io_x_host = x_host;
-        }
-        if (w_host != plan->io_w_host) {
-            plan->io_w_dev = mapped_ptr(w_host);
-            plan->io_w_host = w_host;
-        }
-        if (plan->io_x_dev && plan->io_w_dev) {
-            cudaError_t e0 = cudaMemsetAsync(plan->d.w_scratch, 0, (size_t)n_out * 16, st);
-            if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
-            const uhmv_program& pr = plan->io[k];
-            bulk::Params bp = make_bulk_params(plan, pr, k, plan->d.x_scratch, plan->d.w_scratch);
-            bp.nstage = plan->io_nstage[k];
-            bp.counters = plan->io_counters;
-            bp.prof = nullptr;
-            bp.x_host = static_cast<const double2*>(plan->io_x_dev);
-            bp.w_host = static_cast<double2*>(plan->io_w_dev);
-            bulk::uhmv_bulk_io_kernel<<<plan->io_grid[k], bulk::kThreads, plan->io_smem[k], st>>>(bp);
-            e0 = cudaGetLastError();
-            if (e0 != cudaSuccess) return cuda_fail(e0, "uhmv_bulk_kernel (host I/O) launch");
-            e0 = cudaStreamSynchronize(st);
-            if (e0 != cudaSuccess) return cuda_fail(e0, "uhmv_matvec_host synchronize");
-            return UHMV_OK;
-        }
+    if (x_host != plan->io_x_host) {  // device-visible pointers of pinned buffers (or null)
+        plan->io_x_dev = mapped_ptr(x_host);
+        plan->io_x_host = x_host;
     }
-    cudaError_t e = cudaMemcpyAsync(plan->d.x_scratch, x_host, (size_t)n_in * 16,
-                                    cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");
-    int rc = uhmv_execute(plan, plan->d.x_scratch, plan->d.w_scratch, adjoint, mode, stream);
-    if (rc) return rc;
-    e = cudaMemcpyAsync(w_host, plan->d.w_scratch, (size_t)n_out * 16, cudaMemcpyDeviceToHost,
-                        st);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H copy of w");
+    if (w_host != plan->io_w_host) {
+        plan->io_w_dev = mapped_ptr(w_host);
+        plan->io_w_host = w_host;
+    }
+    const bool pinned = plan->io_x_dev && plan->io_w_dev;
+    const bool io = pinned && plan->has_io && mode == UHMV_MODE_BULK && plan->io[k].n_ops > 0;
+    cudaError_t e;
+    if (pinned && !plan->no_graphs && !plan->prof) {
+        if (!plan->hg_exec[k] || plan->hg_x[k] != x_host || plan->hg_w[k] != w_host || plan->hg_mode[k] != mode ||
+            plan->hg_io[k] != (int)io) {
+            if (plan->hg_exec[k]) cudaGraphExecDestroy(plan->hg_exec[k]);
+            plan->hg_exec[k] = nullptr;
+            if (!plan->cap_stream) {
+                e = cudaStreamCreateWithFlags(&plan->cap_stream, cudaStreamNonBlocking);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate (graph capture)");
+            }
+            e = cudaStreamBeginCapture(plan->cap_stream, cudaStreamCaptureModeThreadLocal);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamBeginCapture");
+            const int rc = enqueue_host(plan, x_host, w_host, adjoint, mode, plan->cap_stream, io, plan->io_x_dev,
+                                        plan->io_w_dev);
+            cudaGraph_t g = nullptr;
+            e = cudaStreamEndCapture(plan->cap_stream, &g);
+            if (rc) {
+                if (g) cudaGraphDestroy(g);
+                return rc;
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+            e = cudaGraphInstantiate(&plan->hg_exec[k], g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) {
+                plan->hg_exec[k] = nullptr;
+                return cuda_fail(e, "cudaGraphInstantiate");
+            }
+            plan->hg_x[k] = x_host;
+            plan->hg_w[k] = w_host;
+            plan->hg_mode[k] = mode;
+            plan->hg_io[k] = (int)io;
+        }
+        e = cudaGraphLaunch(plan->hg_exec[k], st);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
+    } else {
+        const int rc = enqueue_host(plan, x_host, w_host, adjoint, mode, st, io, plan->io_x_dev, plan->io_w_dev);
+        if (rc) return rc;
+    }
     e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "uhmv_matvec_host synchronize");
     return UHMV_OK;
@@ -1081,6 +1145,10 @@ int uhmv_dmma_peak(int device, double* tflops) {
 }
 
 int uhmv_plan_destroy(uhmv_plan* plan) {
+    if (plan) {
+        drop_host_graphs(plan);
+        if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
+    }
     delete plan;
     return UHMV_OK;
 }
