@@ -393,6 +393,11 @@ class DeviceOperator:
         mode = mode or default_mode()
         torch = self.torch
         adjoint = bool(adjoint)
+        with self._lock:  # the plan's host-I/O programs and captured graphs are per-plan state
+            return self._matvec_host_locked(x_host, adjoint, out, mode, stream, host_io)
+
+    def _matvec_host_locked(self, x_host, adjoint, out, mode, stream, host_io):
+        torch = self.torch
         use, tuning = False, False
         if mode == "bulk" and host_io is not False and self.attach_io() and self._io[2][int(adjoint)] is not None:
             if host_io:
@@ -409,21 +414,20 @@ class DeviceOperator:
             on = list(self._io_on or (False, False))
             on[int(adjoint)] = False
             self._set_io(*on)
-        with self._lock:
-            t0 = time.perf_counter()
-            # (the device switch costs ~10 us of host time per call: only when needed)
-            if torch.cuda.current_device() == self.device.index:
+        t0 = time.perf_counter()
+        # (the device switch costs ~10 us of host time per call: only when needed)
+        if torch.cuda.current_device() == self.device.index:
+            rc = _lib.lib().uhmv_matvec_host(
+                self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
+                int(adjoint), _MODES[mode], self._stream(stream),
+            )
+        else:
+            with torch.cuda.device(self.device):
                 rc = _lib.lib().uhmv_matvec_host(
                     self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
                     int(adjoint), _MODES[mode], self._stream(stream),
                 )
-            else:
-                with torch.cuda.device(self.device):
-                    rc = _lib.lib().uhmv_matvec_host(
-                        self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
-                        int(adjoint), _MODES[mode], self._stream(stream),
-                    )
-            dt = time.perf_counter() - t0
+        dt = time.perf_counter() - t0
         _lib.check(rc, "uhmv_matvec_host")
         if tuning:
             t_io, t_cp = self._io_tune[adjoint]
