@@ -65,3 +65,12 @@ def test_execute_peer_rejects_bad_arguments():
     assert b"rank range" in L.uhmv_last_error()
     assert L.uhmv_execute_peer(plans, 1, 0, 2, ranks, ctypes.c_void_p(16), ws, 0, 0, None) == -1
     assert b"epoch" in L.uhmv_last_error()
+
+
+def test_diagnostic_and_io_entries_reject_null_plan():
+    L = ensure_built()
+    assert L.uhmv_plan_set_io(None, None, None, None) == -1
+    assert b"null plan" in L.uhmv_last_error()
+    assert L.uhmv_plan_set_trace(None, None) == -1
+    assert L.uhmv_plan_set_profile(None, None) == -1
+    assert L.uhmv_peer_set_diag(None, 28) == 0  # process-wide diagnostics switch, always accepted
