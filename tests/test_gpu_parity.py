@@ -225,3 +225,38 @@ def test_host_io_pinned_buffers(name):
             wp = dop.matvec_host(xv, adjoint=adjoint)  # pageable: copy path
             assert rel(wp, ex[rk]) <= 1e-12
     assert dop.attach_io() == any(q is not None for q in dop.packed.io_programs())
+
+
+def test_host_call_graphs_follow_buffers():
+    """The captured CUDA graph of uhmv_matvec_host is keyed by direction, buffer pair and
+    path: switching between two pinned buffer pairs, pageable buffers, directions and forced
+    paths in an interleaved sequence gives the reference result every time (a stale graph
+    would write the old buffer or read the old x)."""
+    import torch
+
+    from conftest import load_golden
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer import pack
+
+    u, ex = load_golden("ico2_helm_compress")
+    dop = DeviceOperator(pack(u), device="cuda:0")
+    rng = np.random.default_rng(3)
+    pairs = []
+    for _ in range(2):
+        xs = {a: torch.empty(len(ex["vf_0" if not a else "va_0"]), dtype=torch.complex128).pin_memory() for a in (False, True)}
+        ws = {a: torch.empty(len(ex["ref_fwd_0" if not a else "ref_adj_0"]), dtype=torch.complex128).pin_memory() for a in (False, True)}
+        pairs.append((xs, ws))
+    for step in range(40):
+        adjoint = bool(rng.integers(2))
+        vk, rk = ("va_0", "ref_adj_0") if adjoint else ("vf_0", "ref_fwd_0")
+        s = complex(rng.standard_normal(), rng.standard_normal())
+        which = int(rng.integers(3))
+        host_io = [None, True, False][int(rng.integers(3))]
+        if which < 2:
+            xs, ws = pairs[which]
+            xs[adjoint].numpy()[:] = np.asarray(ex[vk]) * s
+            ws[adjoint].numpy()[:] = np.nan
+            w = dop.matvec_host(xs[adjoint].numpy(), adjoint=adjoint, out=ws[adjoint].numpy(), host_io=host_io)
+        else:
+            w = dop.matvec_host(np.asarray(ex[vk]) * s, adjoint=adjoint, host_io=host_io)
+        assert rel(w, np.asarray(ex[rk]) * s) <= 1e-12, (step, adjoint, which, host_io)
