@@ -1037,14 +1037,12 @@ int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjo
     if (!x_host || !w_host) return fail(UHMV_EINVAL, "uhmv_matvec_host: null host pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int k = adjoint ? 1 : 0;
-    if (x_host != plan->io_x_host) {  // device-visible pointers of pinned buffers (or null)
-        plan->io_x_dev = mapped_ptr(x_host);
-        plan->io_x_host = x_host;
-    }
-    if (w_host != plan->io_w_host) {
-        plan->io_w_dev = mapped_ptr(w_host);
-        plan->io_w_host = w_host;
-    }
+    // device-visible pointers of pinned buffers (or null), queried every call (~1 us): a
+    // cached answer could outlive the allocation it described
+    plan->io_x_dev = mapped_ptr(x_host);
+    plan->io_x_host = x_host;
+    plan->io_w_dev = mapped_ptr(w_host);
+    plan->io_w_host = w_host;
     const bool pinned = plan->io_x_dev && plan->io_w_dev;
     const bool io = pinned && plan->has_io && mode == UHMV_MODE_BULK && plan->io[k].n_ops > 0;
     cudaError_t e;
