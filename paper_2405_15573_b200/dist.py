@@ -201,8 +201,17 @@ class DistributedOperator:
         off_c = 2 * wmax * 16
         off_d = off_c + ((4 * cmax + 127) // 128) * 128
         per_dir = off_d + ((4 * self.world + 127) // 128) * 128  # forward block, then adjoint block
-        self._symm_buf = symm.empty(2 * per_dir, dtype=torch.uint8, device=dev)
-        self._symm_buf.zero_()
+        # every rank must reach the (collective) rendezvous or none: agree on the allocation first
+        try:
+            self._symm_buf = symm.empty(2 * per_dir, dtype=torch.uint8, device=dev)
+            self._symm_buf.zero_()
+            ok = 1
+        except Exception:  # noqa: BLE001
+            ok = 0
+        flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=self.group)
+        if int(flag.item()) == 0:
+            raise RuntimeError("symmetric-memory allocation failed on some rank")
         torch.cuda.synchronize(dev)
         grp = self.group if self.group is not None else dist.group.WORLD
         try:
