@@ -111,3 +111,25 @@ def test_config5_multi_rhs_columns():
         for j in (0, 37, 63):
             ref = oracle_matvec_uh(u, Xh[:, j], adjoint=adjoint)
             assert rel(W[:, j].cpu().numpy(), ref) <= TOL, (adjoint, j)
+
+
+def test_config4_full_size_parity():
+    """Gate G1/G4 at the largest config (N = 327680): the bulk engine vs the CPU oracle and
+    vs the output samples the reference itself produced on this operator (stored in the
+    fixture by tools/make_workloads.py), forward and adjoint, 1e-12."""
+    from paper_2405_15573_b200 import workloads
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer import pack
+
+    if not os.path.exists(workloads.workload_path(4)):
+        pytest.skip("fixture missing")
+    u = workloads.build_operator(4)
+    _, d = workloads.load_structure(4)
+    dop = DeviceOperator(pack(u), device="cuda:0")
+    x_np = workloads.seeded_vector(u.shape[1], 0)
+    x = torch.from_numpy(x_np).cuda()
+    s = int(d["x_ref_synth_stride"])
+    for adjoint, key in ((False, "x_ref_synth_sample"), (True, "x_ref_synth_adj_sample")):
+        w = dop.matvec(x, adjoint=adjoint).cpu().numpy()
+        assert rel(w, oracle_matvec_uh(u, x_np, adjoint=adjoint)) <= TOL, adjoint
+        assert rel(w[::s], d[key]) <= TOL, adjoint
