@@ -133,3 +133,23 @@ def test_config4_full_size_parity():
         w = dop.matvec(x, adjoint=adjoint).cpu().numpy()
         assert rel(w, oracle_matvec_uh(u, x_np, adjoint=adjoint)) <= TOL, adjoint
         assert rel(w[::s], d[key]) <= TOL, adjoint
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_h_format_full_size_parity(cfg):
+    """matvec_h (hmatrix.py:143-184) at full size on the config's H-matrix block ranks: the
+    bulk engine vs the CPU oracle, forward and adjoint, 1e-12."""
+    from matvec_oracle import oracle_matvec_h
+    from paper_2405_15573_b200 import workloads
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer_h import pack_h
+
+    if not os.path.exists(workloads.workload_path(cfg)):
+        pytest.skip("fixture missing")
+    h = workloads.build_h_operator(cfg)
+    dop = DeviceOperator(pack_h(h), device="cuda:0")
+    x_np = workloads.seeded_vector(h.shape[1], 0)
+    x = torch.from_numpy(x_np).cuda()
+    for adjoint in (False, True):
+        w = dop.matvec(x, adjoint=adjoint).cpu().numpy()
+        assert rel(w, oracle_matvec_h(h, x_np, adjoint=adjoint)) <= TOL, (cfg, adjoint)
