@@ -52,21 +52,23 @@ def test_peer_emulation_matches_reference(name, world):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
-def test_peer_emulation_config2(world):
-    """Full-size config 2 partition against the single-GPU engine (same ops, same order)."""
+@pytest.mark.parametrize("cfg,world", [(2, 2), (2, 4), (2, 8), (3, 4), (3, 8)])
+def test_peer_emulation_config(cfg, world):
+    """Full-size partitions against the single-GPU engine (same ops, same order), a different
+    x every epoch."""
     from paper_2405_15573_b200 import workloads
     from paper_2405_15573_b200.device import DeviceOperator
     from paper_2405_15573_b200.dist import PeerEmulation
     from paper_2405_15573_b200.packer import pack
 
-    if not os.path.exists(workloads.workload_path(2)):
+    if not os.path.exists(workloads.workload_path(cfg)):
         pytest.skip("fixture missing")
-    u = workloads.build_operator(2)
-    x = torch.from_numpy(workloads.seeded_vector(u.shape[1], 0)).cuda()
+    u = workloads.build_operator(cfg)
+    x0 = torch.from_numpy(workloads.seeded_vector(u.shape[1], 0)).cuda()
     one = DeviceOperator(pack(u), device="cuda:0")
     em = PeerEmulation(u, world, device="cuda:0")
-    for adjoint in (False, True, False):
+    for e, adjoint in enumerate((False, True, False, True, False)):
+        x = x0 * (1.0 + 0.37j * e)
         ref = one.matvec(x, adjoint=adjoint)
         w = em.matvec(x, adjoint=adjoint)
         assert (torch.linalg.norm(w - ref) / torch.linalg.norm(ref)).item() <= 1e-13
