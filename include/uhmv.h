@@ -136,6 +136,15 @@ int uhmv_plan_set_io(uhmv_plan* plan, const uhmv_program* fwd, const uhmv_progra
 int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs,
                       int adjoint, void* stream);
 
+/* Multi-RHS with HOST buffers, pipelined: X_host (n_in x nrhs) and W_host (n_out x nrhs)
+ * row-major complex128 (pinned for overlap); the nrhs columns go in chunks of `chunk` (a
+ * multiple of 16 dividing nrhs): the H2D copy of chunk c+1, the DMMA product of chunk c and
+ * the D2H copy of chunk c-1 run concurrently on three streams.  X_dev / W_dev: device buffers
+ * of 2 x n x chunk complex128 (double buffers); work_mr: work_len x chunk.  Synchronous.
+ * Replaces: the reference's column loop over matvec_uh for a block of right-hand sides. */
+int uhmv_matmat_host(uhmv_plan* plan, const void* X_host, void* W_host, int nrhs, void* X_dev, void* W_dev,
+                     void* work_mr, int chunk, int adjoint, void* stream);
+
 /* One rank of a peer-exchange partition (packer pack(peer=True)), as mapped in the calling
  * process: its own buffers, or a peer's NVLink-mapped ones (CUDA IPC / symmetric memory). */
 typedef struct uhmv_peer_rank {

@@ -83,6 +83,7 @@ EXPORTS = (
     "uhmv_execute_phases",
     "uhmv_matvec_host",
     "uhmv_execute_mrhs",
+    "uhmv_matmat_host",
     "uhmv_execute_peer",
     "uhmv_peer_set_diag",
     "uhmv_plan_set_io",
@@ -117,6 +118,8 @@ def lib():
     L.uhmv_matvec_host.argtypes = [vp, vp, vp, i32, i32, vp]
     L.uhmv_execute_mrhs.argtypes = [vp, vp, vp, vp, i32, i32, vp]
     L.uhmv_execute_mrhs.restype = i32
+    L.uhmv_matmat_host.argtypes = [vp, vp, vp, i32, vp, vp, vp, i32, i32, vp]
+    L.uhmv_matmat_host.restype = i32
     L.uhmv_execute_peer.argtypes = [vp, i32, i32, i32, ctypes.POINTER(UhmvPeerRank), vp, vp, i32, ctypes.c_uint32, vp]
     L.uhmv_execute_peer.restype = i32
     L.uhmv_peer_set_diag.argtypes = [vp, i32]

@@ -449,6 +449,9 @@ struct uhmv_plan {
     int hg_mode[2];
     int hg_io[2];
     cudaStream_t cap_stream;  // capture stream (the caller's may be the legacy default stream)
+    // pipelined host-buffer multi-RHS (uhmv_matmat_host): copy-in / compute / copy-out streams
+    cudaStream_t mm_stream[3];
+    cudaEvent_t mm_ev[3][2];
     int no_graphs;
     int bulk_smem[2];
     int bulk_nstage[2];
@@ -1088,6 +1091,62 @@ int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjo
     return UHMV_OK;
 }
 
+int uhmv_matmat_host(uhmv_plan* plan, const void* X_host, void* W_host, int nrhs, void* X_dev, void* W_dev,
+                     void* work_mr, int chunk, int adjoint, void* stream) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_matmat_host: null plan");
+    if (!X_host || !W_host || !X_dev || !W_dev || !work_mr) return fail(UHMV_EINVAL, "uhmv_matmat_host: null buffer");
+    if (chunk <= 0 || chunk % 16 || nrhs <= 0 || nrhs % chunk)
+        return fail(UHMV_EINVAL, "uhmv_matmat_host: chunk must be a multiple of 16 dividing nrhs");
+    const int64_t n_in = adjoint ? plan->d.n_rows : plan->d.n_cols;
+    const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
+    cudaError_t e;
+    for (int i = 0; i < 3; ++i) {
+        if (!plan->mm_stream[i]) {
+            e = cudaStreamCreateWithFlags(&plan->mm_stream[i], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate (matmat_host)");
+            for (int b = 0; b < 2; ++b) {
+                e = cudaEventCreateWithFlags(&plan->mm_ev[i][b], cudaEventDisableTiming);
+                if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate (matmat_host)");
+            }
+        }
+    }
+    cudaStream_t s_in = plan->mm_stream[0], s_cmp = plan->mm_stream[1], s_out = plan->mm_stream[2];
+    // order after the caller's prior work on its stream
+    cudaEvent_t start;
+    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    cudaEventRecord(start, static_cast<cudaStream_t>(stream));
+    cudaStreamWaitEvent(s_in, start, 0);
+    cudaStreamWaitEvent(s_cmp, start, 0);
+    const int nchunk = nrhs / chunk;
+    const size_t xc = (size_t)n_in * chunk * 16, wc = (size_t)n_out * chunk * 16;
+    for (int c = 0; c < nchunk; ++c) {
+        const int b = c & 1;
+        char* xd = static_cast<char*>(X_dev) + b * xc;
+        char* wd = static_cast<char*>(W_dev) + b * wc;
+        if (c >= 2) cudaStreamWaitEvent(s_in, plan->mm_ev[1][b], 0);  // chunk c-2 done reading xd
+        // H2D of the chunk's columns: rows of chunk * 16 B out of rows of nrhs * 16 B
+        e = cudaMemcpy2DAsync(xd, (size_t)chunk * 16, static_cast<const char*>(X_host) + (size_t)c * chunk * 16,
+                              (size_t)nrhs * 16, (size_t)chunk * 16, (size_t)n_in, cudaMemcpyHostToDevice, s_in);
+        if (e != cudaSuccess) return cuda_fail(e, "H2D copy of X");
+        cudaEventRecord(plan->mm_ev[0][b], s_in);
+        cudaStreamWaitEvent(s_cmp, plan->mm_ev[0][b], 0);
+        if (c >= 2) cudaStreamWaitEvent(s_cmp, plan->mm_ev[2][b], 0);  // chunk c-2's W copied out
+        const int rc = uhmv_execute_mrhs(plan, xd, wd, work_mr, chunk, adjoint, s_cmp);
+        if (rc) return rc;
+        cudaEventRecord(plan->mm_ev[1][b], s_cmp);
+        cudaStreamWaitEvent(s_out, plan->mm_ev[1][b], 0);
+        e = cudaMemcpy2DAsync(static_cast<char*>(W_host) + (size_t)c * chunk * 16, (size_t)nrhs * 16, wd,
+                              (size_t)chunk * 16, (size_t)chunk * 16, (size_t)n_out, cudaMemcpyDeviceToHost, s_out);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H copy of W");
+        cudaEventRecord(plan->mm_ev[2][b], s_out);
+    }
+    cudaEventDestroy(start);
+    e = cudaStreamSynchronize(s_out);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s_cmp);
+    if (e != cudaSuccess) return cuda_fail(e, "uhmv_matmat_host synchronize");
+    return UHMV_OK;
+}
+
 int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int* smem_bytes,
                    int* threads_per_cta, int* stages) {
     if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_info: null plan");
@@ -1146,6 +1205,11 @@ int uhmv_plan_destroy(uhmv_plan* plan) {
     if (plan) {
         drop_host_graphs(plan);
         if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
+        for (int i = 0; i < 3; ++i) {
+            if (!plan->mm_stream[i]) continue;
+            for (int b = 0; b < 2; ++b) cudaEventDestroy(plan->mm_ev[i][b]);
+            cudaStreamDestroy(plan->mm_stream[i]);
+        }
     }
     delete plan;
     return UHMV_OK;
