@@ -52,6 +52,11 @@ def parse():
     ap.add_argument("--l2", default="auto", choices=["auto", "hot"],
                     help="auto: flush L2 between steps when the operator fits in ~4x L2; hot: never "
                          "(the L2-resident number SURVEY §8d asks for at config 1)")
+    ap.add_argument("--slice", default="",
+                    help="predict multi-GPU scaling on ONE GPU: comma-separated world sizes W; each rank's NCCL-path "
+                         "programs (launch A + launch B of the W-way row partition) run alone on the whole GPU")
+    ap.add_argument("--ag-lat-us", type=float, default=15.0, help="--slice model: NCCL all-gather latency (us)")
+    ap.add_argument("--ag-gbs", type=float, default=300.0, help="--slice model: NCCL all-gather bandwidth (GB/s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     return ap.parse_args()
@@ -138,60 +143,70 @@ def cpu_model() -> str:
 
 
 def cpu_baseline(u, x, sample_s: float):
-    """The oracle port (restating uniform.py:476-556) on the host cores: best of BLAS threads
-    {1, all}, bounded to ~sample_s seconds of CPU work."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from matvec_oracle import oracle_matvec_uh
-
+    """The reference's own matvec_uh (or, without oracle/_ref, the oracle port) on the host
+    cores, bounded to ~sample_s seconds: grid over (BLAS threads, workers) in {(1, 1), (all, 1),
+    (1, all)}, best cell reported, every cell listed."""
+    fn, kind, desc = reference_impl()
     try:
         from threadpoolctl import threadpool_limits
     except ImportError:  # pragma: no cover
         threadpool_limits = None
     ncpu = os.cpu_count() or 1
-    best = None
-    for threads in sorted({1, ncpu}):
+    cells = []
+    for threads, workers in sorted({(1, 1), (ncpu, 1), (1, ncpu)}):
         ctx = threadpool_limits(limits=threads) if threadpool_limits else None
         try:
-            oracle_matvec_uh(u, x)  # warm-up, excluded
+            fn(u, x, workers=workers)  # warm-up, excluded
             ts = []
-            t_end = time.perf_counter() + sample_s / 2
+            t_end = time.perf_counter() + sample_s / 3
             while len(ts) < 3 or (time.perf_counter() < t_end and len(ts) < 50):
                 t0 = time.perf_counter()
-                oracle_matvec_uh(u, x)
+                fn(u, x, workers=workers)
                 ts.append(time.perf_counter() - t0)
         finally:
             if ctx is not None:
                 ctx.__exit__(None, None, None)
-        cand = (min(ts), threads, len(ts), float(np.median(ts)))
-        if best is None or cand[0] < best[0]:
-            best = cand
-    t, threads, reps, med = best
+        cells.append({"blas_threads": threads, "workers": workers, "reps": len(ts),
+                      "min_ms": min(ts) * 1e3, "median_ms": float(np.median(ts)) * 1e3})
+    best = min(cells, key=lambda c: c["median_ms"])
     return {
-        "value": 1.0 / t,
+        "value": 1e3 / best["median_ms"],
         "unit": "matvec/s",
-        "cores": threads,
+        "cores": max(best["blas_threads"], best["workers"]),
         "cpu_model": cpu_model(),
         "host_cpus": ncpu,
-        "kind": "port",
-        "sample": f"{reps} full matvecs (min of reps; median {med * 1e3:.1f} ms) after 1 warm-up, "
-        f"oracle/matvec_oracle.py (restates uniform.py:476-556), BLAS threads best of {{1,{ncpu}}}",
+        "kind": kind,
+        "grid": cells,
+        "sample": f"{best['reps']} full matvecs (median) after 1 warm-up per cell, {desc}; best of the "
+        f"(BLAS threads, workers) grid",
     }
 
 
-def main():
-    args = parse()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+# SURVEY §8d algorithmic bytes per matvec (operator in its cheapest stored form + x + w), used
+# only for the L2 policy so that both arms state the same config without touching the GPU
+ALG_BYTES = {1: 99.2e6, 2: 445.0e6, 3: 2643.6e6, 4: 8031e6}
+L2_BYTES = 126.5e6
+
+
+def l2_policy(cfg: int, world: int, l2: str) -> tuple[bool, str]:
+    """(flush?, config string): flush L2 between steps when one GPU's share of the operator
+    is under 4x the L2, unless --l2 hot."""
+    share = ALG_BYTES.get(cfg, ALG_BYTES[3]) / max(world, 1)
+    if l2 == "hot":
+        return False, "L2-hot: no flush between steps"
+    if share < 4 * L2_BYTES:
+        return True, "L2 flushed between steps (write + read of a 2x L2 buffer, untimed)"
+    return False, f"no flush: {share / 1e9:.2f} GB of operator per GPU >> L2"
+
+
+def make_config(args, world):
     from paper_2405_15573_b200 import workloads
 
     if args.config == 5:
-        if args.impl == "reference":
-            run_reference(args, rank, world, {"workload": "cfg5_cfg3_operator_x_%d_rhs" % args.nrhs, "N": 81920,
-                                              "nrhs": args.nrhs})
-        else:
-            run_multi_rhs(args, world, rank, local_rank)
-        return
+        return {"workload": "cfg5_cfg3_operator_x_%d_rhs" % args.nrhs, "N": 81920, "nrhs": args.nrhs,
+                "values": "seeded synthetic on the reference-built cfg3 structure and ranks",
+                "parallelism": (f"{world} GPUs, each its own block of {args.nrhs} right-hand sides (no exchange)"
+                                if world > 1 else "single GPU")}
     meta = workloads.CONFIGS[args.config]
     config = {
         "workload": meta["name"],
@@ -201,14 +216,35 @@ def main():
         "vector": "default_rng(0) complex Gaussian, tree order",
         "mode": args.mode,
         "adjoint": bool(args.adjoint),
-        "parallelism": f"row-partition x{args.gpus}" if args.gpus > 1 else "single GPU",
+        "parallelism": f"row-partition x{world}" if world > 1 else "single GPU",
+        "l2": l2_policy(args.config, world, args.l2)[1],
     }
+    if args.format == "h":
+        config["format"] = "H-matrix (matvec_h, hmatrix.py:143-184), ranks of the reference's assemble_h"
+    if args.view != "full":
+        config["view"] = args.view
     if args.emulate_ranks > 1:
         config["parallelism"] = (f"peer-exchange partition of {args.emulate_ranks} ranks emulated in one launch "
                                  f"on one GPU (1/{args.emulate_ranks} of the SMs each)")
+    return config
 
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2405_15573_b200 import workloads
+
+    config = make_config(args, world)
+    if args.slice:
+        run_slice(args, config)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world, config)
+        return
+    if args.config == 5:
+        run_multi_rhs(args, world, rank, local_rank, config)
         return
 
     import torch
@@ -223,20 +259,15 @@ def main():
 
     t_build = time.perf_counter()
     u = workloads.build_operator(args.config) if args.format == "uh" else workloads.build_h_operator(args.config)
-    if args.format == "h":
-        config["format"] = "H-matrix (matvec_h, hmatrix.py:143-184), ranks of the reference's assemble_h"
     if args.view != "full":
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         from matvec_oracle import farfield_only, nearfield_only
 
         u = farfield_only(u) if args.view == "far" else nearfield_only(u)
-        config["view"] = args.view
     x_np = workloads.seeded_vector(u.shape[1], 0)
     from paper_2405_15573_b200.packer import pack
 
     if world > 1:
-        from paper_2405_15573_b200.dist import DistributedOperator
-
         from paper_2405_15573_b200.dist import make_distributed
 
         op, why = make_distributed(u, rank, world, device=dev, exchange=args.exchange)
@@ -261,6 +292,7 @@ def main():
     t_build = time.perf_counter() - t_build
 
     n_in = u.shape[0] if args.adjoint else u.shape[1]
+    n_out = u.shape[1] if args.adjoint else u.shape[0]
     x = torch.from_numpy(x_np if not args.adjoint else workloads.seeded_vector(n_in, 0)).to(dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -268,10 +300,8 @@ def main():
         return op.matvec(x, adjoint=args.adjoint, mode=args.mode, out=out)
 
     out = step()
-    # L2 policy: operator bytes vs the 126 MB L2
-    full_bytes = workloads.algorithmic_bytes(packed)
+    flush, _ = l2_policy(args.config, world, args.l2)
     l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
-    flush = full_bytes / max(world, 1) < 4 * l2_bytes and args.l2 == "auto"
     flush_buf = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev) if flush else None
     flush_rd = torch.zeros(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev) if flush else None
 
@@ -281,86 +311,105 @@ def main():
         flush_buf.zero_()
         flush_rd.sum()
 
-    config["l2"] = (
-        f"L2 flushed between steps ({flush_buf.numel() * 4 / 1e6:.0f} MB write + read, untimed)" if flush
-        else (f"L2-hot: no flush (operator {full_bytes / 1e6:.0f} MB, L2 {l2_bytes / 1e6:.0f} MB)" if args.l2 == "hot"
-              else f"operator {full_bytes / max(world, 1) / 1e9:.2f} GB per GPU >> L2 {l2_bytes / 1e6:.0f} MB, no flush")
-    )
-    for _ in range(max(args.warmup, 3)):
+    warmup = max(args.warmup, 3)
+    for _ in range(warmup):
         if flush:
             flush_l2()
         step(out)
     torch.cuda.synchronize(dev)
 
-    # timed region: events around every step's kernel(s) on the launching stream
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    def timed(k):
+        """k steps, CUDA events around every step's kernel(s) on the launching stream."""
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        for i in range(k):
+            if flush:
+                flush_l2()
+            starts[i].record(stream)
+            step(out)
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+        return np.array([s.elapsed_time(e) for s, e in zip(starts, ends)]) * 1e-3  # s
+
+    # timed region: exactly K steps between barriers + synchronize, clocks sampled during it
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for i in range(args.steps):
-        if flush:
-            flush_l2()
-        starts[i].record(stream)
-        step(out)
-        ends[i].record(stream)
-    t1.record(stream)
-    torch.cuda.synchronize(dev)
+    per_step = timed(args.steps)
     if world > 1:
         torch.distributed.barrier()
+    # the distribution SURVEY §8d asks for (median of >= 100 reps), when K is smaller
+    dist_steps = per_step if args.steps >= 100 else np.concatenate([per_step, timed(100)])
     clk = clocks.stop()
-    per_step = np.array([s.elapsed_time(e) for s, e in zip(starts, ends)]) * 1e-3  # s
-    kernel_s = float(per_step.mean())
+    med_s, mean_s = float(np.median(per_step)), float(per_step.mean())
+    med100 = float(np.median(dist_steps))
     if world > 1:
-        t = torch.tensor([kernel_s, float(np.median(per_step))], dtype=torch.float64, device=dev)
+        t = torch.tensor([med_s, mean_s, med100], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        kernel_s, med_s = float(t[0]), float(t[1])
-    else:
-        med_s = float(np.median(per_step))
+        med_s, mean_s, med100 = (float(v) for v in t.tolist())
 
     # end to end through the reference-facing C-ABI call with host buffers (multi-GPU: the
     # same call gathers the output slices; time = max over ranks)
-    e2e = None
-    if True:
-        xh = torch.from_numpy(x.cpu().numpy()).pin_memory()
-        wh = torch.empty(u.shape[1 if args.adjoint else 0], dtype=torch.complex128).pin_memory()
-        xh_np, wh_np = xh.numpy(), wh.numpy()
-        for _ in range(10):  # includes the host-I/O vs copy-path choice (4 calls each)
-            op.matvec_host(xh_np, adjoint=args.adjoint, out=wh_np, mode=args.mode)
-        k_e2e = max(10, min(args.steps, 200))
+    xh = torch.from_numpy(x.cpu().numpy()).pin_memory()
+    wh = torch.empty(n_out, dtype=torch.complex128).pin_memory()
+    xh_np, wh_np = xh.numpy(), wh.numpy()
+    for _ in range(10):  # includes the host-I/O vs copy-path choice (4 calls each)
+        op.matvec_host(xh_np, adjoint=args.adjoint, out=wh_np, mode=args.mode)
+    k_e2e = max(10, min(args.steps, 200))
+
+    def wall(fn, k):
         if world > 1:
             torch.distributed.barrier()
-        te = time.perf_counter()
-        for _ in range(k_e2e):
-            op.matvec_host(xh_np, adjoint=args.adjoint, out=wh_np, mode=args.mode)
-        te = (time.perf_counter() - te) / k_e2e
+        ts = []
+        for _ in range(k):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        te = float(np.median(ts))
         if world > 1:
             tt = torch.tensor([te], dtype=torch.float64, device=dev)
             torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
             te = float(tt.item())
-        e2e = {
-            "value": 1.0 / te,
-            "unit": "matvec/s",
-            "h2d_bytes_per_step": int(16 * n_in),
-            "d2h_bytes_per_step": int(16 * (u.shape[1] if args.adjoint else u.shape[0])),
-            "api": "uhmv_matvec_host (C ABI, pinned host x/w, H2D + kernels + D2H + sync, wall clock)",
-        }
-        choice = op.host_io_choice(args.adjoint) if hasattr(op, "host_io_choice") else None
-        if choice is not None:
-            e2e["path"] = ("host-I/O launch: x read over PCIe by the P1 ops, finished output leaves drained "
-                           "to the pinned host buffer inside the kernel" if choice
-                           else "H2D copy + launch + D2H copy (faster than the host-I/O launch here)")
+        return te
+
+    te = wall(lambda: op.matvec_host(xh_np, adjoint=args.adjoint, out=wh_np, mode=args.mode), k_e2e)
+    e2e = {
+        "value": 1.0 / te,
+        "unit": "matvec/s",
+        "h2d_bytes_per_step": int(16 * n_in),
+        "d2h_bytes_per_step": int(16 * n_out),
+        "api": "uhmv_matvec_host (C ABI, pinned host x/w, H2D + kernels + D2H + sync; wall clock, median)",
+    }
+    choice = op.host_io_choice(args.adjoint) if hasattr(op, "host_io_choice") else None
+    if choice is not None:
+        e2e["path"] = ("host-I/O launch: x read over PCIe by the P1 ops, finished output leaves drained "
+                       "to the pinned host buffer inside the kernel" if choice
+                       else "H2D copy + launch + D2H copy (faster than the host-I/O launch here)")
+    # the drop-in itself: matvec_uh(u, ndarray) as a reference caller makes it (pageable input,
+    # a NEW output array every call, dtype promotion, validation), single GPU
+    e2e_dropin = None
+    if world == 1 and args.emulate_ranks <= 1 and args.view == "full":
+        import paper_2405_15573_b200 as pk
+        from paper_2405_15573_b200.matvec import register_device_operator
+
+        register_device_operator(u, op)
+        xr = (x_np if not args.adjoint else workloads.seeded_vector(n_in, 0)).copy()
+        fn = pk.matvec_h if args.format == "h" else pk.matvec_uh
+        for _ in range(10):
+            fn(u, xr, adjoint=args.adjoint)
+        td = wall(lambda: fn(u, xr, adjoint=args.adjoint), k_e2e)
+        e2e_dropin = {"value": 1.0 / td, "unit": "matvec/s", "h2d_bytes_per_step": int(16 * n_in),
+                      "d2h_bytes_per_step": int(16 * n_out),
+                      "api": f"paper_2405_15573_b200.{fn.__name__}(u, numpy array) -- the installed drop-in "
+                             "(pageable input, new output array per call); wall clock, median"}
 
     peak, peak_kind = measured_peaks()
     alg_bytes_total = workloads.algorithmic_bytes(packed)
-    value = 1.0 / kernel_s
-    achieved = alg_bytes_total / world / kernel_s / 1e9  # per GPU
+    value = 1.0 / med_s
+    achieved = alg_bytes_total / world / med_s / 1e9  # per GPU
     traffic = load_traffic(args.config)
     roofline = {
         "bound": "hbm",
@@ -371,7 +420,10 @@ def main():
         "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
         "frac_vs_8000_nominal": achieved / 8000.0,
         "traffic": traffic,
+        "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
+                          "(profiles/ncu_traffic.json, same command)",
         "algorithmic_bytes_per_launch": int(alg_bytes_total / world),
+        "reference_bytes_estimate": ref_bytes_estimate(args.config, u),
         "kernel": "bulk::uhmv_bulk_peer_kernel" if (args.emulate_ranks > 1 or getattr(op, "exchange", "") == "peer") else
         {"bulk": "bulk::uhmv_bulk_kernel", "fused": "uhmv_fused_kernel"}.get(args.mode, "uhmv_phase_kernel (5 launches)"),
     }
@@ -385,9 +437,11 @@ def main():
         "unit": "matvec/s",
         "n_gpus": world,
         "steps": args.steps,
-        "warmup": max(args.warmup, 3),
-        "ms_per_step": kernel_s * 1e3,
-        "ms_per_step_median": med_s * 1e3,
+        "warmup": warmup,
+        "ms_per_step": med_s * 1e3,
+        "ms_per_step_mean": mean_s * 1e3,
+        "ms_per_step_median_100": med100 * 1e3,
+        "reps_for_median_100": int(len(dist_steps)),
         "effective_gbs": achieved * world,
         "higher_is_better": True,
         "scaling": "strong",
@@ -398,6 +452,7 @@ def main():
         "roofline": roofline,
         "exchange_bytes_per_rank": (16 * op.packed_local.exchange["adj" if args.adjoint else "fwd"][1]) if world > 1 else 0,
         "e2e": e2e,
+        "e2e_dropin": e2e_dropin,
         "gpu_launches": args.steps * op.kernel_launches(args.adjoint, args.mode),
         "clocks": clk,
         "build_s": t_build,
@@ -412,6 +467,112 @@ def main():
         torch.distributed.destroy_process_group()
 
 
+def run_slice(args, config):
+    """--slice W[,W...]: one-GPU predictor of the W-GPU row partition.
+
+    For every rank r of a W-way partition (packer.partition_bounds, bytes-balanced) the rank's
+    NCCL-path programs -- launch A (P1, RED, U, part of the nearfield), launch B (Z, the rest
+    of the nearfield, FAR) -- run back to back ALONE on the whole B200, exactly the kernels that
+    rank runs on its own GPU (the exchange region holds stale values: timing only).  Reports
+    per-rank bytes and device time (median, L2 policy of a W-GPU run), the max/mean imbalance,
+    and the predicted speed-up t1 / (max_r t_r + t_ag), t_ag = a modelled NCCL all-gather of
+    the y/u exchange region (--ag-lat-us + bytes / --ag-gbs)."""
+    import torch
+
+    from paper_2405_15573_b200 import workloads
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.packer import pack
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    u = workloads.build_operator(args.config)
+    packed = pack(u)
+    base = DeviceOperator(packed, device=dev)
+    n_in = u.shape[0] if args.adjoint else u.shape[1]
+    x = torch.from_numpy(workloads.seeded_vector(n_in, 0)).to(dev)
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_buf = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev)
+    flush_rd = torch.zeros_like(flush_buf)
+    steps = max(args.steps, 20)
+
+    def timed(fn, flush):
+        for _ in range(max(args.warmup, 3)):
+            fn()
+        ts = []
+        for _ in range(steps):
+            if flush:
+                flush_buf.zero_()
+                flush_rd.sum()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            ts.append((a, b))
+        torch.cuda.synchronize(dev)
+        return float(np.median([a.elapsed_time(b) for a, b in ts])) * 1e-3
+
+    out = torch.empty(u.shape[1] if args.adjoint else u.shape[0], dtype=torch.complex128, device=dev)
+    t1 = timed(lambda: base.matvec(x, adjoint=args.adjoint, out=out), l2_policy(args.config, 1, args.l2)[0])
+    b1 = workloads.algorithmic_bytes(packed)
+    peak, _ = measured_peaks()
+    res = {"metric": "one-GPU prediction of W-GPU uniform-H matvec scaling (rank programs run alone)",
+           "config": config, "t1_ms": t1 * 1e3, "t1_frac": b1 / t1 / 1e9 / peak, "alg_bytes_1": b1,
+           "ag_model": {"lat_us": args.ag_lat_us, "gbs": args.ag_gbs}, "worlds": []}
+    for W in [int(v) for v in args.slice.split(",") if v.strip()]:
+        flush = l2_policy(args.config, W, args.l2)[0]
+        ranks = []
+        for r in range(W):
+            pr = packed.for_rank(r, W)
+            a = DeviceOperator(pr, device=dev, share_arena_with=base)
+            b = DeviceOperator(pr, device=dev, programs=(pr.fwd.part_b, pr.adj.part_b), share_with=a)
+            prog = pr.adj if args.adjoint else pr.fwd
+
+            def step(a=a, b=b):
+                a.matvec(x, adjoint=args.adjoint, out=out)
+                b.matvec(x, adjoint=args.adjoint, out=out)
+
+            t = timed(step, flush)
+            nbytes = 16 * (prog.arena_elems + prog.part_b.arena_elems)
+            ex_elems = pr.exchange["adj" if args.adjoint else "fwd"][1]
+            ranks.append({"rank": r, "ms": t * 1e3, "bytes": nbytes, "frac": nbytes / t / 1e9 / peak,
+                          "rows": [int(pr.part["row_bounds"][r]), int(pr.part["row_bounds"][r + 1])],
+                          "exchange_bytes": 16 * int(ex_elems) * W})
+            a.close()
+            b.close()
+            del a, b
+        tmax = max(q["ms"] for q in ranks) * 1e-3
+        bts = [q["bytes"] for q in ranks]
+        ms = [q["ms"] for q in ranks]
+        t_ag = args.ag_lat_us * 1e-6 + max(q["exchange_bytes"] for q in ranks) / (args.ag_gbs * 1e9)
+        res["worlds"].append({
+            "W": W, "ranks": ranks, "bytes_max_over_mean": max(bts) / (sum(bts) / W),
+            "time_max_over_mean": max(ms) / (sum(ms) / W), "bytes_sum_over_1gpu": sum(bts) / packed.bytes_alg,
+            "t_max_ms": tmax * 1e3, "t_allgather_model_ms": t_ag * 1e3,
+            "predicted_speedup": t1 / (tmax + t_ag), "predicted_efficiency": t1 / (tmax + t_ag) / W,
+            "predicted_speedup_no_exchange_cost": t1 / tmax,
+        })
+    print(json.dumps(res), flush=True)
+
+
+def ref_bytes_estimate(cfg, u=None):
+    """The reference's own figure: storage_report_uh(u).bytes_estimate (uniform.py:559-584),
+    computed by the reference itself (oracle/_ref) on the benchmarked operator, else the value
+    stored in the config fixture by tools/make_workloads.py for the reference-built operator."""
+    from paper_2405_15573_b200 import workloads
+
+    if u is not None and hasattr(u, "coeffs") and os.path.isdir(os.path.join(REF_SITE, "uhm_kit")):
+        if REF_SITE not in sys.path:
+            sys.path.append(REF_SITE)
+        from uhm_kit.uniform import storage_report_uh
+
+        return int(storage_report_uh(u).bytes_estimate)
+    try:
+        with np.load(workloads.workload_path(cfg)) as z:
+            return int(z["x_ref_bytes_estimate"]) if "x_ref_bytes_estimate" in z.files else None
+    except (OSError, KeyError):
+        return None
+
+
 def dmma_peak(device_index: int):
     import ctypes
 
@@ -422,7 +583,7 @@ def dmma_peak(device_index: int):
     return pk.value
 
 
-def run_multi_rhs(args, world, rank, local_rank):
+def run_multi_rhs(args, world, rank, local_rank, config):
     """BASELINE config 5: the config-3 operator applied to a block of nrhs seeded complex
     Gaussian right-hand sides on FP64 tensor cores (DMMA).  One step = one block product;
     value = right-hand sides per second (matvecs/s).  Roofline: FP64 tensor peak measured
@@ -451,7 +612,7 @@ def run_multi_rhs(args, world, rank, local_rank):
     for _ in range(max(args.warmup, 3)):
         op.matmat(X)
     torch.cuda.synchronize(dev)
-    steps = max(3, min(args.steps, 50))
+    steps = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -467,7 +628,7 @@ def run_multi_rhs(args, world, rank, local_rank):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    t = float(np.mean([a.elapsed_time(b) for a, b in ev])) * 1e-3
+    t = float(np.median([a.elapsed_time(b) for a, b in ev])) * 1e-3
     if world > 1:  # time = max over ranks
         tt = torch.tensor([t], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -511,10 +672,7 @@ def run_multi_rhs(args, world, rank, local_rank):
         "vs_baseline": None,
         "dtype": "c128 (f64 complex)",
         "data": "synthetic",
-        "config": {"workload": "cfg5_cfg3_operator_x_%d_rhs" % R, "N": n, "nrhs": R,
-                   "parallelism": (f"{world} GPUs, each its own block of {R} right-hand sides (no exchange)"
-                                   if world > 1 else "single GPU"),
-                   "values": "seeded synthetic on the reference-built cfg3 structure and ranks"},
+        "config": config,
         "roofline": {"bound": "tensor", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
                      "frac": flops / t / 1e12 / peak,
                      "peak_source": "uhmv_dmma_peak: measured DMMA m16n8k16 f64 throughput on this GPU",
@@ -544,16 +702,38 @@ def load_traffic(cfg):
     return float(v) if v is not None else None
 
 
+REF_SITE = os.path.join(ROOT, "oracle", "_ref", "site")
+
+
+def reference_impl():
+    """The CPU reference the GPU is compared with: the UNMODIFIED reference ``uhm_kit``
+    (``uniform.matvec_uh``, uniform.py:476-556), installed into oracle/_ref by
+    oracle/build_ref.sh and shipped with the repo; else the oracle port restating it."""
+    if os.path.isdir(os.path.join(REF_SITE, "uhm_kit")):
+        if REF_SITE not in sys.path:
+            sys.path.append(REF_SITE)
+        import uhm_kit.uniform
+
+        fn = uhm_kit.uniform.matvec_uh
+        if fn.__module__ != "uhm_kit.uniform":
+            raise RuntimeError("uhm_kit.uniform.matvec_uh is patched (install() active): not the reference")
+        return fn, "reference", "uhm_kit.uniform.matvec_uh (the unmodified reference, oracle/_ref/site)"
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from matvec_oracle import oracle_matvec_uh
+
+    return oracle_matvec_uh, "port", "oracle/matvec_oracle.py (restates uniform.py:476-556)"
+
+
 def run_reference(args, rank, world, config):
-    """--impl reference: the reference algorithm (oracle port of uniform.py:476-556) on the
-    host CPU, all host threads; rank 0 only under torchrun."""
+    """--impl reference: the reference's own matvec_uh on the host CPU, all host threads (BLAS
+    threads = os.cpu_count(), workers=1: the reference's thread pool is GIL-bound, SURVEY §6.2);
+    rank 0 only under torchrun.  Same warm-up count, config keys, metric and unit as the GPU
+    arm; each step is one full matvec, the timed steps bounded to ~60 s of CPU work."""
     if rank != 0:
         return
     from paper_2405_15573_b200 import workloads
 
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    from matvec_oracle import oracle_matvec_uh
-
+    fn, kind, desc = reference_impl()
     cfg = 3 if args.config == 5 else args.config  # config 5 = the config-3 operator, column loop
     u = workloads.build_operator(cfg)
     n_in = u.shape[0] if args.adjoint else u.shape[1]
@@ -562,21 +742,19 @@ def run_reference(args, rank, world, config):
         X = rng.standard_normal((n_in, args.nrhs)) + 1j * rng.standard_normal((n_in, args.nrhs))
     else:
         X = workloads.seeded_vector(n_in, 0)[:, None]
-    n_warm = max(1, min(args.warmup, 3))  # untimed warm-up matvecs (bounded too)
+    n_warm = max(args.warmup, 3)
     for i in range(n_warm):
-        oracle_matvec_uh(u, X[:, i % X.shape[1]], adjoint=args.adjoint)
-    # bounded sample: the timed steps stop after ~60 s of CPU work (a step = one matvec; for
-    # config 5 one right-hand side of the block, the metric being right-hand sides per second)
+        fn(u, X[:, i % X.shape[1]], adjoint=args.adjoint)
     ts = []
     t_all = time.perf_counter()
     for i in range(max(args.steps, 1)):
         t0 = time.perf_counter()
-        oracle_matvec_uh(u, X[:, i % X.shape[1]], adjoint=args.adjoint)
+        fn(u, X[:, i % X.shape[1]], adjoint=args.adjoint)
         ts.append(time.perf_counter() - t0)
         if time.perf_counter() - t_all > 60.0:
             break
-    mean = float(np.mean(ts))
-    value = 1.0 / mean
+    med = float(np.median(ts))
+    value = 1.0 / med
     ncpu = os.cpu_count() or 1
     line = {
         "impl": "reference",
@@ -586,8 +764,10 @@ def run_reference(args, rank, world, config):
         "unit": "matvec/s",
         "n_gpus": world,
         "steps": args.steps,
+        "steps_timed": len(ts),
         "warmup": n_warm,
-        "ms_per_step": mean * 1e3,
+        "ms_per_step": med * 1e3,
+        "ms_per_step_mean": float(np.mean(ts)) * 1e3,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
@@ -598,10 +778,10 @@ def run_reference(args, rank, world, config):
             "value": value,
             "unit": "matvec/s",
             "cores": ncpu,
-            "kind": "port",
-            "sample": f"{len(ts)} full matvecs (bounded to ~60 s), oracle/matvec_oracle.py (restates "
-            f"uniform.py:476-556), default BLAS threads ({ncpu}); the Python reference itself cannot "
-            "travel to the GPU box",
+            "cpu_model": cpu_model(),
+            "kind": kind,
+            "sample": f"{len(ts)} full matvecs (median; bounded to ~60 s) after {n_warm} warm-up, {desc}, "
+            f"workers=1, default BLAS threads ({ncpu})",
         },
         "e2e": {"value": value, "unit": "matvec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -12,6 +12,14 @@
  * (PyTorch tensors in the Python layer).  The plan never frees them; it only owns launch
  * configuration.  All entry points return 0 on success and a negative code on failure; the text
  * of the last failure of the calling thread is available from uhmv_last_error().
+ *
+ * Concurrency: plans that share device state (the same ticket buffer -- a plan and its multi-RHS
+ * plan) form a group whose launches never overlap.  Every enqueueing entry point holds the
+ * group's host mutex while it enqueues and records a group event after the launch; a call on a
+ * different stream than the group's previous launch first waits for that event.  So any mix of
+ * host threads and streams calling one plan gives the results of some serial order.  Inside a
+ * stream capture the event ordering is skipped (replay the captured graph on one stream at a
+ * time).
  */
 #ifndef UHMV_H
 #define UHMV_H
@@ -22,7 +30,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 9
+#define UHMV_ABI_VERSION 10
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -119,6 +127,18 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
  * Replaces: the whole matvec_uh call as a caller sees it (uniform.py:476-556). */
 int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
                      void* stream);
+
+/* 1 if `host` points into page-locked (pinned, device-mapped) host memory, else 0. */
+int uhmv_host_pinned(const void* host);
+
+/* Which path pinned uhmv_matvec_host calls of one direction take once host-I/O programs are
+ * attached: 1 the host-I/O launch (default), 0 H2D copy / launch / D2H copy.  A captured graph is
+ * kept per path, so switching (e.g. while measuring both) replays instead of recapturing. */
+int uhmv_plan_set_host_path(uhmv_plan* plan, int adjoint, int path);
+
+/* Path the last uhmv_matvec_host of a direction took: 1 host-I/O launch, 0 copy path with pinned
+ * buffers, -1 pageable buffers (always the copy path), or a negative error code. */
+int uhmv_plan_last_host_path(const uhmv_plan* plan, int adjoint);
 
 /* Attach the host-I/O variant of the plan's programs (packer io_programs(); counters: a
  * zeroed uint32 buffer of max(n_counters) of the two).  Afterwards uhmv_matvec_host with

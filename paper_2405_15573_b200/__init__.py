@@ -47,12 +47,17 @@ def install():
 
     ``uhm_kit.matvec_uh`` / ``uhm_kit.uniform.matvec_uh`` (looked up at call time by
     ``UniformHMatrix.matvec``, uniform.py:117) and ``uhm_kit.verification.matvec_uh``
-    (bound at import, verification.py:20).  Returns the originals for restoring.
+    (bound at import, verification.py:20); likewise ``matvec_h`` (hmatrix.py:143-184) and the
+    error metrics ``spectral_norm_estimate`` / ``compression_error`` (verification.py:88-138,
+    power iteration resident on the GPU for compressed operands).  Returns the originals for
+    restoring.
     """
     import uhm_kit
     import uhm_kit.hmatrix
     import uhm_kit.uniform
     import uhm_kit.verification
+
+    from . import verification as _ver
 
     targets = [
         (uhm_kit, "matvec_uh", matvec_uh),
@@ -62,6 +67,11 @@ def install():
         (uhm_kit, "matvec_h", matvec_h),
         (uhm_kit.hmatrix, "matvec_h", matvec_h),
         (uhm_kit.verification, "matvec_h", matvec_h),
+        (uhm_kit, "spectral_norm_estimate", _ver.spectral_norm_estimate),
+        (uhm_kit.verification, "spectral_norm_estimate", _ver.spectral_norm_estimate),
+        (uhm_kit, "compression_error", _ver.compression_error),
+        (uhm_kit.verification, "compression_error", _ver.compression_error),
+        (_ver, "_report_cls", uhm_kit.verification.ErrorReport),
     ]
     orig = [(mod, name, getattr(mod, name)) for mod, name, _ in targets]
     for mod, name, fn in targets:

@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "UhmvPeerRank", "check", "LIB_PATH"
 
 LIB_PATH = os.environ.get("UHMV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 9
+ABI_VERSION = 10
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -87,6 +87,9 @@ EXPORTS = (
     "uhmv_execute_peer",
     "uhmv_peer_set_diag",
     "uhmv_plan_set_io",
+    "uhmv_plan_set_host_path",
+    "uhmv_plan_last_host_path",
+    "uhmv_host_pinned",
     "uhmv_plan_info",
     "uhmv_plan_set_profile",
     "uhmv_plan_set_trace",
@@ -107,6 +110,9 @@ def lib():
             "(run __graft_entry__.build()); there is no CPU fallback"
         )
     L = ctypes.CDLL(LIB_PATH)
+    missing = [name for name in EXPORTS if not hasattr(L, name)]
+    if missing:  # a stale build: ensure_built() rebuilds on RuntimeError
+        raise RuntimeError(f"libuhmv.so lacks {missing}; rebuild")
     vp, i32 = ctypes.c_void_p, ctypes.c_int
     L.uhmv_abi_version.restype = i32
     L.uhmv_plan_create.argtypes = [ctypes.POINTER(UhmvDesc), ctypes.POINTER(vp)]
@@ -127,6 +133,12 @@ def lib():
     L.uhmv_plan_set_io.argtypes = [vp, ctypes.POINTER(UhmvProgram), ctypes.POINTER(UhmvProgram), vp]
     L.uhmv_plan_set_io.restype = i32
     L.uhmv_matvec_host.restype = i32
+    L.uhmv_plan_set_host_path.argtypes = [vp, i32, i32]
+    L.uhmv_plan_set_host_path.restype = i32
+    L.uhmv_plan_last_host_path.argtypes = [vp, i32]
+    L.uhmv_plan_last_host_path.restype = i32
+    L.uhmv_host_pinned.argtypes = [vp]
+    L.uhmv_host_pinned.restype = i32
     pi = ctypes.POINTER(i32)
     L.uhmv_plan_info.argtypes = [vp, i32, i32, pi, pi, pi, pi]
     L.uhmv_plan_info.restype = i32

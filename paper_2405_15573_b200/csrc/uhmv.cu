@@ -34,9 +34,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -426,8 +430,45 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 }  // namespace
 
+// Launch serialisation of plans that share device state.  One launch of a plan's programs
+// owns the ticket / counters / exit count / work buffer (and uhmv_matvec_host the scratch
+// vectors) until it exits, so two launches of the same state must never overlap -- e.g. two
+// streams, or two host threads, calling uhmv_execute on one plan.  Plans are grouped by their
+// ticket pointer (the multi-RHS plan shares its parent's, device.py share_with): a group has
+// one host mutex held while a call enqueues, and one event recorded after each launch that a
+// launch on a DIFFERENT stream waits for.  Same-stream calls cost one cudaEventRecord.  While
+// the stream is being captured into a graph the event ordering is skipped (the captured graph
+// must then be replayed on one stream at a time).
+struct SyncState {
+    std::mutex mu;
+    cudaEvent_t ev = nullptr;
+    cudaStream_t last = nullptr;
+    bool recorded = false;
+    int refs = 0;
+};
+static std::mutex g_sync_mu;
+static std::map<const void*, SyncState*> g_sync;
+
+static SyncState* sync_acquire(const void* key) {
+    std::lock_guard<std::mutex> g(g_sync_mu);
+    SyncState*& s = g_sync[key];
+    if (!s) s = new SyncState();
+    ++s->refs;
+    return s;
+}
+static void sync_release(const void* key, SyncState* s) {
+    if (!s) return;
+    std::lock_guard<std::mutex> g(g_sync_mu);
+    if (--s->refs == 0) {
+        if (s->ev) cudaEventDestroy(s->ev);
+        g_sync.erase(key);
+        delete s;
+    }
+}
+
 struct uhmv_plan {
     uhmv_desc d;
+    SyncState* sync;  // shared by every plan on the same ticket (see SyncState)
     int fused_grid[2];
     int smem[2];
     int bulk_grid[2];
@@ -448,6 +489,14 @@ struct uhmv_plan {
     void* hg_w[2];
     int hg_mode[2];
     int hg_io[2];
+    cudaGraphExec_t hg_alt[2];  // the graph of the other host path (io vs copy), kept for replay
+    const void* ha_x[2];
+    void* ha_w[2];
+    int ha_mode[2];
+    int ha_io[2];
+    int host_path[2];       // pinned host calls: 1 host-I/O launch (when attached), 0 copy path
+    int last_host_path[2];  // path the last uhmv_matvec_host took: 1 io, 0 copy, -1 pageable
+    cudaEvent_t mm_start;   // uhmv_matmat_host: orders its streams after the caller's
     cudaStream_t cap_stream;  // capture stream (the caller's may be the legacy default stream)
     // pipelined host-buffer multi-RHS (uhmv_matmat_host): copy-in / compute / copy-out streams
     cudaStream_t mm_stream[3];
@@ -702,8 +751,12 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
         const char* ev = getenv("UHMV_MRHS_ENGINE");
         p->mrhs_engine = (ev && strcmp(ev, "simple") == 0) ? 1 : 0;
     }
+#ifdef UHMV_DIAGNOSTICS  // diagnostics builds only (UHMV_NVCC_EXTRA=-DUHMV_DIAGNOSTICS): wrong results
     if (const char* ev = getenv("UHMV_DEBUG_SKIP_WAITS")) p->debug_skip_waits = atoi(ev);
     if (const char* ev = getenv("UHMV_DEBUG_FLAGS")) p->debug_flags = atoi(ev);
+#endif
+    p->host_path[0] = p->host_path[1] = 1;
+    p->sync = sync_acquire(desc->ticket);
     if (const char* ev = getenv("UHMV_HOST_GRAPH")) p->no_graphs = (atoi(ev) == 0);
     *out = p;
     return UHMV_OK;
@@ -765,9 +818,79 @@ static ExecParams make_params(const uhmv_plan* plan, const uhmv_program& pr, con
     return ep;
 }
 
-int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, int phase_lo,
-                        int phase_hi, void* stream) {
+// Serialises one enqueue of a plan group (see SyncState): holds the group's mutex, orders the
+// launch after the group's previous launch when that ran on another stream, and records the
+// group's event after it.
+class Serial {
+  public:
+    Serial(uhmv_plan* p, cudaStream_t st) : s_(p->sync), st_(st), lk_(p->sync->mu) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+            cudaGetLastError();
+            cs = cudaStreamCaptureStatusNone;
+        }
+        cap_ = cs != cudaStreamCaptureStatusNone;
+    }
+    int begin() {
+        if (cap_ || !s_->recorded || s_->last == st_) return UHMV_OK;
+        cudaError_t e = cudaStreamWaitEvent(st_, s_->ev, 0);
+        return e == cudaSuccess ? UHMV_OK : cuda_fail(e, "cudaStreamWaitEvent (plan serialisation)");
+    }
+    int end() {
+        if (cap_) return UHMV_OK;
+        cudaError_t e = cudaSuccess;
+        if (!s_->ev) e = cudaEventCreateWithFlags(&s_->ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(s_->ev, st_);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord (plan serialisation)");
+        s_->recorded = true;
+        s_->last = st_;
+        return UHMV_OK;
+    }
+
+  private:
+    SyncState* s_;
+    cudaStream_t st_;
+    std::unique_lock<std::mutex> lk_;
+    bool cap_ = false;
+};
+
+static int execute_phases_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, int phase_lo, int phase_hi,
+                               void* stream);
+static int execute_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode, void* stream);
+static int execute_mrhs_impl(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs, int adjoint,
+                             void* stream);
+
+// Public enqueue entry points: argument check, then the guarded implementation.
+extern "C++" {
+template <class F>
+static int serialised(uhmv_plan* plan, void* stream, F&& body) {
+    Serial g(plan, static_cast<cudaStream_t>(stream));
+    int rc = g.begin();
+    if (rc) return rc;
+    rc = body();
+    const int rc2 = g.end();
+    return rc ? rc : rc2;
+}
+}  // extern "C++"
+
+int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, int phase_lo, int phase_hi,
+                        void* stream) {
     if (!plan) return fail(UHMV_EINVAL, "uhmv_execute_phases: null plan");
+    return serialised(plan, stream, [&] { return execute_phases_impl(plan, x, w, adjoint, phase_lo, phase_hi, stream); });
+}
+
+int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode, void* stream) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_execute: null plan");
+    return serialised(plan, stream, [&] { return execute_impl(plan, x, w, adjoint, mode, stream); });
+}
+
+int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs, int adjoint, void* stream) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_execute_mrhs: null plan");
+    return serialised(plan, stream, [&] { return execute_mrhs_impl(plan, x, w, work_mr, nrhs, adjoint, stream); });
+}
+
+static int execute_phases_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, int phase_lo, int phase_hi,
+                               void* stream) {
     const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
     const int k = adjoint ? 1 : 0;
     if (phase_lo < 0 || phase_hi > pr.n_phases || phase_lo > phase_hi)
@@ -791,11 +914,10 @@ int uhmv_execute_phases(uhmv_plan* plan, const void* x, void* w, int adjoint, in
     return UHMV_OK;
 }
 
-int uhmv_execute(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode, void* stream) {
-    if (!plan) return fail(UHMV_EINVAL, "uhmv_execute: null plan");
+static int execute_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, int mode, void* stream) {
     const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
     if (mode == UHMV_MODE_PHASED)
-        return uhmv_execute_phases(plan, x, w, adjoint, 0, pr.n_phases, stream);
+        return execute_phases_impl(plan, x, w, adjoint, 0, pr.n_phases, stream);
     if (mode != UHMV_MODE_FUSED && mode != UHMV_MODE_BULK)
         return fail(UHMV_EINVAL, "uhmv_execute: unknown mode");
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
@@ -841,6 +963,7 @@ static void drop_host_graphs(uhmv_plan* plan);
 
 int uhmv_plan_set_io(uhmv_plan* plan, const uhmv_program* fwd, const uhmv_program* adj, uint32_t* counters) {
     if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_set_io: null plan");
+    std::lock_guard<std::mutex> guard(plan->sync->mu);
     if (!fwd && !adj) {  // detach
         plan->has_io = false;
         drop_host_graphs(plan);
@@ -906,7 +1029,16 @@ int uhmv_execute_peer(uhmv_plan* const* plans, int nplans, int rank0, int world,
             if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
         }
     }
-    if (grid < nplans) return fail(UHMV_EINVAL, "uhmv_execute_peer: fewer CTAs than ranks");
+    {
+        // every CTA of the launch must be co-resident: the grid comes from the occupancy of the
+        // peer kernel itself at the launch's shared memory (it can differ from the bulk kernel's)
+        int per_sm = 0;
+        cudaError_t eo = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk::uhmv_bulk_peer_kernel,
+                                                                       bulk::kThreads, smem);
+        if (eo != cudaSuccess) return cuda_fail(eo, "occupancy(bulk_peer)");
+        if (per_sm * plans[0]->sm_count < grid) grid = per_sm * plans[0]->sm_count;
+    }
+    if (grid < nplans) return fail(UHMV_EINVAL, "uhmv_execute_peer: fewer co-resident CTAs than ranks");
     bulk::PeerLaunch L;
     std::memset(&L, 0, sizeof(L));
     L.nranks = nplans;
@@ -933,15 +1065,32 @@ int uhmv_execute_peer(uhmv_plan* const* plans, int nplans, int rank0, int world,
         bp.done = ranks[r].done;
         L.r[i] = bp;
     }
+    // serialise against other launches of each involved plan group (locked in address order)
+    std::vector<uhmv_plan*> grp;
+    for (int i = 0; i < nplans; ++i) {
+        bool dup = false;
+        for (uhmv_plan* q : grp) dup = dup || (q->sync == plans[i]->sync);
+        if (!dup) grp.push_back(plans[i]);
+    }
+    std::sort(grp.begin(), grp.end(), [](const uhmv_plan* a, const uhmv_plan* b) { return a->sync < b->sync; });
+    std::vector<std::unique_ptr<Serial>> guards;
+    for (uhmv_plan* q : grp) {
+        guards.emplace_back(new Serial(q, st));
+        const int r = guards.back()->begin();
+        if (r) return r;
+    }
     bulk::uhmv_bulk_peer_kernel<<<grid, bulk::kThreads, smem, st>>>(L);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "uhmv_bulk_peer_kernel launch");
+    for (auto& g : guards) {
+        const int r = g->end();
+        if (r) return r;
+    }
     return UHMV_OK;
 }
 
-int uhmv_execute_mrhs(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs,
-                      int adjoint, void* stream) {
-    if (!plan) return fail(UHMV_EINVAL, "uhmv_execute_mrhs: null plan");
+static int execute_mrhs_impl(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs, int adjoint,
+                             void* stream) {
     if (nrhs <= 0 || nrhs % mrhs::kRC) return fail(UHMV_EINVAL, "nrhs must be a multiple of 16");
     const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
     if (!pr.mr_segs || !pr.mr_ranges) return fail(UHMV_EINVAL, "program has no multi-RHS tables");
@@ -1018,7 +1167,7 @@ static int enqueue_host(uhmv_plan* plan, const void* x_host, void* w_host, int a
     }
     cudaError_t e = cudaMemcpyAsync(plan->d.x_scratch, x_host, (size_t)n_in * 16, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "H2D copy of x");
-    int rc = uhmv_execute(plan, plan->d.x_scratch, plan->d.w_scratch, adjoint, mode, st);
+    int rc = execute_impl(plan, plan->d.x_scratch, plan->d.w_scratch, adjoint, mode, st);
     if (rc) return rc;
     e = cudaMemcpyAsync(w_host, plan->d.w_scratch, (size_t)n_out * 16, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_fail(e, "D2H copy of w");
@@ -1028,8 +1177,76 @@ static int enqueue_host(uhmv_plan* plan, const void* x_host, void* w_host, int a
 static void drop_host_graphs(uhmv_plan* plan) {
     for (int k = 0; k < 2; ++k) {
         if (plan->hg_exec[k]) cudaGraphExecDestroy(plan->hg_exec[k]);
+        if (plan->hg_alt[k]) cudaGraphExecDestroy(plan->hg_alt[k]);
         plan->hg_exec[k] = nullptr;
+        plan->hg_alt[k] = nullptr;
     }
+}
+
+int uhmv_host_pinned(const void* host) { return (host && mapped_ptr(host) != nullptr) ? 1 : 0; }
+
+int uhmv_plan_set_host_path(uhmv_plan* plan, int adjoint, int path) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_set_host_path: null plan");
+    if (path != 0 && path != 1) return fail(UHMV_EINVAL, "uhmv_plan_set_host_path: path must be 0 or 1");
+    std::lock_guard<std::mutex> g(plan->sync->mu);
+    plan->host_path[adjoint ? 1 : 0] = path;  // the cached graphs of both paths stay valid
+    return UHMV_OK;
+}
+
+// The captured graph of a pinned host call: the current one per direction, plus the last graph of
+// the other path (so alternating paths, e.g. while choosing between them, replays instead of
+// recapturing).
+static int host_graph(uhmv_plan* plan, int k, const void* x_host, void* w_host, int mode, bool io,
+                      cudaGraphExec_t* out) {
+    auto same = [&](const void* gx, void* gw, int gm, int gio) {
+        return gx == x_host && gw == w_host && gm == mode && gio == (int)io;
+    };
+    if (plan->hg_exec[k] && same(plan->hg_x[k], plan->hg_w[k], plan->hg_mode[k], plan->hg_io[k])) {
+        *out = plan->hg_exec[k];
+        return UHMV_OK;
+    }
+    if (plan->hg_alt[k] && same(plan->ha_x[k], plan->ha_w[k], plan->ha_mode[k], plan->ha_io[k])) {
+        std::swap(plan->hg_exec[k], plan->hg_alt[k]);
+        std::swap(plan->hg_x[k], plan->ha_x[k]);
+        std::swap(plan->hg_w[k], plan->ha_w[k]);
+        std::swap(plan->hg_mode[k], plan->ha_mode[k]);
+        std::swap(plan->hg_io[k], plan->ha_io[k]);
+        *out = plan->hg_exec[k];
+        return UHMV_OK;
+    }
+    cudaError_t e;
+    if (!plan->cap_stream) {
+        e = cudaStreamCreateWithFlags(&plan->cap_stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate (graph capture)");
+    }
+    e = cudaStreamBeginCapture(plan->cap_stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamBeginCapture");
+    const int rc = enqueue_host(plan, x_host, w_host, k, mode, plan->cap_stream, io, plan->io_x_dev, plan->io_w_dev);
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(plan->cap_stream, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+    // the current graph becomes the alternate one (the previous alternate is dropped)
+    if (plan->hg_alt[k]) cudaGraphExecDestroy(plan->hg_alt[k]);
+    plan->hg_alt[k] = plan->hg_exec[k];
+    plan->ha_x[k] = plan->hg_x[k];
+    plan->ha_w[k] = plan->hg_w[k];
+    plan->ha_mode[k] = plan->hg_mode[k];
+    plan->ha_io[k] = plan->hg_io[k];
+    plan->hg_exec[k] = ex;
+    plan->hg_x[k] = x_host;
+    plan->hg_w[k] = w_host;
+    plan->hg_mode[k] = mode;
+    plan->hg_io[k] = (int)io;
+    *out = ex;
+    return UHMV_OK;
 }
 
 int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjoint, int mode,
@@ -1040,55 +1257,36 @@ int uhmv_matvec_host(uhmv_plan* plan, const void* x_host, void* w_host, int adjo
     if (!x_host || !w_host) return fail(UHMV_EINVAL, "uhmv_matvec_host: null host pointer");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int k = adjoint ? 1 : 0;
-    // device-visible pointers of pinned buffers (or null), queried every call (~1 us): a
-    // cached answer could outlive the allocation it described
-    plan->io_x_dev = mapped_ptr(x_host);
-    plan->io_x_host = x_host;
-    plan->io_w_dev = mapped_ptr(w_host);
-    plan->io_w_host = w_host;
-    const bool pinned = plan->io_x_dev && plan->io_w_dev;
-    const bool io = pinned && plan->has_io && mode == UHMV_MODE_BULK && plan->io[k].n_ops > 0;
-    cudaError_t e;
-    if (pinned && !plan->no_graphs && !plan->prof) {
-        if (!plan->hg_exec[k] || plan->hg_x[k] != x_host || plan->hg_w[k] != w_host || plan->hg_mode[k] != mode ||
-            plan->hg_io[k] != (int)io) {
-            if (plan->hg_exec[k]) cudaGraphExecDestroy(plan->hg_exec[k]);
-            plan->hg_exec[k] = nullptr;
-            if (!plan->cap_stream) {
-                e = cudaStreamCreateWithFlags(&plan->cap_stream, cudaStreamNonBlocking);
-                if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreate (graph capture)");
-            }
-            e = cudaStreamBeginCapture(plan->cap_stream, cudaStreamCaptureModeThreadLocal);
-            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamBeginCapture");
-            const int rc = enqueue_host(plan, x_host, w_host, adjoint, mode, plan->cap_stream, io, plan->io_x_dev,
-                                        plan->io_w_dev);
-            cudaGraph_t g = nullptr;
-            e = cudaStreamEndCapture(plan->cap_stream, &g);
-            if (rc) {
-                if (g) cudaGraphDestroy(g);
-                return rc;
-            }
-            if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-            e = cudaGraphInstantiate(&plan->hg_exec[k], g, 0);
-            cudaGraphDestroy(g);
-            if (e != cudaSuccess) {
-                plan->hg_exec[k] = nullptr;
-                return cuda_fail(e, "cudaGraphInstantiate");
-            }
-            plan->hg_x[k] = x_host;
-            plan->hg_w[k] = w_host;
-            plan->hg_mode[k] = mode;
-            plan->hg_io[k] = (int)io;
+    const int rc = serialised(plan, stream, [&]() -> int {
+        // device-visible pointers of pinned buffers (or null), queried every call (~1 us): a
+        // cached answer could outlive the allocation it described
+        plan->io_x_dev = mapped_ptr(x_host);
+        plan->io_x_host = x_host;
+        plan->io_w_dev = mapped_ptr(w_host);
+        plan->io_w_host = w_host;
+        const bool pinned = plan->io_x_dev && plan->io_w_dev;
+        const bool io = pinned && plan->has_io && plan->host_path[k] == 1 && mode == UHMV_MODE_BULK &&
+                        plan->io[k].n_ops > 0;
+        plan->last_host_path[k] = !pinned ? -1 : (io ? 1 : 0);
+        if (pinned && !plan->no_graphs && !plan->prof) {
+            cudaGraphExec_t ex = nullptr;
+            const int r = host_graph(plan, k, x_host, w_host, mode, io, &ex);
+            if (r) return r;
+            cudaError_t e = cudaGraphLaunch(ex, st);
+            return e == cudaSuccess ? UHMV_OK : cuda_fail(e, "cudaGraphLaunch");
         }
-        e = cudaGraphLaunch(plan->hg_exec[k], st);
-        if (e != cudaSuccess) return cuda_fail(e, "cudaGraphLaunch");
-    } else {
-        const int rc = enqueue_host(plan, x_host, w_host, adjoint, mode, st, io, plan->io_x_dev, plan->io_w_dev);
-        if (rc) return rc;
-    }
-    e = cudaStreamSynchronize(st);
+        return enqueue_host(plan, x_host, w_host, adjoint, mode, st, io, plan->io_x_dev, plan->io_w_dev);
+    });
+    // the caller's buffers may still be read / written by copies already enqueued: always drain
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (rc) return rc;
     if (e != cudaSuccess) return cuda_fail(e, "uhmv_matvec_host synchronize");
     return UHMV_OK;
+}
+
+int uhmv_plan_last_host_path(const uhmv_plan* plan, int adjoint) {
+    if (!plan) return fail(UHMV_EINVAL, "uhmv_plan_last_host_path: null plan");
+    return plan->last_host_path[adjoint ? 1 : 0];
 }
 
 int uhmv_matmat_host(uhmv_plan* plan, const void* X_host, void* W_host, int nrhs, void* X_dev, void* W_dev,
@@ -1099,6 +1297,10 @@ int uhmv_matmat_host(uhmv_plan* plan, const void* X_host, void* W_host, int nrhs
         return fail(UHMV_EINVAL, "uhmv_matmat_host: chunk must be a multiple of 16 dividing nrhs");
     const int64_t n_in = adjoint ? plan->d.n_rows : plan->d.n_cols;
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
+    cudaStream_t caller = static_cast<cudaStream_t>(stream);
+    Serial guard(plan, caller);
+    int rc = guard.begin();
+    if (rc) return rc;
     cudaError_t e;
     for (int i = 0; i < 3; ++i) {
         if (!plan->mm_stream[i]) {
@@ -1110,41 +1312,60 @@ int uhmv_matmat_host(uhmv_plan* plan, const void* X_host, void* W_host, int nrhs
             }
         }
     }
+    if (!plan->mm_start) {
+        e = cudaEventCreateWithFlags(&plan->mm_start, cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate (matmat_host)");
+    }
     cudaStream_t s_in = plan->mm_stream[0], s_cmp = plan->mm_stream[1], s_out = plan->mm_stream[2];
-    // order after the caller's prior work on its stream
-    cudaEvent_t start;
-    cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
-    cudaEventRecord(start, static_cast<cudaStream_t>(stream));
-    cudaStreamWaitEvent(s_in, start, 0);
-    cudaStreamWaitEvent(s_cmp, start, 0);
+    // every enqueue below is checked; after the first failure nothing more is enqueued, and the
+    // three streams are drained before returning (copies may still read X_host / write W_host)
+    auto ck = [&](cudaError_t err, const char* what) {
+        if (err != cudaSuccess && rc == UHMV_OK) rc = cuda_fail(err, what);
+        return rc == UHMV_OK;
+    };
+    // order after the caller's prior work on its stream (and the plan group's previous launch)
+    if (ck(cudaEventRecord(plan->mm_start, caller), "cudaEventRecord") &&
+        ck(cudaStreamWaitEvent(s_in, plan->mm_start, 0), "cudaStreamWaitEvent"))
+        ck(cudaStreamWaitEvent(s_cmp, plan->mm_start, 0), "cudaStreamWaitEvent");
     const int nchunk = nrhs / chunk;
     const size_t xc = (size_t)n_in * chunk * 16, wc = (size_t)n_out * chunk * 16;
-    for (int c = 0; c < nchunk; ++c) {
+    for (int c = 0; c < nchunk && rc == UHMV_OK; ++c) {
         const int b = c & 1;
         char* xd = static_cast<char*>(X_dev) + b * xc;
         char* wd = static_cast<char*>(W_dev) + b * wc;
-        if (c >= 2) cudaStreamWaitEvent(s_in, plan->mm_ev[1][b], 0);  // chunk c-2 done reading xd
+        // chunk c-2 must be done reading xd before its H2D overwrite
+        if (c >= 2 && !ck(cudaStreamWaitEvent(s_in, plan->mm_ev[1][b], 0), "cudaStreamWaitEvent")) break;
         // H2D of the chunk's columns: rows of chunk * 16 B out of rows of nrhs * 16 B
-        e = cudaMemcpy2DAsync(xd, (size_t)chunk * 16, static_cast<const char*>(X_host) + (size_t)c * chunk * 16,
-                              (size_t)nrhs * 16, (size_t)chunk * 16, (size_t)n_in, cudaMemcpyHostToDevice, s_in);
-        if (e != cudaSuccess) return cuda_fail(e, "H2D copy of X");
-        cudaEventRecord(plan->mm_ev[0][b], s_in);
-        cudaStreamWaitEvent(s_cmp, plan->mm_ev[0][b], 0);
-        if (c >= 2) cudaStreamWaitEvent(s_cmp, plan->mm_ev[2][b], 0);  // chunk c-2's W copied out
-        const int rc = uhmv_execute_mrhs(plan, xd, wd, work_mr, chunk, adjoint, s_cmp);
-        if (rc) return rc;
-        cudaEventRecord(plan->mm_ev[1][b], s_cmp);
-        cudaStreamWaitEvent(s_out, plan->mm_ev[1][b], 0);
-        e = cudaMemcpy2DAsync(static_cast<char*>(W_host) + (size_t)c * chunk * 16, (size_t)nrhs * 16, wd,
-                              (size_t)chunk * 16, (size_t)chunk * 16, (size_t)n_out, cudaMemcpyDeviceToHost, s_out);
-        if (e != cudaSuccess) return cuda_fail(e, "D2H copy of W");
-        cudaEventRecord(plan->mm_ev[2][b], s_out);
+        if (!ck(cudaMemcpy2DAsync(xd, (size_t)chunk * 16, static_cast<const char*>(X_host) + (size_t)c * chunk * 16,
+                                  (size_t)nrhs * 16, (size_t)chunk * 16, (size_t)n_in, cudaMemcpyHostToDevice, s_in),
+                "H2D copy of X") ||
+            !ck(cudaEventRecord(plan->mm_ev[0][b], s_in), "cudaEventRecord") ||
+            !ck(cudaStreamWaitEvent(s_cmp, plan->mm_ev[0][b], 0), "cudaStreamWaitEvent"))
+            break;
+        // chunk c-2's W must be copied out before wd is rewritten
+        if (c >= 2 && !ck(cudaStreamWaitEvent(s_cmp, plan->mm_ev[2][b], 0), "cudaStreamWaitEvent")) break;
+        const int r = execute_mrhs_impl(plan, xd, wd, work_mr, chunk, adjoint, s_cmp);
+        if (r) {
+            rc = r;
+            break;
+        }
+        if (!ck(cudaEventRecord(plan->mm_ev[1][b], s_cmp), "cudaEventRecord") ||
+            !ck(cudaStreamWaitEvent(s_out, plan->mm_ev[1][b], 0), "cudaStreamWaitEvent") ||
+            !ck(cudaMemcpy2DAsync(static_cast<char*>(W_host) + (size_t)c * chunk * 16, (size_t)nrhs * 16, wd,
+                                  (size_t)chunk * 16, (size_t)chunk * 16, (size_t)n_out, cudaMemcpyDeviceToHost, s_out),
+                "D2H copy of W") ||
+            !ck(cudaEventRecord(plan->mm_ev[2][b], s_out), "cudaEventRecord"))
+            break;
     }
-    cudaEventDestroy(start);
-    e = cudaStreamSynchronize(s_out);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s_cmp);
-    if (e != cudaSuccess) return cuda_fail(e, "uhmv_matmat_host synchronize");
-    return UHMV_OK;
+    // drain all three streams whatever happened
+    const cudaError_t e1 = cudaStreamSynchronize(s_in);
+    const cudaError_t e2 = cudaStreamSynchronize(s_cmp);
+    const cudaError_t e3 = cudaStreamSynchronize(s_out);
+    if (rc) return rc;
+    if (!ck(e1, "uhmv_matmat_host synchronize") || !ck(e2, "uhmv_matmat_host synchronize") ||
+        !ck(e3, "uhmv_matmat_host synchronize"))
+        return rc;
+    return guard.end();
 }
 
 int uhmv_plan_info(const uhmv_plan* plan, int adjoint, int mode, int* grid, int* smem_bytes,
@@ -1203,7 +1424,13 @@ int uhmv_dmma_peak(int device, double* tflops) {
 
 int uhmv_plan_destroy(uhmv_plan* plan) {
     if (plan) {
+        {  // wait for the plan group's last launch (its buffers may be freed after this)
+            std::lock_guard<std::mutex> g(plan->sync->mu);
+            if (plan->sync->recorded) cudaEventSynchronize(plan->sync->ev);
+        }
+        sync_release(plan->d.ticket, plan->sync);
         drop_host_graphs(plan);
+        if (plan->mm_start) cudaEventDestroy(plan->mm_start);
         if (plan->cap_stream) cudaStreamDestroy(plan->cap_stream);
         for (int i = 0; i < 3; ++i) {
             if (!plan->mm_stream[i]) continue;

@@ -264,6 +264,14 @@ class DeviceOperator:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         return ctypes.c_void_p(s.cuda_stream)
 
+    def _check_out(self, out, shape):
+        """The C side writes exactly prod(shape) complex128 at out.data_ptr(): refuse anything
+        else (a wrong size, dtype, stride or device would be an out-of-bounds HBM write)."""
+        torch = self.torch
+        if (not isinstance(out, torch.Tensor) or out.dtype != torch.complex128 or out.device != self.device
+                or tuple(out.shape) != tuple(shape) or not out.is_contiguous()):
+            raise ValueError(f"out must be a contiguous complex128 {self.device} tensor of shape {tuple(shape)}")
+
     def matvec(self, x, adjoint=False, out=None, mode=None, stream=None):
         """Device API: x is a CUDA complex128 tensor (n_in,), returns/fills out (n_out,)."""
         torch = self.torch
@@ -274,6 +282,8 @@ class DeviceOperator:
         x = x.contiguous()
         if out is None:
             out = torch.empty(n_out, dtype=torch.complex128, device=self.device)
+        else:
+            self._check_out(out, (n_out,))
         mode = mode or default_mode()
         rc = _lib.lib().uhmv_execute(
             self._plan, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()), int(adjoint),
@@ -288,8 +298,10 @@ class DeviceOperator:
         torch = self.torch
         p = self.packed
         n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
-        if X.dim() != 2 or X.shape[0] != n_in or X.dtype != torch.complex128:
-            raise ValueError(f"X must be complex128 of shape ({n_in}, R)")
+        if X.dim() != 2 or X.shape[0] != n_in or X.dtype != torch.complex128 or X.device != self.device:
+            raise ValueError(f"X must be a complex128 {self.device} tensor of shape ({n_in}, R)")
+        if out is not None:
+            self._check_out(out, (n_out, X.shape[1]))
         R = X.shape[1]
         Rp = max(16, (R + 15) // 16 * 16)
         if Rp != R:
@@ -377,8 +389,8 @@ class DeviceOperator:
         _lib.check(rc, "uhmv_execute_phases")
 
     def attach_io(self) -> bool:
-        """Build and upload the host-I/O programs (packer ``io_programs``) once: with them
-        ``matvec_host`` on pinned buffers can run ONE launch that reads x and writes w over
+        """Build, upload and attach the host-I/O programs (packer ``io_programs``) once: with
+        them ``matvec_host`` on pinned buffers can run ONE launch that reads x and writes w over
         PCIe itself.  False when the operator has none (or this is a partitioned / re-chunked
         plan)."""
         if getattr(self, "_io", None) is not None:
@@ -394,32 +406,30 @@ class DeviceOperator:
         dev = [_DeviceProgram(torch, q, self.device) if q is not None else None for q in (fwd, adj)]
         n_ctr = max([q.n_counters for q in (fwd, adj) if q is not None] + [1])
         ctr = torch.zeros(n_ctr, dtype=torch.int32, device=self.device)
-        self._io = (dev, ctr, [d.struct() if d is not None else None for d in dev])
-        self._io_on = None
+        structs = [d.struct() if d is not None else _lib.UhmvProgram() for d in dev]  # empty = copy path
+        with self.torch.cuda.device(self.device):
+            _lib.check(_lib.lib().uhmv_plan_set_io(self._plan, ctypes.byref(structs[0]), ctypes.byref(structs[1]),
+                                                   ctypes.c_void_p(ctr.data_ptr())), "uhmv_plan_set_io")
+        self._io = (dev, ctr, structs, (fwd is not None, adj is not None))
+        self._io_path = {}  # per direction: the path the C plan is set to
         self._io_tune = {False: ([], []), True: ([], [])}  # per direction: (io times, copy times)
         self._io_use = {}
         return True
 
-    def _set_io(self, fwd_on: bool, adj_on: bool):
-        """Enable the host-I/O program of each direction (an empty program = copy path)."""
-        if self._io_on == (fwd_on, adj_on):
-            return
-        _dev, ctr, structs = self._io
-        sf = structs[0] if (fwd_on and structs[0] is not None) else _lib.UhmvProgram()
-        sa = structs[1] if (adj_on and structs[1] is not None) else _lib.UhmvProgram()
-        with self.torch.cuda.device(self.device):
-            _lib.check(_lib.lib().uhmv_plan_set_io(self._plan, ctypes.byref(sf), ctypes.byref(sa),
-                                                   ctypes.c_void_p(ctr.data_ptr())), "uhmv_plan_set_io")
-        self._io_on = (fwd_on, adj_on)
+    def _set_path(self, adjoint: bool, io: bool):
+        if self._io_path.get(adjoint) != io:
+            _lib.check(_lib.lib().uhmv_plan_set_host_path(self._plan, int(adjoint), int(io)), "set_host_path")
+            self._io_path[adjoint] = io
 
     def matvec_host(self, x_host: np.ndarray, adjoint=False, out: np.ndarray | None = None, mode=None, stream=None,
                     host_io=None):
         """End-to-end C-ABI call with host buffers, then a stream synchronize.
         Pinned buffers (e.g. ``tensor.pin_memory().numpy()``) can take the host-I/O launch (x read
         and w written over PCIe inside the kernel, overlapping it); pageable ones always take
-        H2D copy, kernel, D2H copy.  ``host_io``: None = measure both on the first calls of each
-        direction and keep the faster (the host-I/O launch pays PCIe latency at the start of
-        the kernel, which loses on small operators), True / False = force."""
+        H2D copy, kernel, D2H copy.  ``host_io``: None = with pinned buffers, time both paths on
+        the first calls of each direction (graph replays of each) and keep the faster (the
+        host-I/O launch pays PCIe latency at the start of the kernel, which loses on small
+        operators); True / False = force."""
         p = self.packed
         n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
         if x_host.dtype != np.complex128 or not x_host.flags.c_contiguous:
@@ -431,50 +441,76 @@ class DeviceOperator:
         elif out.dtype != np.complex128 or not out.flags.c_contiguous or out.shape != (n_out,):
             raise ValueError(f"out must be a contiguous complex128 array of shape ({n_out},)")
         mode = mode or default_mode()
-        torch = self.torch
         adjoint = bool(adjoint)
-        with self._lock:  # the plan's host-I/O programs and captured graphs are per-plan state
+        with self._lock:  # the plan's path choice and the C graph cache are per-plan state
             return self._matvec_host_locked(x_host, adjoint, out, mode, stream, host_io)
 
     def _matvec_host_locked(self, x_host, adjoint, out, mode, stream, host_io):
         torch = self.torch
+        L = _lib.lib()
         use, tuning = False, False
-        if mode == "bulk" and host_io is not False and self.attach_io() and self._io[2][int(adjoint)] is not None:
+        if mode == "bulk" and host_io is not False and self.attach_io() and self._io[3][int(adjoint)]:
+            pinned = bool(L.uhmv_host_pinned(ctypes.c_void_p(x_host.ctypes.data))) and bool(
+                L.uhmv_host_pinned(ctypes.c_void_p(out.ctypes.data)))
             if host_io:
                 use = True
             elif adjoint in self._io_use:
                 use = self._io_use[adjoint]
-            else:
+            elif pinned:  # only pinned calls can take the host-I/O launch: only they are timed
                 t_io, t_cp = self._io_tune[adjoint]
                 use, tuning = len(t_io) <= len(t_cp), True
-            on = list(self._io_on or (False, False))
-            on[int(adjoint)] = use
-            self._set_io(*on)
+            self._set_path(adjoint, use)
         elif getattr(self, "_io", None):
-            on = list(self._io_on or (False, False))
-            on[int(adjoint)] = False
-            self._set_io(*on)
+            self._set_path(adjoint, False)
         t0 = time.perf_counter()
         # (the device switch costs ~10 us of host time per call: only when needed)
         if torch.cuda.current_device() == self.device.index:
-            rc = _lib.lib().uhmv_matvec_host(
+            rc = L.uhmv_matvec_host(
                 self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
                 int(adjoint), _MODES[mode], self._stream(stream),
             )
         else:
             with torch.cuda.device(self.device):
-                rc = _lib.lib().uhmv_matvec_host(
+                rc = L.uhmv_matvec_host(
                     self._plan, ctypes.c_void_p(x_host.ctypes.data), ctypes.c_void_p(out.ctypes.data),
                     int(adjoint), _MODES[mode], self._stream(stream),
                 )
         dt = time.perf_counter() - t0
         _lib.check(rc, "uhmv_matvec_host")
-        if tuning:
+        if tuning and L.uhmv_plan_last_host_path(self._plan, int(adjoint)) == int(use):
             t_io, t_cp = self._io_tune[adjoint]
             (t_io if use else t_cp).append(dt)
-            if len(t_io) >= 4 and len(t_cp) >= 4:  # first call of each is a warm-up
+            if len(t_io) >= 4 and len(t_cp) >= 4:  # the first call of each path captures its graph
                 self._io_use[adjoint] = min(t_io[1:]) < min(t_cp[1:])
         return out
+
+    def matvec_array(self, v: np.ndarray, adjoint=False, dtype=np.complex128) -> np.ndarray:
+        """The drop-in's host call (``matvec_uh(u, ndarray)``): ``v`` of any dtype and layout is
+        copied (and promoted) into a plan-owned pinned staging vector, the pinned host call runs
+        (captured graph, §5b of DESIGN.md), and the result is copied into a NEW array of
+        ``dtype`` (real part for a real result type, as uniform.py:495 implies)."""
+        p = self.packed
+        n_in, n_out = (p.n_rows, p.n_cols) if adjoint else (p.n_cols, p.n_rows)
+        if v.shape != (n_in,):
+            raise ValueError(f"x must have shape ({n_in},)")
+        adjoint = bool(adjoint)
+        with self._lock:
+            st = getattr(self, "_staging", None)
+            if st is None:
+                torch = self.torch
+                st = {}
+                for adj in (False, True):
+                    a, b = (p.n_rows, p.n_cols) if adj else (p.n_cols, p.n_rows)
+                    st[adj] = (torch.empty(max(a, 1), dtype=torch.complex128).pin_memory(),
+                               torch.empty(max(b, 1), dtype=torch.complex128).pin_memory())
+                self._staging = st
+            xs, ws = st[adjoint]
+            xs_np, ws_np = xs.numpy()[:n_in], ws.numpy()[:n_out]
+            np.copyto(xs_np, v, casting="unsafe" if np.iscomplexobj(v) else "same_kind")
+            self._matvec_host_locked(xs_np, adjoint, ws_np, default_mode(), None, None)
+            if np.issubdtype(dtype, np.complexfloating):
+                return ws_np.astype(dtype, copy=True)
+            return ws_np.real.astype(dtype, copy=True)
 
     def host_io_choice(self, adjoint=False):
         """Which path matvec_host settled on for pinned buffers: True host-I/O, False copy,

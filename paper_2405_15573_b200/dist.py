@@ -41,6 +41,15 @@ def exchange_views(work, packed, adjoint: bool):
     return region, mine
 
 
+def _check_vec(t, n, device, name):
+    """C-ABI buffers are raw pointers: a wrong size, dtype, stride or device is refused here."""
+    import torch
+
+    if (not isinstance(t, torch.Tensor) or t.dtype != torch.complex128 or t.device != device
+            or tuple(t.shape) != (n,) or not t.is_contiguous()):
+        raise ValueError(f"{name} must be a contiguous complex128 {device} tensor of shape ({n},)")
+
+
 def _peer_rank(work, work_len, counters, done):
     from . import _lib
 
@@ -140,6 +149,7 @@ class PeerEmulation:
         x = x.contiguous()
         if out is None:
             out = torch.empty(n_out, dtype=torch.complex128, device=self.device)
+        _check_vec(out, n_out, self.device, "out")
         adjoint = bool(adjoint)
         self.epoch[adjoint] += 1
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -247,9 +257,11 @@ class DistributedOperator:
     def matvec(self, x, adjoint=False, out=None, mode=None, gather=False):
         if self.exchange == "peer":
             torch = self.a.torch
-            n_out = self.n_cols if adjoint else self.n_rows
+            n_in, n_out = (self.n_rows, self.n_cols) if adjoint else (self.n_cols, self.n_rows)
+            _check_vec(x, n_in, self.device, "x")
             if out is None:
                 out = torch.empty(n_out, dtype=torch.complex128, device=self.device)
+            _check_vec(out, n_out, self.device, "out")
             adjoint = bool(adjoint)
             self.epoch[adjoint] += 1
             _execute_peer([self.a._plan], self.rank, self.world, self.ranks[adjoint], x.contiguous(), [out], adjoint,

@@ -183,9 +183,7 @@ class PackedOperator:
         bct = self.geo["bct"]
         part = None
         if world > 1:
-            rb = partition_bounds(bct.row_tree, world)
-            cb = rb if bct.col_tree is bct.row_tree else partition_bounds(bct.col_tree, world)
-            part = dict(rank=rank, world=world, row_bounds=rb, col_bounds=cb)
+            part = _partition(self.geo, world, rank)
         kw = dict(self.build_kw, part=part, peer=bool(peer and world > 1))
         fwd, work_f, ex_f = _build_program(self.geo, adjoint=False, **kw)
         adj, work_a, ex_a = _build_program(self.geo, adjoint=True, **kw)
@@ -472,9 +470,7 @@ def pack(
         vstack=vstack, ustack=ustack, cwidth=cwidth, spos=spos,
     )
     if world > 1:
-        rb = partition_bounds(bct.row_tree, world)
-        cb = rb if bct.col_tree is bct.row_tree else partition_bounds(bct.col_tree, world)
-        part = dict(rank=rank, world=world, row_bounds=rb, col_bounds=cb)
+        part = _partition(geo, world, rank)
     else:
         part = None
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in SPLIT_DEFAULTS.items()}
@@ -522,16 +518,38 @@ def pack(
     )
 
 
-def partition_bounds(tree, world: int):
+def partition_bounds(tree, world: int, weights=None, keep=()):
     """Cut the tree's index range into ``world`` contiguous slices on leaf boundaries.
 
-    Cuts at tree level log2(world) when that is a power of two and the tree is balanced
-    (subtree-aligned), otherwise leaf-balanced by index count."""
+    ``weights`` (leaf id -> bytes a rank streams for that leaf, :func:`leaf_bytes`): cut the
+    prefix sums of the weights at r/world of the total -- row clusters partitioned by bytes
+    touched (BASELINE north_star) -- only at leaf ends that cut no cluster of ``keep`` (a cut
+    cluster's Z op would run on both ranks), when there are enough of those.  Without weights:
+    leaf-balanced by index count."""
     leaves, _ = _leaves_under(tree)
     nodes = tree.nodes
     lo = nodes[getattr(tree, "root", 0)].lo
     hi = nodes[getattr(tree, "root", 0)].hi
     ends = [nodes[l].hi for l in leaves]
+    if weights is not None and world > 1:
+        cum = np.cumsum([float(weights.get(l, 0.0)) for l in leaves])
+        total = float(cum[-1]) if len(cum) else 0.0
+        if total > 0:
+            kept = [nodes[c] for c in keep]
+            ok = [i for i, e in enumerate(ends) if e < hi and not any(c.lo < e < c.hi for c in kept)]
+            if len(ok) < world - 1:
+                ok = [i for i, e in enumerate(ends) if e < hi]
+            bounds = [lo]
+            for r in range(1, world):
+                target = total * r / world
+                cand = [i for i in ok if ends[i] > bounds[-1]]
+                if not cand:
+                    bounds.append(hi)
+                    continue
+                best = min(cand, key=lambda i: abs(cum[i] - target))
+                bounds.append(ends[best])
+            bounds.append(hi)
+            return bounds
     bounds = [lo]
     for r in range(1, world):
         target = lo + (hi - lo) * r / world
@@ -540,6 +558,42 @@ def partition_bounds(tree, world: int):
         bounds.append(best)
     bounds.append(hi)
     return bounds
+
+
+def leaf_bytes(geo) -> dict:
+    """Bytes one rank streams per row-tree leaf L of a forward matvec if it owns L (shared
+    row / column tree): the dense blocks of L's rows (NEAR), L's row of the leaf stacks US_L
+    and VS_L (FAR, P1), and the coupling C_s / Y_t of the clusters whose first leaf is L (Z,
+    U).  None for two-tree operators (partition_bounds then cuts by index count)."""
+    bct = geo["bct"]
+    if bct.col_tree is not bct.row_tree:
+        return None
+    nodes = bct.row_tree.nodes
+    leaves, span = _leaves_under(bct.row_tree)
+    w = {l: 0 for l in leaves}
+    for key, stacks in (("US", geo["ustack"]), ("VS", geo["vstack"])):
+        for leaf, (W, _cols) in stacks.items():
+            w[leaf] += nodes[leaf].size * W
+    for leaf, bids in geo["dense_by_rleaf"].items():
+        for bid in bids:
+            r, c = bct.block_shape(bid)
+            w[leaf] += r * c
+    for s, wd in geo["cwidth"].items():
+        w[leaves[span[s][0]]] += geo["rank_r"][s] * wd
+    for t, (_cols, k) in geo["ycols"].items():
+        w[leaves[span[t][0]]] += geo["rank_c"][t] * k
+    return {l: 16 * v for l, v in w.items()}
+
+
+def _partition(geo, world, rank):
+    bct = geo["bct"]
+    keep = [c for c in bct.row_map if geo["rank_r"][c] > 0]
+    if bct.col_tree is bct.row_tree:
+        keep += [c for c in bct.col_map if geo["rank_c"][c] > 0 and c not in bct.row_map]
+    lb = leaf_bytes(geo)
+    rb = partition_bounds(bct.row_tree, world, weights=lb, keep=keep)
+    cb = rb if bct.col_tree is bct.row_tree else partition_bounds(bct.col_tree, world)
+    return dict(rank=rank, world=world, row_bounds=rb, col_bounds=cb)
 
 
 def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):

@@ -10,6 +10,11 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 for p in (ROOT, os.path.join(ROOT, "oracle")):
     if p not in sys.path:
         sys.path.insert(0, p)
+# the reference package itself, installed by oracle/build_ref.sh (git-ignored, shipped to the
+# GPU box): lowest priority, used only as the checker
+REF_SITE = os.path.join(ROOT, "oracle", "_ref", "site")
+if os.path.isdir(REF_SITE) and REF_SITE not in sys.path:
+    sys.path.append(REF_SITE)
 
 
 def pytest_configure(config):

@@ -23,7 +23,9 @@ def test_library_exports_all_header_symbols():
     L = ensure_built()
     for s in header_symbols():
         assert hasattr(L, s), s
-    assert L.uhmv_abi_version() == 9
+    from paper_2405_15573_b200 import _lib
+
+    assert L.uhmv_abi_version() == _lib.ABI_VERSION == 10
     assert L.uhmv_last_error() == b""
 
 
@@ -74,3 +76,6 @@ def test_diagnostic_and_io_entries_reject_null_plan():
     assert L.uhmv_plan_set_trace(None, None) == -1
     assert L.uhmv_plan_set_profile(None, None) == -1
     assert L.uhmv_peer_set_diag(None, 28) == 0  # process-wide diagnostics switch, always accepted
+    assert L.uhmv_plan_set_host_path(None, 0, 1) == -1
+    assert L.uhmv_plan_last_host_path(None, 0) == -1
+    assert L.uhmv_host_pinned(None) == 0  # no CUDA context needed for a null pointer

@@ -41,3 +41,43 @@ def test_install_patches_reference_names():
     finally:
         pk.uninstall(orig)
     assert uhm_kit.matvec_uh is not pk.matvec_uh
+
+
+def test_install_patches_error_metrics():
+    uhm_kit = pytest.importorskip("uhm_kit")
+    import uhm_kit.verification
+
+    from paper_2405_15573_b200 import verification as ver
+
+    orig = pk.install()
+    try:
+        assert uhm_kit.compression_error is ver.compression_error
+        assert uhm_kit.verification.spectral_norm_estimate is ver.spectral_norm_estimate
+        assert ver._report_cls is uhm_kit.verification.ErrorReport
+    finally:
+        pk.uninstall(orig)
+    assert uhm_kit.compression_error is not ver.compression_error
+    assert ver._report_cls is ver.ErrorReport
+
+
+def test_error_metrics_closure_operands_match_reference_values(golden):
+    """Closure operands take the host loop (verification.py:54-138 step for step): the
+    reference's own stored values for the golden operators."""
+    from matvec_oracle import farfield_only, oracle_matvec_uh
+
+    from paper_2405_15573_b200 import verification as ver
+
+    name, u, ex = golden
+    if "pi_est" not in ex:
+        pytest.skip("no verification values stored")
+    n = u.shape[1]
+    op = lambda a: (lambda v: oracle_matvec_uh(a, v), lambda v: oracle_matvec_uh(a, v, adjoint=True), n)  # noqa: E731
+    est = ver.spectral_norm_estimate(*op(u), iters=30, seed=0)
+    assert abs(est - float(ex["pi_est"])) <= 1e-10 * float(ex["pi_est"])
+    rep = ver.compression_error(op(u), op(farfield_only(u)), iters=30, seed=0)
+    assert abs(rep.rel_spectral_estimate - float(ex["ce_rel"])) <= 1e-9 * float(ex["ce_rel"])
+    assert rep.iterations == int(ex["ce_used"])
+    with pytest.raises(ValueError):
+        ver.spectral_norm_estimate(lambda v: v, lambda v: v, 5, iters=0)
+    with pytest.raises(ValueError):
+        ver.compression_error(np.eye(3), op(u))

@@ -173,7 +173,7 @@ def test_power_iteration_on_device(golden):
     name, u, ex = golden
     if "pi_est" not in ex:
         pytest.skip("no verification values stored")
-    est = verification.spectral_norm_estimate(u, iters=30, seed=0)
+    est = verification.operator_norm_estimate(u, iters=30, seed=0)
     assert abs(est - float(ex["pi_est"])) <= 1e-10 * float(ex["pi_est"])
     rep = verification.compression_error(u, farfield_only(u), iters=30, seed=0)
     assert abs(rep.rel_spectral_estimate - float(ex["ce_rel"])) <= 1e-9 * float(ex["ce_rel"])
