@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--adjoint", action="store_true")
     ap.add_argument("--view", default="full", choices=["full", "far", "near"], help="diagnostics: parity view")
-    ap.add_argument("--format", default="uh", choices=["uh", "h"],
+    ap.add_argument("--format", default="uh", choices=["uh", "h", "sym"],
                     help="uh: uniform H-matrix (the hot path); h: the source H-matrix (matvec_h)")
     ap.add_argument("--exchange", default="auto", choices=["auto", "nccl", "peer"],
                     help="multi-GPU y/u exchange: NCCL all-gather between two launches, or peer stores "
@@ -221,6 +221,9 @@ def make_config(args, world):
     }
     if args.format == "h":
         config["format"] = "H-matrix (matvec_h, hmatrix.py:143-184), ranks of the reference's assemble_h"
+    if args.format == "sym":
+        config["format"] = ("symmetric single-triangle variant (paper Remark 4.5; a LABELLED variant, not the "
+                            "reference's two-triangle operator): one basis, lower blocks only, every slab read once")
     if args.view != "full":
         config["view"] = args.view
     if args.emulate_ranks > 1:
@@ -258,7 +261,14 @@ def main():
     torch.cuda.set_device(dev)
 
     t_build = time.perf_counter()
-    u = workloads.build_operator(args.config) if args.format == "uh" else workloads.build_h_operator(args.config)
+    if args.format == "sym":
+        if args.adjoint or world > 1 or args.emulate_ranks > 1 or args.view != "full":
+            raise SystemExit("--format sym: forward, single GPU, full view only")
+        u = workloads.build_symmetric_operator(args.config)
+    elif args.format == "uh":
+        u = workloads.build_operator(args.config)
+    else:
+        u = workloads.build_h_operator(args.config)
     if args.view != "full":
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         from matvec_oracle import farfield_only, nearfield_only
@@ -286,6 +296,10 @@ def main():
             from paper_2405_15573_b200.packer_h import pack_h
 
             packed = pack_h(u)
+        elif args.format == "sym":
+            from paper_2405_15573_b200.packer_sym import pack_sym
+
+            packed = pack_sym(u)
         else:
             packed = pack(u)
         op = DeviceOperator(packed, device=dev)
@@ -397,7 +411,7 @@ def main():
 
         register_device_operator(u, op)
         xr = (x_np if not args.adjoint else workloads.seeded_vector(n_in, 0)).copy()
-        fn = pk.matvec_h if args.format == "h" else pk.matvec_uh
+        fn = {"h": pk.matvec_h, "sym": pk.matvec_uh_sym}.get(args.format, pk.matvec_uh)
         for _ in range(10):
             fn(u, xr, adjoint=args.adjoint)
         td = wall(lambda: fn(u, xr, adjoint=args.adjoint), k_e2e)
@@ -410,7 +424,7 @@ def main():
     alg_bytes_total = workloads.algorithmic_bytes(packed)
     value = 1.0 / med_s
     achieved = alg_bytes_total / world / med_s / 1e9  # per GPU
-    traffic = load_traffic(args.config)
+    traffic = load_traffic(args.config) if args.format == "uh" else None
     roofline = {
         "bound": "hbm",
         "achieved": achieved,
@@ -423,8 +437,9 @@ def main():
         "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
                           "(profiles/ncu_traffic.json, same command)",
         "algorithmic_bytes_per_launch": int(alg_bytes_total / world),
-        "reference_bytes_estimate": ref_bytes_estimate(args.config, u),
-        "kernel": "bulk::uhmv_bulk_peer_kernel" if (args.emulate_ranks > 1 or getattr(op, "exchange", "") == "peer") else
+        "reference_bytes_estimate": ref_bytes_estimate(args.config, u) if args.format != "sym" else None,
+        "kernel": "bulk::uhmv_bulk_sym_kernel" if args.format == "sym" else
+        "bulk::uhmv_bulk_peer_kernel" if (args.emulate_ranks > 1 or getattr(op, "exchange", "") == "peer") else
         {"bulk": "bulk::uhmv_bulk_kernel", "fused": "uhmv_fused_kernel"}.get(args.mode, "uhmv_phase_kernel (5 launches)"),
     }
     if rank != 0:

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 10
+#define UHMV_ABI_VERSION 11
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -78,7 +78,12 @@ typedef struct uhmv_program {
     void* tmaps;              /* DEVICE buffer, 2 * n_tmaps * 128 bytes, 64-B aligned, that
                                  uhmv_plan_create fills with TMA tensor maps over the arena
                                  (per ld: a 16 x 16 and a 16 x 80 complex box)              */
+    int32_t flags;            /* UHMV_PROG_SYM: symmetric single-triangle program
+                                 (paper_2405_15573_b200/packer_sym.py; T-mode and alias
+                                 pieces): bulk engine only                                  */
 } uhmv_program;
+
+#define UHMV_PROG_SYM 1
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */
 typedef struct uhmv_desc {

@@ -19,6 +19,7 @@ from paper_2405_15573_b200.packer import (
     MODE_N,
     MODE_NW,
     MODE_S,
+    MODE_T,
     MR_FIRST,
     MR_ZERO,
     OP_PEER,
@@ -63,6 +64,8 @@ def run_op(prog, i, bufs, engine="segs", peers=()):
             out[out_off : out_off + rows] += m @ vin[in_off : in_off + cols]
         elif mode == MODE_H:
             out[out_off : out_off + cols] += np.conj(m).T @ vin[in_off : in_off + rows]
+        elif mode == MODE_T:  # symmetric variant (packer_sym): transpose without conjugation
+            out[out_off : out_off + cols] += m.T @ vin[in_off : in_off + rows]
         elif mode == MODE_S:
             out[out_off : out_off + cols] += m.sum(axis=0)
         else:

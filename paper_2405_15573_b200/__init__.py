@@ -4,8 +4,9 @@ The reference (arXiv 2405.15573, package ``uhm_kit``) builds the operator; this 
 packs it into HBM and replaces only the product (reference uniform.py:476-556).
 """
 
-from .matvec import clear_cache, device_operator, matmat_uh, matvec_h, matvec_uh
+from .matvec import clear_cache, device_operator, matmat_uh, matvec_h, matvec_uh, matvec_uh_sym
 from .packer import PackedOperator, pack
+from .symmetric import SymmetricUniformHMatrix, symmetrize_uh
 from .uh_types import (
     BlockClusterTree,
     BlockNode,
@@ -23,6 +24,9 @@ __all__ = [
     "matvec_uh",
     "matmat_uh",
     "matvec_h",
+    "matvec_uh_sym",
+    "SymmetricUniformHMatrix",
+    "symmetrize_uh",
     "device_operator",
     "clear_cache",
     "pack",

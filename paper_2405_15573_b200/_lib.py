@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "UhmvPeerRank", "check", "LIB_PATH"
 
 LIB_PATH = os.environ.get("UHMV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 10
+ABI_VERSION = 11
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -42,7 +42,11 @@ class UhmvProgram(ctypes.Structure):
         ("n_tmaps", ctypes.c_int32),
         ("tmap_lds", ctypes.c_void_p),
         ("tmaps", ctypes.c_void_p),
+        ("flags", ctypes.c_int32),
     ]
+
+
+PROG_SYM = 1  # uhmv_program.flags: symmetric single-triangle program (bulk engine only)
 
 
 class UhmvDesc(ctypes.Structure):

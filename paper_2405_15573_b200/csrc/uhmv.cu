@@ -89,6 +89,11 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
     return r;
 }
 
+// fp64 reduction into global memory without a returned value: one RED.E.ADD.F64 (the generic
+// atomicAdd(double*) also emits a shared-memory CAS loop behind an address-space test)
+__device__ __forceinline__ void red_add_f64(double* p, double v) {
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(__cvta_generic_to_global(p)), "d"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -320,8 +325,8 @@ __device__ void run_op(const ExecParams& p, int op, double2* xin, double2* outv,
         if (flags & 2) {  // fp64 red.add into the pre-zeroed output (<= 2 addends per entry)
             for (int i = tid; i < len; i += kThreads) {
                 const double2 v = outv[dst + i];
-                atomicAdd(&dp[i].x, v.x);
-                atomicAdd(&dp[i].y, v.y);
+                red_add_f64(&dp[i].x, v.x);
+                red_add_f64(&dp[i].y, v.y);
             }
             continue;
         }
@@ -700,6 +705,12 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              smem_optin);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(bulk::uhmv_bulk_sym_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_optin);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(bulk::uhmv_bulk_sym_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem_optin);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(bulk::uhmv_bulk_peer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem_optin);
     if (e == cudaSuccess)
@@ -893,6 +904,8 @@ static int execute_phases_impl(uhmv_plan* plan, const void* x, void* w, int adjo
                                void* stream) {
     const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
     const int k = adjoint ? 1 : 0;
+    if (pr.flags & UHMV_PROG_SYM)
+        return fail(UHMV_EINVAL, "uhmv_execute_phases: symmetric single-triangle programs run on the bulk engine only");
     if (phase_lo < 0 || phase_hi > pr.n_phases || phase_lo > phase_hi)
         return fail(UHMV_EINVAL, "uhmv_execute_phases: bad phase range");
     if (pr.n_ops > 0 && (!x || !w)) return fail(UHMV_EINVAL, "null vector pointer");
@@ -920,6 +933,8 @@ static int execute_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, in
         return execute_phases_impl(plan, x, w, adjoint, 0, pr.n_phases, stream);
     if (mode != UHMV_MODE_FUSED && mode != UHMV_MODE_BULK)
         return fail(UHMV_EINVAL, "uhmv_execute: unknown mode");
+    if ((pr.flags & UHMV_PROG_SYM) && mode != UHMV_MODE_BULK)
+        return fail(UHMV_EINVAL, "uhmv_execute: symmetric single-triangle programs run on the bulk engine only");
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
     if (n_out > 0 && pr.zero_output) {  // NEAR/FAR add into a zeroed output
         if (!w) return fail(UHMV_EINVAL, "null output pointer");
@@ -932,12 +947,16 @@ static int execute_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, in
     if (mode == UHMV_MODE_BULK) {
         if (!pr.pieces) return fail(UHMV_EINVAL, "bulk mode needs the piece table");
         bulk::Params bp = make_bulk_params(plan, pr, k, x, w);
-        if (bp.prof)
-            bulk::uhmv_bulk_kernel<true><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k],
-                                           static_cast<cudaStream_t>(stream)>>>(bp);
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const bool sym = (pr.flags & UHMV_PROG_SYM) != 0;
+        if (bp.prof && sym)
+            bulk::uhmv_bulk_sym_kernel<true><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
+        else if (sym)
+            bulk::uhmv_bulk_sym_kernel<false><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
+        else if (bp.prof)
+            bulk::uhmv_bulk_kernel<true><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
         else
-            bulk::uhmv_bulk_kernel<false><<<plan->bulk_grid[k], bulk::kThreads,
-                                            plan->bulk_smem[k], static_cast<cudaStream_t>(stream)>>>(bp);
+            bulk::uhmv_bulk_kernel<false><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "uhmv_bulk_kernel launch");
         return UHMV_OK;
@@ -1091,6 +1110,8 @@ int uhmv_execute_peer(uhmv_plan* const* plans, int nplans, int rank0, int world,
 
 static int execute_mrhs_impl(uhmv_plan* plan, const void* x, void* w, void* work_mr, int nrhs, int adjoint,
                              void* stream) {
+    if (((adjoint ? plan->d.adj : plan->d.fwd).flags & UHMV_PROG_SYM))
+        return fail(UHMV_EINVAL, "uhmv_execute_mrhs: no multi-RHS engine for symmetric single-triangle programs");
     if (nrhs <= 0 || nrhs % mrhs::kRC) return fail(UHMV_EINVAL, "nrhs must be a multiple of 16");
     const uhmv_program& pr = adjoint ? plan->d.adj : plan->d.fwd;
     if (!pr.mr_segs || !pr.mr_ranges) return fail(UHMV_EINVAL, "program has no multi-RHS tables");

@@ -50,12 +50,16 @@ constexpr int kSlotRuns = 48;     // run descriptors cached per op slot
 constexpr int kSlotPieces = 128;  // piece descriptors cached per op slot
 constexpr int kGatherBatch = 8;   // loads in flight per thread in the gather
 constexpr int64_t kPiBegin = 1ll << 24, kPiEnd = 1ll << 25, kPiDirect = 1ll << 26,
-                  kPiXStage = 1ll << 28;
+                  kPiXStage = 1ll << 28, kPiAlias = 1ll << 29;
+constexpr int kModeT = 4;  // out[j] += sum_r M[r,j] in[r] (no conjugation; symmetric variant)
 
 // compressed consumer-side piece descriptor (int4):
-//   x = rows << 16 | cols, y = in_off, z = out_off,
-//   w = smem_off | mode << 16 | begin << 20 | end << 21 | direct << 22 | xstage << 23
-constexpr int kCBegin = 1 << 20, kCEnd = 1 << 21, kCDirect = 1 << 22, kCXStage = 1 << 23;
+//   x = rows << 16 | cols, y = in_off (alias pieces: in_off | smem row stride << 16), z = out_off,
+//   w = smem_off | mode << 16 | begin << 20 | end << 21 | direct << 22 | xstage << 23 | alias << 24
+// An alias piece (packer_sym) copies nothing: it re-reads a column sub-block of the rows the
+// N piece before it staged, as a T / H product (one HBM read, the product and its mirror).
+constexpr int kCBegin = 1 << 20, kCEnd = 1 << 21, kCDirect = 1 << 22, kCXStage = 1 << 23,
+              kCAlias = 1 << 24;
 
 struct OpSlot {
     int hdr[16];
@@ -243,11 +247,11 @@ __device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64
                                                int64_t in_off, int64_t out_off, int64_t info) {
     int4 c;
     c.x = (int)((rows << 16) | cols);
-    c.y = (int)in_off;
+    c.y = (info & kPiAlias) ? (int)(in_off | (((info >> 32) & 0xFFFF) << 16)) : (int)in_off;
     c.z = (int)out_off;
     c.w = (int)((info & 0xFFFF) | (mode << 16) | ((info & kPiBegin) ? kCBegin : 0) |
                 ((info & kPiEnd) ? kCEnd : 0) | ((info & kPiDirect) ? kCDirect : 0) |
-                ((info & kPiXStage) ? kCXStage : 0));
+                ((info & kPiXStage) ? kCXStage : 0) | ((info & kPiAlias) ? kCAlias : 0));
     return c;
 }
 
@@ -361,7 +365,7 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                     if (lane == 0)
                         mbar_arrive_expect_tx(&full[stage], (uint32_t)(((info >> 32) & 0xFFFFFF) * 16));
                 }
-                if (lane == 0) {
+                if (lane == 0 && !(info & kPiAlias)) {  // (alias pieces re-read staged rows)
                     unsigned char* dst =
                         stages + (size_t)stage * p.stage_bytes + (size_t)(info & 0xFFFFFF) * 16;
                     const double2* src = p.arena + m_off;
@@ -430,7 +434,7 @@ __device__ __forceinline__ int4 get_piece(const Params& p, const OpSlot* S, int 
                           __ldg(d + 7));
 }
 
-template <bool PROF, bool PEER, bool IO>
+template <bool PROF, bool PEER, bool IO, bool SYM>
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
                                          double2* outv, uint64_t* full, uint64_t* empty,
                                          uint64_t* opfull, uint64_t* opempty, OpSlot* slots,
@@ -545,7 +549,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                         }
                     }
                 }
-            } else if (g_mode == kModeH || g_mode == kModeS) {  // (NW rows went to outv directly)
+            } else if (g_mode == kModeH || g_mode == kModeS || (SYM && g_mode == kModeT)) {  // (NW: outv directly)
                 const int P = h_lanes(g_cols);
                 const int nJ = kConsumers / P;
                 const int cw = 32 / P;  // columns per warp: lane = column + cw * row offset
@@ -579,7 +583,9 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         for (int i = 0; i < pc_e - pc_b; ++i) {
             const int4 c = get_piece(p, S, pc_b, i);
             const int rows = c.x >> 16, cols = c.x & 0xFFFF;
-            const int in_off = c.y, out_off = c.z;
+            const bool alias = SYM && (c.w & kCAlias) != 0;
+            const int in_off = alias ? (c.y & 0xFFFF) : c.y, out_off = c.z;
+            const int rs = alias ? (c.y >> 16) : cols;  // smem row stride of the tile
             const int mode = (c.w >> 16) & 0xF;
             const bool direct = (c.w & kCDirect) != 0;
             if ((mode == kModeN || mode == kModeNW) ? (g_mode != mode)
@@ -740,14 +746,22 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                             ar += m.x;
                             ai += m.y;
                         }
+                    } else if (SYM && mode == kModeT) {  // transpose without conjugation (packer_sym)
+                        const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
+                        int r = pp;
+                        for (; r + P < rows; r += 2 * P) {
+                            cmac(ar, ai, tile[r * rs + j], xv[r]);
+                            cmac(br, bi, tile[(r + P) * rs + j], xv[r + P]);
+                        }
+                        if (r < rows) cmac(ar, ai, tile[r * rs + j], xv[r]);
                     } else {
                         const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
                         int r = pp;
                         for (; r + P < rows; r += 2 * P) {  // two independent chains
-                            cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
-                            cmac_conj(br, bi, tile[(r + P) * cols + j], xv[r + P]);
+                            cmac_conj(ar, ai, tile[r * rs + j], xv[r]);
+                            cmac_conj(br, bi, tile[(r + P) * rs + j], xv[r + P]);
                         }
-                        if (r < rows) cmac_conj(ar, ai, tile[r * cols + j], xv[r]);
+                        if (r < rows) cmac_conj(ar, ai, tile[r * rs + j], xv[r]);
                     }
                     accr[k] += ar + br;
                     acci[k] += ai + bi;
@@ -779,8 +793,8 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 const int64_t o = R.off + (pos - R.dst);
                 for (int q = 0; q < p.world; ++q) __stcg(p.peer_work[q] + o, v);
             } else if (flags & 2) {  // fp64 red.add into the pre-zeroed output (<= 2 addends per entry)
-                atomicAdd(&dp->x, v.x);
-                atomicAdd(&dp->y, v.y);
+                red_add_f64(&dp->x, v.x);
+                red_add_f64(&dp->y, v.y);
             } else if (flags & 1) {
                 const double2 o = __ldcg(dp);
                 __stcg(dp, make_double2(v.x + o.x, v.y + o.y));
@@ -836,7 +850,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     }
 }
 
-template <bool PROF, bool PEER, bool IO = false>
+template <bool PROF, bool PEER, bool IO = false, bool SYM = false>
 __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.stage_bytes, p.xin_max, p.out_max);
@@ -867,7 +881,7 @@ __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
     if (warp == kConsumerWarps) {
         producer<PROF, IO>(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer<PROF, PEER, IO>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
+        consumer<PROF, PEER, IO, SYM>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch
@@ -899,6 +913,12 @@ __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
 template <bool PROF>
 __global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
     run_cta<PROF, false>(p, blockIdx.x, gridDim.x);
+}
+
+// Symmetric single-triangle programs (packer_sym, UHMV_PROG_SYM): T-mode and alias pieces.
+template <bool PROF>
+__global__ void __maxnreg__(128) uhmv_bulk_sym_kernel(const Params p) {
+    run_cta<PROF, false, false, true>(p, blockIdx.x, gridDim.x);
 }
 
 // Host-I/O programs (uhmv_matvec_host with pinned buffers): x gathered over PCIe by the P1

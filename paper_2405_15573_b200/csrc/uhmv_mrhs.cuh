@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kThreads) uhmv_mrhs_kernel(const Params p) {
                             double* dp = reinterpret_cast<double*>(
                                              out_ptr(p, out_b, out_e, s0.out_off + n, &at) + rbase + r) + d;
                             if (at) {
-                                atomicAdd(dp, acc[mt][nt][v]);
+                                red_add_f64(dp, acc[mt][nt][v]);
                             } else {
                                 __stcg(dp, __ldcg(dp) + acc[mt][nt][v]);
                             }

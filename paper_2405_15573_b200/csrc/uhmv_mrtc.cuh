@@ -497,8 +497,8 @@ __device__ void consumer(const Params& p, double2* stages, const int* s_kv, uint
                 }
                 double2* dp = ps->out[j] + r;
                 if ((ps->atom[j >> 5] >> (j & 31)) & 1u) {
-                    atomicAdd(&dp->x, acc.x);
-                    atomicAdd(&dp->y, acc.y);
+                    red_add_f64(&dp->x, acc.x);
+                    red_add_f64(&dp->y, acc.y);
                 } else if (ps->first) {
                     __stcg(dp, acc);
                 } else {
@@ -568,8 +568,8 @@ __device__ void consumer(const Params& p, double2* stages, const int* s_kv, uint
                             double2* dp = base + mt * 8;
                             const double re = acc[mt][j][ee], im = acc[mt][j][2 + ee];
                             if (at) {
-                                atomicAdd(&dp->x, re);
-                                atomicAdd(&dp->y, im);
+                                red_add_f64(&dp->x, re);
+                                red_add_f64(&dp->y, im);
                             } else if (ps->first) {
                                 __stcg(dp, make_double2(re, im));
                             } else {

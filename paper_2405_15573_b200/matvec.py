@@ -26,13 +26,16 @@ import numpy as np
 from .device import DeviceOperator
 from .packer import pack
 
-__all__ = ["matvec_uh", "matmat_uh", "matvec_h", "device_operator", "register_device_operator", "clear_cache"]
+__all__ = ["matvec_uh", "matmat_uh", "matvec_h", "matvec_uh_sym", "device_operator", "register_device_operator",
+           "clear_cache"]
 
 _cache: dict = {}
 _cache_lock = threading.Lock()
 
 
 def _fingerprint(u):
+    if hasattr(u, "coupling"):  # SymmetricUniformHMatrix
+        return (id(u.bct), id(u.basis), id(u.coupling), len(u.coupling), id(u.dense), len(u.dense), u.kind)
     if hasattr(u, "admissible"):  # HMatrix
         return (id(u.bct), id(u.admissible), len(u.admissible), id(u.dense), len(u.dense))
     return (
@@ -48,6 +51,10 @@ def _fingerprint(u):
 
 
 def _pack_any(u):
+    if hasattr(u, "coupling"):
+        from .packer_sym import pack_sym
+
+        return pack_sym(u)
     if hasattr(u, "admissible") and not hasattr(u, "coeffs"):
         from .packer_h import pack_h
 
@@ -134,6 +141,36 @@ def matvec_h(h, v, workers: int = 1, adjoint: bool = False, stats=None):
     signature, ValueError, result dtype (hmatrix.py:155-157) and stats semantics (one count
     per admissible and dense block), run on the same sm_100a engine."""
     return matvec_uh(h, v, workers=workers, adjoint=adjoint, stats=stats)
+
+
+def matvec_uh_sym(us, v, workers: int = 1, adjoint: bool = False, stats=None):
+    """Matvec of the symmetric single-triangle variant (symmetric.py, paper Remark 4.5) with
+    the reference's ``matvec_uh`` signature and semantics (ValueError, result dtype, new array,
+    stats = |P+| + |P-| of the two-triangle operator).  Every stored slab is streamed once per
+    product (packer_sym).  Adjoint: the forward for a hermitian operator, conj(A conj(v)) for
+    a symmetric one (A^T = A)."""
+    n = us.shape[0]
+    conj = bool(adjoint) and us.kind == "symmetric"
+    if _is_torch_cuda(v):
+        if tuple(v.shape) != (n,):
+            raise ValueError(f"vector of shape {tuple(v.shape)} does not match operator input size {n}")
+        import torch
+
+        dop = device_operator(us, device=v.device)
+        x = v.to(torch.complex128)
+        out = dop.matvec(x.conj().resolve_conj() if conj else x)
+        if stats is not None:
+            stats.count(dop.packed.n_adm + dop.packed.n_dense)
+        return out.conj().resolve_conj() if conj else out
+    v = np.asarray(v)
+    if v.shape != (n,):
+        raise ValueError(f"vector of shape {v.shape} does not match operator input size {n}")
+    dtype = np.result_type(v.dtype, us._dtype)
+    dop = device_operator(us)
+    w = dop.matvec_array(np.conj(v) if conj else v, adjoint=False, dtype=dtype)
+    if stats is not None:
+        stats.count(dop.packed.n_adm + dop.packed.n_dense)
+    return np.conj(w) if conj else w
 
 
 def matmat_uh(u, V, adjoint: bool = False):

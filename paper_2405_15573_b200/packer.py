@@ -49,6 +49,7 @@ __all__ = ["PackedOperator", "Program", "pack", "MODE_N", "MODE_H", "MODE_S"]
 
 MODE_N, MODE_H, MODE_S = 0, 1, 2
 MODE_NW = 3  # bulk-kernel piece mode: an N piece of a wide-row op (one warp per row)
+MODE_T = 4  # out[j] += sum_r M[r,j] in[r]: H without the conjugation (symmetric variant, packer_sym)
 WIDE_COLS = 288  # an op whose N segments all have rows this long (<= 4 rows per stage) runs them warp-per-row
 BUF_ARENA, BUF_WORK, BUF_X, BUF_W = 0, 1, 2, 3
 RUN_ADD = 1  # out run: read-modify-write add (single writer)
@@ -61,6 +62,7 @@ OP_PEER = 16  # op field 12 flag (peer-exchange programs): the op writes peer da
 OP_XHOST = 32  # P1 op: gathers its x window from the host buffer and stores it into device x
 OP_XWAIT = 64  # NEAR op: its x windows come from device x -> the producer waits for them first
 OP_DRAIN = 128  # NEAR / FAR op: the last op finishing an output leaf copies w[leaf] to the host
+OP_XIN = 256  # op gathers its x runs into xin although its N pieces carry x windows (packer_sym NEAR)
 BUF_HOSTW = 4  # drain descriptor run (after the op's out runs): lo, len, counter, expected count
 
 OP_FIELDS = 16  # int32 per op
@@ -78,7 +80,10 @@ MR_ZERO = 1  # op flag: some output position is written by no group -- zero the 
 # 26 direct (no stage: coherent loads from the work buffer), 27 input read from x directly,
 # 28 x window carried in the stage behind the matrix rows (in_off = its x index),
 # [32,56) elements of the stage (on stage_begin pieces)
+# 29 alias: no copy -- the piece re-reads a sub-block of the stage data of the N piece before it
+# (its smem row stride in bits [32,56)); m_off / ld still address the arena (VM, checker)
 PI_BEGIN, PI_END, PI_DIRECT, PI_XGLOBAL, PI_XSTAGE = 1 << 24, 1 << 25, 1 << 26, 1 << 27, 1 << 28
+PI_ALIAS = 1 << 29
 
 KIND_P1, KIND_NEAR, KIND_RED, KIND_U, KIND_Z, KIND_FAR, KIND_ZERO = range(7)
 KIND_NAMES = ["P1", "NEAR", "RED", "U", "Z", "FAR", "ZERO"]
@@ -128,6 +133,7 @@ class Program:
     peer: bool = False  # multi-GPU peer-exchange program: ONE launch per rank, y/u stored into
     #                     the peers' work buffers and counters signalled across ranks (RUN_PEER)
     host_io: bool = False  # host-I/O program (OP_XHOST / OP_XWAIT / OP_DRAIN ops)
+    bulk_only: bool = False  # T-mode / alias pieces (packer_sym): only the bulk engine runs it
 
     @property
     def n_ops(self) -> int:
@@ -1112,17 +1118,23 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_pa
 
     split = []
     for sg in segs:  # H/S groups own at most BULK_HCOLS_MAX output columns: cut wider ones
-        m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off = sg
+        m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off = sg[:9]
+        alias = sg[9] if len(sg) > 9 else ()
         if mode != MODE_N and cols > min(h_panel, stage_elems // 2):
             for c0, c1 in _chunks(0, cols, min(h_panel, stage_elems // 2)):
-                split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off))
+                split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off, ()))
         elif mode == MODE_N and cols > min(ncols_max, stage_elems // 2):  # rows wider than a stage
             for c0, c1 in _chunks(0, cols, min(ncols_max, stage_elems // 2)):  # -> column panels
+                sub = []  # the alias sub-blocks (column ranges) that fall into this panel
+                for a0, ac, amode, a_in, a_out in alias:
+                    lo, hi = max(a0, c0), min(a0 + ac, c1)
+                    if lo < hi:
+                        sub.append((lo - c0, hi - lo, amode, a_in, a_out + (lo - a0)))
                 split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off + c0, out_off,
-                              x_off + c0 if x_off >= 0 else x_off))
+                              x_off + c0 if x_off >= 0 else x_off, tuple(sub)))
         else:
-            split.append(sg)
-    for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off in split:
+            split.append(tuple(sg[:9]) + (alias,))
+    for m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off, alias in split:
         xs = x_off >= 0 and has_x
         if buf == BUF_WORK:  # coherent in-kernel data: no bulk copy, no stage
             close()  # the open stage ends with the last staged piece
@@ -1149,6 +1161,9 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_pa
             else:
                 in_v = in_off + (r if mode != MODE_N else 0)
             out.append([m_off + r * ld, ld, n, cols, mode, in_v, out_off + (r if mode == MODE_N else 0), info])
+            # alias pieces: the same staged rows used a second time (one HBM read, two products)
+            for a0, ac, amode, a_in, a_out in alias:
+                out.append([m_off + r * ld + a0, ld, n, ac, amode, a_in + r, a_out, (fill + a0) | PI_ALIAS | (cols << 32)])
             fill += n * per_row + extra
             r += n
     close()
@@ -1219,7 +1234,7 @@ def _mr_groups(mr, n_out):
 
 
 def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, peer_limit=None,
-            h_panel=BULK_HCOLS_MAX):
+            h_panel=BULK_HCOLS_MAX, bulk_only=False):
     """Flatten op tuples into arrays in the phased order; the fused order is a
     permutation (``fused_order[ticket] = op index``).  ``keep_waits_on``: in a partial program
     keep only waits on counters signalled by ops of this kind inside the program.
@@ -1276,7 +1291,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         ordered = _order_segments(sg)
         seg_b = len(segs)
         for s in ordered:
-            segs.extend(_panel_split(s))
+            segs.extend(_panel_split(s[:9]))
         seg_e = len(segs)
         pc_b = len(pieces)
         nsg = [q for q in ordered if q[5] == MODE_N]
@@ -1290,7 +1305,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         pieces.extend(pcs)
         pc_e = len(pieces)
         mr_b = len(mr_segs)
-        mr, mr_flags = _mr_groups(_resolve_inputs(ordered, in_runs), n_out)
+        mr, mr_flags = ([], 0) if bulk_only else _mr_groups(_resolve_inputs([q[:9] for q in ordered], in_runs), n_out)
         mr_segs.extend(mr)
         mr_ranges.append((mr_b, len(mr_segs), mr_flags))
         w_b = len(waits)
@@ -1299,7 +1314,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         s_b = len(sigs)
         sigs.extend(sgn)
         s_e = len(sigs)
-        xin_len = 0 if (has_x and not kind & OP_XHOST) else n_in  # x windows travel in the stages
+        xin_len = 0 if (has_x and not kind & (OP_XHOST | OP_XIN)) else n_in  # x windows travel in the stages
         ops[i] = (n_in, n_out, in_b, in_e, seg_b, seg_e, out_b, out_e, w_b, w_e, s_b, s_e, kind | op_flags, pc_b, pc_e,
                   xin_len)
         in_max = max(in_max, n_in)
@@ -1325,4 +1340,5 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         stage_elems=stage_elems,
         mr_segs=np.asarray(mr_segs, dtype=np.int64).reshape(-1, MR_FIELDS),
         mr_ranges=np.asarray(mr_ranges, dtype=np.int32).reshape(-1, MR_RANGE_FIELDS),
+        bulk_only=bulk_only,
     )

@@ -29,7 +29,8 @@ import numpy as np
 from .uh_io import bct_from_arrays
 from .uh_types import ClusterBasis, CoefficientPair, UniformHMatrix
 
-__all__ = ["CONFIGS", "load_structure", "build_operator", "seeded_vector", "algorithmic_bytes", "workload_path"]
+__all__ = ["CONFIGS", "load_structure", "build_operator", "build_symmetric_operator", "seeded_vector",
+           "algorithmic_bytes", "workload_path"]
 
 HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "workloads")
 
@@ -151,6 +152,37 @@ def build_h_operator(cfg: int, seed: int = 0):
             adm[b] = SVDForm(qu[i], np.geomspace(1.0, 1e-6, k) if k else np.zeros(0), qv[i])
     u = build_operator(cfg, seed)
     return HMatrix(bct, adm, u.dense)
+
+
+def build_symmetric_operator(cfg: int, kind: str = "symmetric", seed: int = 0):
+    """Seeded symmetric single-triangle variant (symmetric.py, paper Remark 4.5) on the
+    config's reference structure: X_t = the row bases of ``build_operator``, the coupling of
+    every lower admissible block s_x s_y^H (ell_s x ell_t, s_y fresh Gaussian), the lower dense
+    leaves as stored and the diagonal ones symmetrised.  A labelled variant: not the
+    reference's operator (which stores both triangles)."""
+    from .symmetric import SymmetricUniformHMatrix, lower_blocks
+
+    u = build_operator(cfg, seed)
+    bct = u.bct
+    low_adm, low_dense = lower_blocks(bct)
+    basis = dict(u.row_basis.matrices)
+    for c in bct.col_map:
+        if c not in basis:
+            basis[c] = np.conj(u.col_basis.matrices[c]) if kind == "symmetric" else u.col_basis.matrices[c]
+    rng = np.random.default_rng([seed, 6])
+    coupling = {}
+    for b in low_adm:  # s_x of the block times a fresh s_y of the column cluster's (row) rank
+        blk = bct.nodes[b]
+        s_x = u.coeffs[b].s_x
+        s_y = _gauss(rng, (basis[blk.col].shape[1], s_x.shape[1]))
+        coupling[b] = s_x @ np.conj(s_y).T
+    dense = {}
+    for b in low_dense:
+        d = u.dense[b]
+        if bct.nodes[b].row == bct.nodes[b].col:
+            d = 0.5 * (d + (d.T if kind == "symmetric" else np.conj(d).T))
+        dense[b] = d
+    return SymmetricUniformHMatrix(bct, ClusterBasis(basis), coupling, dense, kind)
 
 
 def seeded_vector(n: int, seed: int = 0) -> np.ndarray:

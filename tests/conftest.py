@@ -22,7 +22,10 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long-running")
 
 
-GOLDEN_NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")) if not os.path.basename(p).startswith("h_"))
+GOLDEN_NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                      if not os.path.basename(p).startswith(("h_", "sym_")))
+# symmetric single-triangle variant fixtures (tools/make_golden_sym.py)
+SYM_NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "sym_*.npz")))
 
 _cache = {}
 
@@ -33,6 +36,17 @@ def load_golden(name):
 
         _cache[name] = load_uh(os.path.join(GOLDEN, f"{name}.npz"))
     return _cache[name]
+
+
+_sym_cache = {}
+
+
+def load_sym_golden(name):
+    if name not in _sym_cache:
+        from paper_2405_15573_b200.symmetric import load_sym
+
+        _sym_cache[name] = load_sym(os.path.join(GOLDEN, f"{name}.npz"))
+    return _sym_cache[name]
 
 
 def rel(a, b):

@@ -16,12 +16,12 @@ import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-_counts = {"matvec_uh": 0, "matvec_h": 0}
+_counts = {"matvec_uh": 0, "matvec_h": 0}  # + every other name install() rebinds
 
 
 def _counted(fn, name):
     def wrapper(*a, **k):
-        _counts[name] += 1
+        _counts[name] = _counts.get(name, 0) + 1
         return fn(*a, **k)
 
     wrapper.__wrapped__ = fn
