@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--slice", default="",
                     help="predict multi-GPU scaling on ONE GPU: comma-separated world sizes W; each rank's NCCL-path "
                          "programs (launch A + launch B of the W-way row partition) run alone on the whole GPU")
+    ap.add_argument("--slice-exchange", default="both", choices=["nccl", "peer", "both"],
+                    help="--slice: the NCCL path (launch A + B) and/or the fused peer-exchange launch (remote "
+                         "y/u counters pre-satisfied: the data of the other ranks assumed there when needed)")
     ap.add_argument("--ag-lat-us", type=float, default=15.0, help="--slice model: NCCL all-gather latency (us)")
     ap.add_argument("--ag-gbs", type=float, default=300.0, help="--slice model: NCCL all-gather bandwidth (GB/s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -535,6 +538,10 @@ def run_slice(args, config):
            "ag_model": {"lat_us": args.ag_lat_us, "gbs": args.ag_gbs}, "worlds": []}
     for W in [int(v) for v in args.slice.split(",") if v.strip()]:
         flush = l2_policy(args.config, W, args.l2)[0]
+        if args.slice_exchange in ("peer", "both"):
+            res["worlds_peer"] = res.get("worlds_peer", []) + [_slice_peer(args, packed, base, x, W, flush, t1, peak)]
+        if args.slice_exchange == "peer":
+            continue
         ranks = []
         for r in range(W):
             pr = packed.for_rank(r, W)
@@ -567,6 +574,76 @@ def run_slice(args, config):
             "predicted_speedup_no_exchange_cost": t1 / tmax,
         })
     print(json.dumps(res), flush=True)
+
+
+def _slice_peer(args, packed, base, x, W, flush, t1, peak):
+    """One rank of the fused peer-exchange path (``pack(peer=True)``: ONE launch per rank and
+    matvec) run alone on the whole GPU: its own work / counters / done flags, the peers'
+    buffers replaced by scratch, and before every epoch e the counters only OTHER ranks signal
+    set to their final value (need x e) and the peers' done flags to e -- i.e. the remote y/u
+    are taken to arrive by the time this rank needs them (the ranks run symmetric programs on
+    equal shares, and the all-gather payload is ~1 MB against GBs of operator)."""
+    import torch
+
+    from paper_2405_15573_b200.device import DeviceOperator
+    from paper_2405_15573_b200.dist import _execute_peer, _peer_rank
+
+    dev = base.device
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush_buf = torch.empty(int(2 * l2_bytes) // 4 + 1024, dtype=torch.float32, device=dev)
+    flush_rd = torch.zeros_like(flush_buf)
+    steps = max(args.steps, 20)
+    ranks_out = []
+    for r in range(W):
+        pr = packed.for_rank(r, W, peer=True)
+        op = DeviceOperator(pr, device=dev, share_arena_with=base)
+        prog = pr.adj if args.adjoint else pr.fwd
+        n_ctr = max(pr.fwd.n_counters, pr.adj.n_counters, 1)
+        wl = max(pr.work_len, 1)
+        own = (torch.zeros(2 * wl, dtype=torch.complex128, device=dev), torch.zeros(n_ctr, dtype=torch.int32, device=dev),
+               torch.zeros(W, dtype=torch.int32, device=dev))
+        dummy = (torch.zeros(2 * wl, dtype=torch.complex128, device=dev), torch.zeros(n_ctr, dtype=torch.int32, device=dev),
+                 torch.zeros(W, dtype=torch.int32, device=dev))
+        ranks = [_peer_rank(b[0].data_ptr(), wl, b[1].data_ptr(), b[2].data_ptr()) for b in
+                 [own if q == r else dummy for q in range(W)]]
+        signalled = set(int(c) for c in prog.sigs)
+        need = {}
+        for c, n in prog.waits:
+            if int(c) not in signalled:
+                need[int(c)] = max(need.get(int(c), 0), int(n))
+        idx = torch.tensor(sorted(need), dtype=torch.long, device=dev)
+        nv = torch.tensor([need[c] for c in sorted(need)], dtype=torch.int32, device=dev)
+        n_out = packed.n_cols if args.adjoint else packed.n_rows
+        out = torch.empty(n_out, dtype=torch.complex128, device=dev)
+        stream = torch.cuda.current_stream(dev)
+        epoch = 0
+        ts = []
+        for i in range(max(args.warmup, 3) + steps):
+            epoch += 1
+            if flush:
+                flush_buf.zero_()
+                flush_rd.sum()
+            if len(need):
+                own[1][idx] = nv * epoch
+            own[2].fill_(epoch)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            _execute_peer([op._plan], r, W, ranks, x, [out], args.adjoint, epoch, stream)
+            b.record(stream)
+            if i >= max(args.warmup, 3):
+                ts.append((a, b))
+        torch.cuda.synchronize(dev)
+        t = float(np.median([a.elapsed_time(b) for a, b in ts])) * 1e-3
+        nbytes = 16 * prog.arena_elems
+        ranks_out.append({"rank": r, "ms": t * 1e3, "bytes": nbytes, "frac": nbytes / t / 1e9 / peak,
+                          "remote_counters": len(need)})
+        op.close()
+        del op, own, dummy
+    tmax = max(q["ms"] for q in ranks_out) * 1e-3
+    bts = [q["bytes"] for q in ranks_out]
+    return {"W": W, "exchange": "peer (one launch per rank, remote y/u pre-satisfied)", "ranks": ranks_out,
+            "bytes_max_over_mean": max(bts) / (sum(bts) / W), "t_max_ms": tmax * 1e3,
+            "predicted_speedup": t1 / tmax, "predicted_efficiency": t1 / tmax / W}
 
 
 def ref_bytes_estimate(cfg, u=None):

@@ -40,6 +40,11 @@ constexpr int kRunPeer = 4;       // out-run flag (packer.RUN_PEER)
 constexpr int kOpXHost = 32;  // P1: gather x from the host buffer, publish it to device x
 constexpr int kOpXWait = 64;  // NEAR: the producer waits for the op's x windows in device x
 constexpr int kOpDrain = 128; // NEAR/FAR: the last op of an output leaf copies w[leaf] to the host
+// symmetric single-triangle programs (packer_sym OP_DUAL): the op's N pieces and their alias
+// T / H pieces write disjoint output ranges (own part vs mirror slots), so they need no barrier
+// between them, N rows go straight to outv, and a T group's register accumulators live across
+// the interleaved N pieces until the next T group (one flush per mirrored block, not per stage)
+constexpr int kOpDual = 512;
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
 static_assert((kRowGroups & (kRowGroups - 1)) == 0 && (kConsumers & (kConsumers - 1)) == 0,
@@ -474,6 +479,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         const bool peer_op = PEER && (S->hdr[12] & kOpPeer);  // (read while the slot is held)
         const bool xhost = IO && (S->hdr[12] & kOpXHost) != 0;
         const bool drain_op = IO && (S->hdr[12] & kOpDrain) != 0;
+        const bool dual = SYM && (S->hdr[12] & kOpDual) != 0;
         const int n_in_runs = in_e - in_b;
         const int n_runs = out_e - in_b;
         if (!p.skip_waits) {  // every consumer thread polls one dependency counter in parallel
@@ -524,9 +530,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         consumer_sync();
 
         double accr[kSlots], acci[kSlots];
-#pragma unroll
-        for (int k = 0; k < kSlots; ++k) accr[k] = acci[k] = 0.0;
-        const bool nreg = n_out <= kSlots * kRowGroups;
+        const bool nreg = n_out <= kSlots * kRowGroups && !dual;
         int g_mode = -1, g_out = 0, g_cols = 0;
         auto flush = [&]() {
             if (g_mode == kModeN) {
@@ -582,13 +586,21 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         }
         for (int i = 0; i < pc_e - pc_b; ++i) {
             const int4 c = get_piece(p, S, pc_b, i);
+            const int c_end = c.w & kCEnd;
             const int rows = c.x >> 16, cols = c.x & 0xFFFF;
             const bool alias = SYM && (c.w & kCAlias) != 0;
             const int in_off = alias ? (c.y & 0xFFFF) : c.y, out_off = c.z;
             const int rs = alias ? (c.y >> 16) : cols;  // smem row stride of the tile
             const int mode = (c.w >> 16) & 0xF;
             const bool direct = (c.w & kCDirect) != 0;
-            if ((mode == kModeN || mode == kModeNW) ? (g_mode != mode)
+            if (dual) {
+                if (mode != kModeN && mode != kModeNW && (g_mode != mode || g_out != out_off || g_cols != cols)) {
+                    flush();  // the previous mirrored block's T / H group (disjoint outputs: no barrier)
+                    g_mode = mode;
+                    g_out = out_off;
+                    g_cols = cols;
+                }
+            } else if ((mode == kModeN || mode == kModeNW) ? (g_mode != mode)
                                                     : (g_mode != mode || g_out != out_off || g_cols != cols)) {
                 // row-group (N), warp (NW) and column (H/S) owners differ: order their outv adds
                 const bool to_other = g_mode >= 0 && g_mode != mode &&
@@ -767,7 +779,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     acci[k] += ai + bi;
                 }
             }
-            if (!direct && (c.w & kCEnd)) {
+            if (!direct && c_end) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[stage]);
                 if (++stage == p.nstage) {

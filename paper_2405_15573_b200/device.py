@@ -93,13 +93,18 @@ class _DeviceProgram:
 class DeviceOperator:
     """A packed uniform H-matrix resident in HBM, with its C-ABI plan."""
 
-    def __init__(self, packed: PackedOperator, device=None, programs=None, share_with=None, share_arena_with=None):
+    def __init__(self, packed: PackedOperator, device=None, programs=None, share_with=None, share_arena_with=None,
+                 guard: int = 0):
         """``programs=(fwd, adj)`` overrides the packed programs; ``share_with`` reuses another
         DeviceOperator's arena / work / counter buffers (multi-GPU launch B);
-        ``share_arena_with`` reuses only its arena (the ranks of a peer-exchange emulation)."""
+        ``share_arena_with`` reuses only its arena (the ranks of a peer-exchange emulation).
+        ``guard`` > 0 (diagnostics, a compute-sanitizer stand-in): every buffer the kernels write
+        gets ``guard`` sentinel elements on both sides; :meth:`check_guards` verifies them."""
         torch = _torch()
         L = _lib.lib()
         self.torch = torch
+        self._guard = int(guard)
+        self._guards = []
         self.packed = packed
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         if dev.index is None:
@@ -129,14 +134,14 @@ class DeviceOperator:
                 self._arena_pad = pad
                 self.arena = torch.zeros(len(packed.arena) + pad + 16, dtype=torch.complex128, device=dev)
                 self.arena[: len(packed.arena)].copy_(torch.from_numpy(packed.arena))
-            self.work = torch.zeros(packed.work_len, dtype=torch.complex128, device=dev)
+            self.work = self.zeros(packed.work_len, torch.complex128)
             n_ctr = max(packed.fwd.n_counters, packed.adj.n_counters, 1)
-            self.counters = torch.zeros(n_ctr, dtype=torch.int32, device=dev)
-            self.ticket = torch.zeros(1, dtype=torch.int64, device=dev)
-            self.exit_count = torch.zeros(1, dtype=torch.int32, device=dev)
+            self.counters = self.zeros(n_ctr, torch.int32)
+            self.ticket = self.zeros(1, torch.int64)
+            self.exit_count = self.zeros(1, torch.int32)
             nmax = max(packed.n_rows, packed.n_cols, 1)
-            self.x_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
-            self.w_scratch = torch.zeros(nmax, dtype=torch.complex128, device=dev)
+            self.x_scratch = self.zeros(nmax, torch.complex128)
+            self.w_scratch = self.zeros(nmax, torch.complex128)
         self.fwd = _DeviceProgram(torch, fwd_p, dev)
         self.adj = _DeviceProgram(torch, adj_p, dev)
         d = _lib.UhmvDesc()
@@ -161,6 +166,40 @@ class DeviceOperator:
             _lib.check(L.uhmv_plan_create(ctypes.byref(d), ctypes.byref(handle)), "uhmv_plan_create")
         self._plan = handle
         self._lock = threading.Lock()
+
+    # ---- guarded buffers (diagnostics) ----
+    _SENTINEL = {8: 0x7FF8DEADBEEF0001, 4: 0x7EADBEEF}
+
+    def zeros(self, n, dtype):
+        """A zeroed device buffer of n elements; with ``guard`` it sits between two sentinel
+        bands (bit patterns: a NaN payload for 16-B / 8-B elements, 0x7EADBEEF for 4-B ones)."""
+        torch = self.torch
+        G = self._guard
+        if G <= 0:
+            return torch.zeros(max(int(n), 1), dtype=dtype, device=self.device)
+        n = max(int(n), 1)
+        buf = torch.empty(n + 2 * G, dtype=dtype, device=self.device)
+        iv = buf.view(torch.int64) if buf.element_size() >= 8 else buf.view(torch.int32)
+        iv.fill_(self._SENTINEL[iv.element_size()])
+        mid = buf[G : G + n]
+        mid.zero_()
+        self._guards.append((buf, G, n))
+        return mid
+
+    def check_guards(self) -> list:
+        """Names / offsets of sentinel elements some kernel overwrote ([] = clean)."""
+        torch = self.torch
+        bad = []
+        torch.cuda.synchronize(self.device)
+        for i, (buf, G, n) in enumerate(self._guards):
+            iv = buf.view(torch.int64) if buf.element_size() >= 8 else buf.view(torch.int32)
+            k = iv.numel() // buf.numel()
+            want = self._SENTINEL[iv.element_size()]
+            for lo, hi in ((0, G * k), ((G + n) * k, (2 * G + n) * k)):
+                hit = (iv[lo:hi] != want).nonzero()
+                if hit.numel():
+                    bad.append((i, int(hit[0]) + lo))
+        return bad
 
     # ---- info ----
     def launch_info(self, adjoint=False, mode=None):
@@ -314,7 +353,7 @@ class DeviceOperator:
         mr, work_len = self._mr_plan()
         need = work_len * Rp
         if getattr(self, "_work_mr", None) is None or self._work_mr.numel() < need:
-            self._work_mr = torch.zeros(need, dtype=torch.complex128, device=self.device)
+            self._work_mr = self.zeros(need, torch.complex128)
         rc = _lib.lib().uhmv_execute_mrhs(
             mr._plan, ctypes.c_void_p(Xp.data_ptr()), ctypes.c_void_p(W.data_ptr()),
             ctypes.c_void_p(self._work_mr.data_ptr()), int(Rp), int(adjoint), self._stream(stream),

@@ -63,6 +63,7 @@ OP_XHOST = 32  # P1 op: gathers its x window from the host buffer and stores it 
 OP_XWAIT = 64  # NEAR op: its x windows come from device x -> the producer waits for them first
 OP_DRAIN = 128  # NEAR / FAR op: the last op finishing an output leaf copies w[leaf] to the host
 OP_XIN = 256  # op gathers its x runs into xin although its N pieces carry x windows (packer_sym NEAR)
+OP_DUAL = 512  # packer_sym Z / NEAR: N pieces + alias T / H pieces with disjoint outputs (no barrier between)
 BUF_HOSTW = 4  # drain descriptor run (after the op's out runs): lo, len, counter, expected count
 
 OP_FIELDS = 16  # int32 per op

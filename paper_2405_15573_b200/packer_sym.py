@@ -8,7 +8,8 @@ out[j] += sum_r M[r,j] in[r]) or H (hermitian, conjugated) products -- the mirro
 
 Arena (complex128, 128-B aligned slabs):
   XS_L  leaf stacks of the ONE basis: rows of X_t of every ancestor t of leaf L, side by side
-  C_s   per cluster s: [S_b1 | S_b2 | ...] over its lower blocks b = (s, t) (t before s)
+  S_b   per lower block b = (s, t) (t before s): ell_s x ell_t, contiguous, grouped by s (a block
+        is staged whole, so its mirror product's register accumulators are flushed once)
   D_b   lower and diagonal dense leaves, grouped by row leaf
 
 Program (one; the adjoint is the forward for hermitian, conj(A conj x) for symmetric):
@@ -45,6 +46,7 @@ from .packer import (
     MODE_N,
     MODE_S,
     MODE_T,
+    OP_DUAL,
     OP_XIN,
     P1_CHUNK,
     RUN_ATOMIC,
@@ -113,14 +115,11 @@ def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0
     stacks = _stacks(tree, {c: None for c in rank}, rank)
     for leaf, (W, _cols) in sorted(stacks.items()):
         alloc(("XS", leaf), nodes[leaf].size * W, W)
-    cwidth, spos = {}, {}
+    cwidth = {}
     for s in sorted(lower_of):
-        w = 0
+        cwidth[s] = sum(rank[t] for _b, t in lower_of[s])
         for bid, t in lower_of[s]:
-            spos[bid] = w
-            w += rank[t]
-        cwidth[s] = w
-        alloc(("C", s), rank[s] * w, w)
+            alloc(("S", bid), rank[s] * rank[t], rank[t])
     dense_by_rleaf = {}
     for bid in low_dense:
         dense_by_rleaf.setdefault(bct.nodes[bid].row, []).append(bid)
@@ -137,9 +136,8 @@ def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0
         for c, c0 in cols:
             blk[:, c0 : c0 + rank[c]] = X[c][L.lo - nodes[c].lo : L.hi - nodes[c].lo]
     for s, blocks in lower_of.items():
-        cs = arena[offs[("C", s)] : offs[("C", s)] + rank[s] * cwidth[s]].reshape(rank[s], cwidth[s])
         for bid, t in blocks:
-            cs[:, spos[bid] : spos[bid] + rank[t]] = us.coupling[bid]
+            arena[offs[("S", bid)] : offs[("S", bid)] + rank[s] * rank[t]] = np.asarray(us.coupling[bid]).reshape(-1)
     for bid in low_dense:
         d = us.dense[bid]
         arena[offs[("D", bid)] : offs[("D", bid)] + d.size] = np.asarray(d).reshape(-1)
@@ -232,11 +230,11 @@ def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0
         ops[KIND_RED].append((KIND_RED, 0, rank[c], [], segs, [(BUF_WORK, y_off[c], rank[c], 0, 0)],
                               [(c_part[c], k)], [c_y[c]], k * rank[c]))
         y_wait[c] = [(c_y[c], 1)]
-    # Z: one op per (s, block group): N over the group's columns of C_s, T/H aliases per block
+    # Z: one op per (s, block group): per block an N segment (S_b y_t -> own slot) whose pieces
+    # are followed by alias T / H pieces (M(S_b) y_s -> the block's mirror slot)
     for s, groups in zgroups.items():
-        ls, cw = rank[s], cwidth[s]
+        ls = rank[s]
         for g, grp in enumerate(groups):
-            col0 = spos[grp[0][0]]
             k_in = sum(rank[t] for _b, t in grp)
             in_runs, waits, pos = [], list(y_wait[s]), 0
             for _b, t in grp:
@@ -244,14 +242,16 @@ def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0
                 waits.extend(y_wait[t])
                 pos += rank[t]
             in_runs.append((BUF_WORK, y_off[s], ls, pos, 0))  # y_s: the mirror products' input
-            alias, outs, sigs, oo = [], [(BUF_WORK, zreg[s] + g * ls, ls, 0, 0)], [c_zs[s]], ls
+            segs, outs, sigs, oo, pos = [], [(BUF_WORK, zreg[s] + g * ls, ls, 0, 0)], [c_zs[s]], ls, 0
             for bid, t in grp:
-                alias.append((spos[bid] - col0, rank[t], mmode, k_in, oo))
-                outs.append((BUF_WORK, zreg[t] + mirror_row[bid] * rank[t], rank[t], oo, 0))
+                lt = rank[t]
+                segs.append(_seg(offs[("S", bid)], BUF_ARENA, ls, lt, lt, MODE_N, pos, 0) + (((0, lt, mmode, k_in, oo),),))
+                outs.append((BUF_WORK, zreg[t] + mirror_row[bid] * lt, lt, oo, 0))
                 sigs.append(c_zs[t])
-                oo += rank[t]
-            seg = _seg(offs[("C", s)] + col0, BUF_ARENA, ls, k_in, cw, MODE_N, 0, 0) + (tuple(alias),)
-            ops[KIND_Z].append((KIND_Z, k_in + ls, oo, in_runs, [seg], outs, sorted(set(waits)), sigs, ls * k_in))
+                oo += lt
+                pos += lt
+            ops[KIND_Z].append((KIND_Z | OP_DUAL, k_in + ls, oo, in_runs, segs, outs, sorted(set(waits)), sigs,
+                                ls * k_in))
     # ZSUM: z_c = sum of its slot rows (fixed order)
     for c in y_off:
         if not zslot_rows[c]:
@@ -294,7 +294,7 @@ def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0
                     oo += C.size
                 segs.append(_seg(offs[("D", bid)], BUF_ARENA, R.size, C.size, C.size, MODE_N, 0, 0, C.lo) + (alias,))
                 nbytes += R.size * C.size
-            ops[KIND_NEAR].append((KIND_NEAR | OP_XIN, R.size, oo, [(BUF_X, R.lo, R.size, 0, 0)], segs, outs, [],
+            ops[KIND_NEAR].append((KIND_NEAR | OP_XIN | OP_DUAL, R.size, oo, [(BUF_X, R.lo, R.size, 0, 0)], segs, outs, [],
                                    sigs, nbytes))
     # WSUM: w[q] += sum of its slot rows (fixed order)
     for q in wleaves:
@@ -326,7 +326,7 @@ def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0
     phased = [ops[KIND_P1] + near, ops[KIND_RED], ops[KIND_Z], zsum_ops + wsum_ops, ops[KIND_FAR]]
     prog = _finish(phased, fused, n_ctr, stage_elems=stage_elems, bulk_only=True)
     basis_el = sum(nodes[c].size * rank[c] for c in rank)
-    coup_el = sum(rank[s] * cwidth[s] for s in cwidth)
+    coup_el = sum(rank[s] * cwidth[s] for s in cwidth)  # (the per-block slabs, without alignment)
     dense_el = sum(np.asarray(us.dense[b]).size for b in low_dense)
     return PackedOperator(
         n_rows=n, n_cols=n, dtype=np.dtype(us._dtype), arena=arena, work_len=max(work, 1), fwd=prog, adj=prog,

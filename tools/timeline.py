@@ -18,7 +18,8 @@ cfg = int(sys.argv[1])
 adj = len(sys.argv) > 2 and sys.argv[2] == "adj"
 view = sys.argv[3] if len(sys.argv) > 3 else "full"
 fmt = sys.argv[4] if len(sys.argv) > 4 else "uh"
-u = workloads.build_operator(cfg) if fmt == "uh" else workloads.build_h_operator(cfg)
+u = {"uh": workloads.build_operator, "h": workloads.build_h_operator,
+     "sym": workloads.build_symmetric_operator}[fmt](cfg)
 if view != "full":
     from matvec_oracle import farfield_only, nearfield_only
 
@@ -27,6 +28,10 @@ if fmt == "h":
     from paper_2405_15573_b200.packer_h import pack_h
 
     op = DeviceOperator(pack_h(u), device="cuda:0")
+elif fmt == "sym":
+    from paper_2405_15573_b200.packer_sym import pack_sym
+
+    op = DeviceOperator(pack_sym(u), device="cuda:0")
 else:
     op = DeviceOperator(pack(u), device="cuda:0")
 x = torch.from_numpy(workloads.seeded_vector(u.shape[0] if adj else u.shape[1], 0)).cuda()
@@ -37,7 +42,7 @@ prog = op.progs[1] if adj else op.progs[0]
 ticket = np.empty(prog.n_ops, dtype=np.int64)
 ticket[prog.fused_order] = np.arange(prog.n_ops)
 span = t[:, 2].max()
-print(f"cfg{cfg} {'adj' if adj else 'fwd'} {view}: span {span / 1e3:.1f} us, ops {prog.n_ops}")
+print(f"cfg{cfg} {fmt} {'adj' if adj else 'fwd'} {view}: span {span / 1e3:.1f} us, ops {prog.n_ops}")
 for k in range(7):
     m = kinds == k
     if not m.any():
