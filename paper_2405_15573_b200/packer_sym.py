@@ -83,8 +83,12 @@ def _groups(items, width, cap):
     return out
 
 
-def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0.2, 0.5),
+def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=None,
              group_out: int = SYM_GROUP_OUT) -> PackedOperator:
+    import os
+
+    if near_interleave is None:
+        near_interleave = tuple(float(v) for v in os.environ.get("UHMV_SYM_INTERLEAVE", "0.3,0.1,0.2,0.4").split(","))
     bct = us.bct
     tree = bct.row_tree
     nodes = tree.nodes
@@ -321,8 +325,11 @@ def pack_sym(us, *, stage_elems: int = STAGE_ELEMS, near_interleave=(0.2, 0.1, 0
     f = f / f[-1]
     cut = [int(round(v * len(near))) for v in f]
     parts = [near[cut[i] : cut[i + 1]] for i in range(len(near_interleave))] + [[], [], [], []]
-    fused = (ops[KIND_P1] + parts[0] + ops[KIND_RED] + parts[1] + ops[KIND_Z] + parts[2] + zsum_ops + parts[3]
-             + ops[KIND_FAR] + wsum_ops)
+    # chain first (ZSUM right behind the Z ops, FAR before the last nearfield share): the
+    # nearfield (no dependencies) fills the gaps, and WSUM -- which waits for every NEAR op
+    # of its leaf -- closes the program
+    fused = (ops[KIND_P1] + parts[0] + ops[KIND_RED] + parts[1] + ops[KIND_Z] + zsum_ops + parts[2]
+             + ops[KIND_FAR] + parts[3] + wsum_ops)
     phased = [ops[KIND_P1] + near, ops[KIND_RED], ops[KIND_Z], zsum_ops + wsum_ops, ops[KIND_FAR]]
     prog = _finish(phased, fused, n_ctr, stage_elems=stage_elems, bulk_only=True)
     basis_el = sum(nodes[c].size * rank[c] for c in rank)
