@@ -719,6 +719,12 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(bulk::uhmv_bulk_kernel<true>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
+    // the whole shared-memory carveout: several CTAs per SM need it (the driver's default
+    // choice can leave room for one CTA of ~110 KB only)
+    for (const void* fn : {(const void*)bulk::uhmv_bulk_kernel<false>, (const void*)bulk::uhmv_bulk_kernel<true>,
+                           (const void*)bulk::uhmv_bulk_sym_kernel<false>, (const void*)bulk::uhmv_bulk_sym_kernel<true>,
+                           (const void*)bulk::uhmv_bulk_io_kernel, (const void*)bulk::uhmv_bulk_peer_kernel})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) {
         delete p;
         return cuda_fail(e, "cudaFuncSetAttribute(bulk)");

@@ -28,7 +28,15 @@
 
 namespace bulk {
 
-constexpr int kConsumerWarps = 4;
+// consumer warps per CTA and the register cap (build-time experiments: -DUHMV_CWARPS=8
+// -DUHMV_BULK_REGS=112 with UHMV_BULK_CTAS=2 runs 16 consumer warps per SM instead of 12)
+#ifndef UHMV_CWARPS
+#define UHMV_CWARPS 4
+#endif
+#ifndef UHMV_BULK_REGS
+#define UHMV_BULK_REGS 128
+#endif
+constexpr int kConsumerWarps = UHMV_CWARPS;
 constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
 
@@ -464,7 +472,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             if (prof)
                 for (int i = 0; i < 56; ++i) p.prof[(size_t)blockIdx.x * 64 + i] = sprof[i];
             __syncwarp();
-            if (PROF && lane == 0) p.prof[(size_t)blockIdx.x * 64 + 58 + (tid >> 5)] = sprof[58 + (tid >> 5)];
+            if (PROF && lane == 0) p.prof[(size_t)blockIdx.x * 64 + 58 + ((tid >> 5) & 3)] = sprof[58 + ((tid >> 5) & 3)];
             break;
         }
         if (PROF && tid == 0 && p.trace) {
@@ -621,7 +629,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                     }
                     long long tw = PROF ? clock64() : 0;
                     mbar_wait(&full[stage], sphase);
-                    if (PROF && lane == 0) sprof[58 + (tid >> 5)] += clock64() - tw;  // every warp
+                    if (PROF && lane == 0) sprof[58 + ((tid >> 5) & 3)] += clock64() - tw;  // every warp
                     if (prof) {
                         const long long t1 = clock64();
                         pr[kind * 8 + 0] += t1 - t0;
@@ -923,24 +931,24 @@ __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
 }
 
 template <bool PROF>
-__global__ void __maxnreg__(128) uhmv_bulk_kernel(const Params p) {
+__global__ void __maxnreg__(UHMV_BULK_REGS) uhmv_bulk_kernel(const Params p) {
     run_cta<PROF, false>(p, blockIdx.x, gridDim.x);
 }
 
 // Symmetric single-triangle programs (packer_sym, UHMV_PROG_SYM): T-mode and alias pieces.
 template <bool PROF>
-__global__ void __maxnreg__(128) uhmv_bulk_sym_kernel(const Params p) {
+__global__ void __maxnreg__(UHMV_BULK_REGS) uhmv_bulk_sym_kernel(const Params p) {
     run_cta<PROF, false, false, true>(p, blockIdx.x, gridDim.x);
 }
 
 // Host-I/O programs (uhmv_matvec_host with pinned buffers): x gathered over PCIe by the P1
 // ops, finished output leaves drained to the host by their last NEAR / FAR op.
-__global__ void __maxnreg__(128) uhmv_bulk_io_kernel(const Params p) {
+__global__ void __maxnreg__(UHMV_BULK_REGS) uhmv_bulk_io_kernel(const Params p) {
     run_cta<false, false, true>(p, blockIdx.x, gridDim.x);
 }
 
 // Peer-exchange programs: L.nranks ranks share the grid (n = 1 on a real multi-GPU rank).
-__global__ void __maxnreg__(128) uhmv_bulk_peer_kernel(const __grid_constant__ PeerLaunch L) {
+__global__ void __maxnreg__(UHMV_BULK_REGS) uhmv_bulk_peer_kernel(const __grid_constant__ PeerLaunch L) {
     const int n = L.nranks;
     const int r = (int)(((long long)blockIdx.x * n) / gridDim.x);
     const int lo = (int)(((long long)r * gridDim.x + n - 1) / n);

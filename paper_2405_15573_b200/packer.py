@@ -95,6 +95,9 @@ ROWS_PER_CHUNK = 16  # output rows per NEAR op (= consumer row-groups: one row e
 MR_ROWS = 80  # multi-RHS programs: NEAR / FAR output rows per op (= mrtc kNP, one pass)
 FAR_ROWS = 64  # output rows per FAR op (4 register slots of 16 row-groups)
 P1_CHUNK = 256  # max input rows per P1 op
+# adjoint NEAR: output columns per op (default: the whole leaf; 40- / 27-column panels measured
+# 1.36x / 1.59x slower at config 3 -- strided per-row copies make the producer the bottleneck)
+ADJ_NEAR_COLS = int(os.environ.get("UHMV_ADJ_NEAR_COLS", 1 << 30))
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_NCOLS_MAX = 640  # widest N piece row (two rows + x window still fit a stage)
 NW_COLS = int(os.environ.get("UHMV_NW_COLS", 640))  # widest panel of a warp-per-row op (sweeps: 352/176 slower)
@@ -939,7 +942,9 @@ def _build_program(
         dlist = dense_by_outleaf.get(leaf, [])
         # forward: row chunks of the leaf; adjoint: the whole column leaf (H segments reduce
         # over the block rows, so the op owns all |c| output entries of the leaf)
-        near_chunks = _chunks(n.lo, n.hi, rows_per_chunk) if not adjoint else [(n.lo, n.hi)]
+        # (adjoint: column panels of the leaf, ADJ_NEAR_COLS wide -- the H segments reduce over
+        # the block rows, so an op owns whole output columns)
+        near_chunks = _chunks(n.lo, n.hi, rows_per_chunk if not adjoint else ADJ_NEAR_COLS)
         for a, b in near_chunks:
             if not dlist:
                 continue
@@ -958,9 +963,9 @@ def _build_program(
                 else:
                     r = bct.row_tree.nodes[blk.row]
                     in_runs.append((BUF_X, r.lo, r.size, pos, 0))
-                    segs.append(_seg(offs[("D", bid)], BUF_ARENA, r.size, n.size, n.size, MODE_H, pos, 0, r.lo))
+                    segs.append(_seg(offs[("D", bid)] + (a - n.lo), BUF_ARENA, r.size, rows, n.size, MODE_H, pos, 0, r.lo))
                     pos += r.size
-                    nbytes += r.size * n.size
+                    nbytes += r.size * rows
             kind, waits_n, outs_n = KIND_NEAR, [], [(BUF_W, a, rows, 0, RUN_ATOMIC)]
             if host_io:
                 kind |= OP_XWAIT | OP_DRAIN

@@ -15,7 +15,10 @@ KEYS = [
     "launch__occupancy_limit_registers", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-    "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second",
+    "lts__t_sector_hit_rate.pct", "sm__cycles_elapsed.avg.per_second", "smsp__inst_executed.sum",
+    # FP64 tensor pipe (DMMA) of the multi-RHS engine (names from ncu --query-metrics --chip gb100)
+    "smsp__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_dmma.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
