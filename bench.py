@@ -427,7 +427,8 @@ def main():
     alg_bytes_total = workloads.algorithmic_bytes(packed)
     value = 1.0 / med_s
     achieved = alg_bytes_total / world / med_s / 1e9  # per GPU
-    traffic = load_traffic(args.config) if args.format == "uh" else None
+    traffic = (load_traffic(args.config) if args.format == "uh" and args.view == "full" and not args.adjoint
+               else load_traffic(f"sym_cfg{args.config}" if args.format == "sym" else None))
     roofline = {
         "bound": "hbm",
         "achieved": achieved,
@@ -790,7 +791,7 @@ def load_traffic(cfg):
         return None
     with open(path) as fh:
         d = json.load(fh)
-    v = d.get(f"cfg{cfg}")
+    v = d.get(cfg if isinstance(cfg, str) else f"cfg{cfg}") if cfg is not None else None
     return float(v) if v is not None else None
 
 
