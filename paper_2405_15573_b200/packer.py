@@ -483,12 +483,16 @@ def pack(
         part = _partition(geo, world, rank)
     else:
         part = None
-    split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in SPLIT_DEFAULTS.items()}
+    op_bytes = 16 * (bytes_bases + bytes_coupling + bytes_dense)
+    tiny = op_bytes < 2e8  # config 1 (99 MB): bound by the P1 -> RED -> U -> Z -> FAR chain
     if near_interleave is None:
         # forward nearfield shares between the farfield phases (measured): operators under
-        # ~1 GB are chain-latency-bound and want the chain started early (configs 1-2: -3..4%)
-        small = 16 * (bytes_bases + bytes_coupling + bytes_dense) < 1e9
-        near_interleave = (0.2, 0.1, 0.2, 0.5) if small else (0.35, 0.1, 0.2, 0.35)
+        # ~1 GB are chain-latency-bound and want the chain started early (configs 1-2: -3..4%);
+        # under ~200 MB almost all of the nearfield goes behind the chain
+        small = op_bytes < 1e9
+        near_interleave = (0.05, 0.05, 0.1, 0.8) if tiny else (0.2, 0.1, 0.2, 0.5) if small else (0.35, 0.1, 0.2, 0.35)
+    split_def = dict(SPLIT_DEFAULTS, **({"z_rows": 13} if tiny else {}))  # config 1: Z ops in two row parts
+    split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in split_def.items()}
     if os.environ.get("UHMV_NEAR_INTERLEAVE"):
         near_interleave = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE"].split(","))
     if os.environ.get("UHMV_NEAR_INTERLEAVE_ADJ"):

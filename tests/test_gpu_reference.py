@@ -149,3 +149,34 @@ def test_real_h_operator(cfg):
         e_st = rel(ours, out["ref_h_adj" if adjoint else "ref_h_fwd"])
         assert e_box <= 1e-12 and e_st <= 1e-12, (adjoint, e_box, e_st)
     pk.clear_cache()
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_real_operator_symmetric_variant(cfg):
+    """The symmetric single-triangle variant (paper Remark 4.5) of the REAL compress-path
+    operator: the GPU engine against the reference's matvec_uh on the variant's two-triangle
+    expansion (a genuine uhm_kit UniformHMatrix) at 1e-12, and the variant's distance to the
+    operator itself (the icosphere Nystrom weights make the Helmholtz matrix only nearly
+    symmetric) recorded in gpurun_out/ for DESIGN.md."""
+    u, out = _real(cfg)
+    import uhm_kit.uniform as ref_uniform
+
+    import paper_2405_15573_b200 as pk
+    from paper_2405_15573_b200.symmetric import expand_uh, storage_sym, symmetrize_uh
+
+    us = symmetrize_uh(u, "symmetric")
+    full = expand_uh(us, types=ref_uniform)
+    x = out["xf"]
+    ours = pk.matvec_uh_sym(us, x)
+    ref = ref_uniform.matvec_uh(full, x)
+    assert rel(ours, ref) <= 1e-12
+    ours_a = pk.matvec_uh_sym(us, out["xa"], adjoint=True)
+    assert rel(ours_a, ref_uniform.matvec_uh(full, out["xa"], adjoint=True)) <= 1e-12
+    dist = rel(ours, out["ref_full_fwd"])
+    st = storage_sym(us)
+    log = os.path.join(ROOT, "gpurun_out")
+    if os.path.isdir(log):
+        with open(os.path.join(log, f"real_cfg{cfg}_symmetric.json"), "w") as fh:
+            json.dump({"cfg": cfg, "rel_diff_to_operator": dist, "storage_ratio": st["total"] / st["two_triangle_total"],
+                       "bytes_estimate_sym": st["bytes_estimate"]}, fh)
+    pk.clear_cache()
