@@ -55,8 +55,25 @@ constexpr int kOpDrain = 128; // NEAR/FAR: the last op of an output leaf copies 
 constexpr int kOpDual = 512;
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
-static_assert((kRowGroups & (kRowGroups - 1)) == 0 && (kConsumers & (kConsumers - 1)) == 0,
-              "row groups / column groups are addressed with power-of-2 masks");
+constexpr bool kPow2 = (kConsumers & (kConsumers - 1)) == 0;
+// owner index v mod m (v may be negative): a mask for the power-of-2 consumer counts
+template <int M>
+__device__ __forceinline__ int wrapc(int v) {
+    if constexpr ((M & (M - 1)) == 0) {
+        return v & (M - 1);
+    } else {
+        const int r = v % M;
+        return r < 0 ? r + M : r;
+    }
+}
+__device__ __forceinline__ int wrap_nj(int v, int nJ) {  // nJ = kConsumers / P, P in {1, 2, 4}
+    if constexpr (kPow2) {
+        return v & (nJ - 1);
+    } else {
+        const int r = v % nJ;
+        return r < 0 ? r + nJ : r;
+    }
+}
 constexpr int kPieceFields = 8;
 constexpr int kSlots = 4;         // register accumulator slots per thread
 constexpr int kSlotRuns = 48;     // run descriptors cached per op slot
@@ -566,7 +583,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 const int nJ = kConsumers / P;
                 const int cw = 32 / P;  // columns per warp: lane = column + cw * row offset
                 const int pp = lane / cw;
-                const int j0 = ((tid >> 5) * cw + (lane & (cw - 1)) - g_out) & (nJ - 1);  // powers of 2
+                const int j0 = wrap_nj((tid >> 5) * cw + (lane & (cw - 1)) - g_out, nJ);
 #pragma unroll
                 for (int k = 0; k < kSlots; ++k) {
                     if (k * nJ >= g_cols) break;
@@ -644,7 +661,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 // diagnostics: no compute
             } else if (mode == kModeN) {
                 const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
-                const int r0 = (rg - out_off) & (kRowGroups - 1);  // first row of this row group
+                const int r0 = wrapc<kRowGroups>(rg - out_off);  // first row of this row group
                 for (int r = r0; r < rows; r += kRowGroups) {
                     const double2* T = tile + r * cols + g;
                     const double2* X = xv + g;
@@ -703,7 +720,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 // warp; row o belongs to warp o mod 4 in every piece (deterministic outv adds)
                 const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
                 const int w = tid >> 5;
-                for (int r = (w - out_off) & (kConsumerWarps - 1); r < rows; r += kConsumerWarps) {
+                for (int r = wrapc<kConsumerWarps>(w - out_off); r < rows; r += kConsumerWarps) {
                     const double2* T = tile + r * cols + lane;
                     const double2* X = xv + lane;
                     double ar = 0.0, ai = 0.0, br = 0.0, bi = 0.0;
@@ -745,7 +762,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 // loads); the P lanes of a column sit cw apart in the warp
                 const int cw = 32 / P;
                 const int pp = lane / cw;
-                const int j0 = ((tid >> 5) * cw + (lane & (cw - 1)) - out_off) & (nJ - 1);
+                const int j0 = wrap_nj((tid >> 5) * cw + (lane & (cw - 1)) - out_off, nJ);
                 int64_t dm = 0, dld = 0;
                 if (direct) {
                     const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
