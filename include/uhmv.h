@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 11
+#define UHMV_ABI_VERSION 12
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -84,6 +84,8 @@ typedef struct uhmv_program {
 } uhmv_program;
 
 #define UHMV_PROG_SYM 1
+#define UHMV_PROG_XWIN 2 /* windowed-input ops (H-format FAR, packer_h OP_XWIN): the bulk engine runs
+                            them with uhmv_bulk_xwin_kernel; no peer / host-I/O programs          */
 
 /* A packed uniform H-matrix.  Replaces the UniformHMatrix dicts (uniform.py:90-117). */
 typedef struct uhmv_desc {

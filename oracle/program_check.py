@@ -130,6 +130,9 @@ def check_program(prog, *, arena_len, arena_pad, work_len, n_in_vec, n_out_vec):
             if info & PI_XSTAGE:
                 if in_off < 0 or in_off + span > n_in_vec:
                     _fail(f"op {i} piece {j}: x window [{in_off}, {in_off + span}) of {n_in_vec}")
+            elif kind & 1024:  # OP_XWIN: the input is gathered window by window (xin_len each)
+                if mode not in (MODE_N, MODE_NW) or in_off < 0 or in_off + span > n_in or span > xin_len:
+                    _fail(f"op {i} piece {j}: windowed input [{in_off}, {in_off + span}) of {n_in} (window {xin_len})")
             elif mode != MODE_S and (in_off < 0 or in_off + span > xin_len):
                 _fail(f"op {i} piece {j}: xin [{in_off}, {in_off + span}) of {xin_len}")
             if m_off < 0 or m_off + (rows - 1) * ld + cols > arena_len:

@@ -721,7 +721,10 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
     // the whole shared-memory carveout: several CTAs per SM need it (the driver's default
     // choice can leave room for one CTA of ~110 KB only)
+    for (const void* fn : {(const void*)bulk::uhmv_bulk_xwin_kernel<false>, (const void*)bulk::uhmv_bulk_xwin_kernel<true>})
+        if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin);
     for (const void* fn : {(const void*)bulk::uhmv_bulk_kernel<false>, (const void*)bulk::uhmv_bulk_kernel<true>,
+                           (const void*)bulk::uhmv_bulk_xwin_kernel<false>, (const void*)bulk::uhmv_bulk_xwin_kernel<true>,
                            (const void*)bulk::uhmv_bulk_sym_kernel<false>, (const void*)bulk::uhmv_bulk_sym_kernel<true>,
                            (const void*)bulk::uhmv_bulk_io_kernel, (const void*)bulk::uhmv_bulk_peer_kernel})
         if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -731,8 +734,12 @@ int uhmv_plan_create(const uhmv_desc* desc, uhmv_plan** out) {
     }
     for (int k = 0; k < 2; ++k) {
         int per_sm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bulk::uhmv_bulk_kernel<false>,
-                                                          bulk::kThreads, p->bulk_smem[k]);
+        const bool sym = (progs[k]->flags & UHMV_PROG_SYM) != 0;
+        const bool xw = (progs[k]->flags & UHMV_PROG_XWIN) != 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, sym ? (const void*)bulk::uhmv_bulk_sym_kernel<false>
+                         : xw ? (const void*)bulk::uhmv_bulk_xwin_kernel<false> : (const void*)bulk::uhmv_bulk_kernel<false>,
+            bulk::kThreads, p->bulk_smem[k]);
         if (e != cudaSuccess) {
             delete p;
             return cuda_fail(e, "occupancy(bulk)");
@@ -955,7 +962,12 @@ static int execute_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, in
         bulk::Params bp = make_bulk_params(plan, pr, k, x, w);
         cudaStream_t st = static_cast<cudaStream_t>(stream);
         const bool sym = (pr.flags & UHMV_PROG_SYM) != 0;
-        if (bp.prof && sym)
+        if (pr.flags & UHMV_PROG_XWIN) {
+            if (bp.prof)
+                bulk::uhmv_bulk_xwin_kernel<true><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
+            else
+                bulk::uhmv_bulk_xwin_kernel<false><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
+        } else if (bp.prof && sym)
             bulk::uhmv_bulk_sym_kernel<true><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
         else if (sym)
             bulk::uhmv_bulk_sym_kernel<false><<<plan->bulk_grid[k], bulk::kThreads, plan->bulk_smem[k], st>>>(bp);
@@ -997,6 +1009,8 @@ int uhmv_plan_set_io(uhmv_plan* plan, const uhmv_program* fwd, const uhmv_progra
     if (!fwd || !adj || !counters) return fail(UHMV_EINVAL, "uhmv_plan_set_io: null argument");
     int rc = check_program(*fwd, "io fwd");
     if (rc || (rc = check_program(*adj, "io adj"))) return rc;
+    if ((fwd->flags | adj->flags) & (UHMV_PROG_SYM | UHMV_PROG_XWIN))
+        return fail(UHMV_EINVAL, "uhmv_plan_set_io: symmetric / windowed programs have no host-I/O engine");
     cudaError_t e = cudaSetDevice(plan->d.device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
     const uhmv_program* progs[2] = {fwd, adj};
@@ -1035,6 +1049,9 @@ int uhmv_execute_peer(uhmv_plan* const* plans, int nplans, int rank0, int world,
         if (!ranks[q].work || !ranks[q].counters || !ranks[q].done || ranks[q].work_len < 0)
             return fail(UHMV_EINVAL, "uhmv_execute_peer: null peer buffer");
     const int k = adjoint ? 1 : 0;
+    for (int i = 0; i < nplans; ++i)
+        if ((adjoint ? plans[i]->d.adj : plans[i]->d.fwd).flags & (UHMV_PROG_SYM | UHMV_PROG_XWIN))
+            return fail(UHMV_EINVAL, "uhmv_execute_peer: symmetric / windowed programs have no peer engine");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int grid = 0, smem = 0;
     for (int i = 0; i < nplans; ++i) {

@@ -53,6 +53,10 @@ constexpr int kOpDrain = 128; // NEAR/FAR: the last op of an output leaf copies 
 // between them, N rows go straight to outv, and a T group's register accumulators live across
 // the interleaved N pieces until the next T group (one flush per mirrored block, not per stage)
 constexpr int kOpDual = 512;
+// windowed-input ops (packer_h FAR, OP_XWIN): the op's N pieces read a gathered input far
+// longer than shared memory allows at 3 CTAs/SM; it is gathered window by window (hdr[15]
+// elements, hdr[0] in total) in piece order, one consumer barrier pair per window
+constexpr int kOpXWin = 1024;
 constexpr int kLanesPerRow = 8;
 constexpr int kRowGroups = kConsumers / kLanesPerRow;  // 16
 constexpr bool kPow2 = (kConsumers & (kConsumers - 1)) == 0;
@@ -464,7 +468,7 @@ __device__ __forceinline__ int4 get_piece(const Params& p, const OpSlot* S, int 
                           __ldg(d + 7));
 }
 
-template <bool PROF, bool PEER, bool IO, bool SYM>
+template <bool PROF, bool PEER, bool IO, bool SYM, bool XWIN = false>
 __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages, double2* xin,
                                          double2* outv, uint64_t* full, uint64_t* empty,
                                          uint64_t* opfull, uint64_t* opempty, OpSlot* slots,
@@ -529,28 +533,34 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         }
         // gather the input vector: all loads of a batch issued before any smem store
         const int n_in = (p.dbg & 2) ? 0 : S->hdr[15];  // work inputs only (x rides in stages)
-        for (int base = 0; base < n_in; base += kGatherBatch * kConsumers) {
-            double2 v[kGatherBatch];
+        const bool xwin = XWIN && (S->hdr[12] & kOpXWin) != 0;
+        const int n_in_all = xwin ? S->hdr[0] : n_in;  // windowed: hdr[15] is the window length
+        int xw_lo = 0;
+        auto gather = [&](int lo, int hi) {  // positions [lo, hi) of the input -> xin[pos - lo]
+            for (int base = lo; base < hi; base += kGatherBatch * kConsumers) {
+                double2 v[kGatherBatch];
 #pragma unroll
-            for (int k = 0; k < kGatherBatch; ++k) {
-                const int pos = base + tid + k * kConsumers;
-                if (pos < n_in) {
-                    const RunRef R = get_run(p, S, in_b, find_run(p, S, in_b, 0, n_in_runs, pos));
-                    const int64_t src = R.off + (pos - R.dst);
-                    if ((R.bf & 0xFF) != kBufX) v[k] = __ldcg(p.work + src);
-                    else v[k] = xhost ? __ldcg(p.x_host + src) : __ldg(p.x + src);  // host: over PCIe
+                for (int k = 0; k < kGatherBatch; ++k) {
+                    const int pos = base + tid + k * kConsumers;
+                    if (pos < hi) {
+                        const RunRef R = get_run(p, S, in_b, find_run(p, S, in_b, 0, n_in_runs, pos));
+                        const int64_t src = R.off + (pos - R.dst);
+                        if ((R.bf & 0xFF) != kBufX) v[k] = __ldcg(p.work + src);
+                        else v[k] = xhost ? __ldcg(p.x_host + src) : __ldg(p.x + src);  // host: over PCIe
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kGatherBatch; ++k) {
+                    const int pos = base + tid + k * kConsumers;
+                    if (pos < hi) {
+                        xin[pos - lo] = v[k];
+                        // host-I/O P1 op: its one input run is x[a:b] -- publish it for the NEAR ops
+                        if (xhost) __stcg(const_cast<double2*>(p.x) + S->roff[0] + pos, v[k]);
+                    }
                 }
             }
-#pragma unroll
-            for (int k = 0; k < kGatherBatch; ++k) {
-                const int pos = base + tid + k * kConsumers;
-                if (pos < n_in) {
-                    xin[pos] = v[k];
-                    // host-I/O P1 op: its one input run is x[a:b] -- publish it for the NEAR ops
-                    if (xhost) __stcg(const_cast<double2*>(p.x) + S->roff[0] + pos, v[k]);
-                }
-            }
-        }
+        };
+        gather(0, xwin ? min(n_in, n_in_all) : n_in);
         for (int i = tid; i < n_out; i += kConsumers) outv[i] = make_double2(0.0, 0.0);
         consumer_sync();
 
@@ -636,6 +646,13 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                 g_out = out_off;
                 g_cols = cols;
             }
+            if (XWIN && xwin && !(c.w & kCXStage) && (mode == kModeN || mode == kModeNW) &&
+                (in_off < xw_lo || in_off + cols > xw_lo + n_in)) {
+                consumer_sync();  // every warp is done with the previous window
+                gather(in_off, min(n_in_all, in_off + n_in));
+                xw_lo = in_off;
+                consumer_sync();
+            }
             const double2* tile = nullptr;
             if (!direct) {
                 if (c.w & kCBegin) {
@@ -660,7 +677,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             if (p.dbg & 1) {
                 // diagnostics: no compute
             } else if (mode == kModeN) {
-                const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
+                const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + (in_off - xw_lo);
                 const int r0 = wrapc<kRowGroups>(rg - out_off);  // first row of this row group
                 for (int r = r0; r < rows; r += kRowGroups) {
                     const double2* T = tile + r * cols + g;
@@ -718,7 +735,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             } else if (mode == kModeNW) {
                 // wide rows (few per piece): warp per row, 32 lanes x 16 B, reduced across the
                 // warp; row o belongs to warp o mod 4 in every piece (deterministic outv adds)
-                const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + in_off;
+                const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + (in_off - xw_lo);
                 const int w = tid >> 5;
                 for (int r = wrapc<kConsumerWarps>(w - out_off); r < rows; r += kConsumerWarps) {
                     const double2* T = tile + r * cols + lane;
@@ -887,7 +904,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
     }
 }
 
-template <bool PROF, bool PEER, bool IO = false, bool SYM = false>
+template <bool PROF, bool PEER, bool IO = false, bool SYM = false, bool XWIN = false>
 __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
     extern __shared__ __align__(128) unsigned char smem[];
     const Layout L = layout(p.nstage, p.stage_bytes, p.xin_max, p.out_max);
@@ -918,7 +935,7 @@ __device__ __forceinline__ void run_cta(const Params& p, int cta, int n_ctas) {
     if (warp == kConsumerWarps) {
         producer<PROF, IO>(p, stages, full, empty, opfull, opempty, slots);
     } else {
-        consumer<PROF, PEER, IO, SYM>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
+        consumer<PROF, PEER, IO, SYM, XWIN>(p, stages, xin, outv, full, empty, opfull, opempty, slots, sprof);
     }
     __syncthreads();
     // self-reset: the last CTA out zeroes the counters and the ticket for the next launch
@@ -956,6 +973,12 @@ __global__ void __maxnreg__(UHMV_BULK_REGS) uhmv_bulk_kernel(const Params p) {
 template <bool PROF>
 __global__ void __maxnreg__(UHMV_BULK_REGS) uhmv_bulk_sym_kernel(const Params p) {
     run_cta<PROF, false, false, true>(p, blockIdx.x, gridDim.x);
+}
+
+// Programs with windowed-input ops (packer_h FAR, UHMV_PROG_XWIN): the H format at 3 CTAs/SM.
+template <bool PROF>
+__global__ void __maxnreg__(UHMV_BULK_REGS) uhmv_bulk_xwin_kernel(const Params p) {
+    run_cta<PROF, false, false, false, true>(p, blockIdx.x, gridDim.x);
 }
 
 // Host-I/O programs (uhmv_matvec_host with pinned buffers): x gathered over PCIe by the P1

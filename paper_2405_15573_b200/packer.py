@@ -64,6 +64,7 @@ OP_XWAIT = 64  # NEAR op: its x windows come from device x -> the producer waits
 OP_DRAIN = 128  # NEAR / FAR op: the last op finishing an output leaf copies w[leaf] to the host
 OP_XIN = 256  # op gathers its x runs into xin although its N pieces carry x windows (packer_sym NEAR)
 OP_DUAL = 512  # packer_sym Z / NEAR: N pieces + alias T / H pieces with disjoint outputs (no barrier between)
+OP_XWIN = 1024  # op gathers its input window by window (field 15 = window length, field 0 = total)
 BUF_HOSTW = 4  # drain descriptor run (after the op's out runs): lo, len, counter, expected count
 
 OP_FIELDS = 16  # int32 per op
@@ -138,6 +139,7 @@ class Program:
     #                     the peers' work buffers and counters signalled across ranks (RUN_PEER)
     host_io: bool = False  # host-I/O program (OP_XHOST / OP_XWAIT / OP_DRAIN ops)
     bulk_only: bool = False  # T-mode / alias pieces (packer_sym): only the bulk engine runs it
+    xwin: bool = False  # windowed-input ops (packer_h FAR, OP_XWIN): the bulk engine's xwin kernel
 
     @property
     def n_ops(self) -> int:

@@ -15,6 +15,8 @@ what the uniform format trades for smaller shared bases.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from .packer import (
@@ -28,8 +30,11 @@ from .packer import (
     KIND_RED,
     MODE_H,
     MODE_N,
+    MODE_NW,
     MODE_S,
+    OP_XWIN,
     P1_CHUNK,
+    PI_XSTAGE,
     ROWS_PER_CHUNK,
     RUN_ATOMIC,
     STAGE_ELEMS,
@@ -119,6 +124,9 @@ def pack_h(h, *, rows_per_chunk: int | None = None, stage_elems: int | None = No
                wstack=wstack, ustack=ustack)
     kw = dict(rows_per_chunk=rows_per_chunk, stage_elems=stage_elems, near_interleave=near_interleave,
               far_rows=int(os.environ.get("UHMV_FAR_ROWS_H", 64)))
+    # windowed FAR inputs pay off on large operators (config 3: 0.818 -> 0.893 of HBM; config 2,
+    # 1 GB, is latency-bound and 4 % slower with them)
+    kw["xwin"] = XWIN if 16 * (elems + dense_elems) >= 2e9 else 0
     fwd, work_f = _build_h(geo, adjoint=False, **kw)
     adj, work_a = _build_h(geo, adjoint=True, **kw)
     _assign_tmaps([fwd, adj])
@@ -151,7 +159,7 @@ def _block_stacks(leaves, span, adm, kb, clus, level):
     return out
 
 
-def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave, far_rows=64):
+def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave, far_rows=64, xwin=0):
     bct, adm, kb, offs = geo["bct"], geo["adm"], geo["kb"], geo["offs"]
     if adjoint:
         in_tree, out_tree = bct.row_tree, bct.col_tree
@@ -346,4 +354,38 @@ def _build_h(geo, *, adjoint, rows_per_chunk, stage_elems, near_interleave, far_
     phased = [ops[KIND_P1] + near, ops[KIND_RED], ops[KIND_FAR]]
     fused = ops[KIND_P1] + parts[0] + ops[KIND_RED] + parts[1] + parts[2] + parts[3] + ops[KIND_FAR]
     # 256-column H panels (more rows per stage) measured best for the wide per-block stacks
-    return _finish(phased, fused, n_ctr, stage_elems=stage_elems, h_panel=H_PANEL), work
+    prog = _finish(phased, fused, n_ctr, stage_elems=stage_elems, h_panel=H_PANEL)
+    return _window_inputs(prog, xwin), work
+
+
+XWIN = int(os.environ.get("UHMV_XWIN_H", 704))  # FAR input window (complex) -- 0: gather whole inputs
+
+
+def _window_inputs(prog, xw):
+    """FAR ops gather the y of every block of every ancestor (~1750 complex at config 3), which
+    at 16 B each would cut the bulk engine to 2 CTAs/SM.  Ops whose input exceeds ``xw`` and
+    whose pieces all read it as N / NW rows (in nondecreasing order) are flagged OP_XWIN: the
+    kernel gathers ``xw`` elements at a time, re-gathering when a piece runs past the window
+    (csrc/uhmv_bulk.cuh, uhmv_bulk_xwin_kernel).  Field 15 becomes the window length."""
+    if xw <= 0:
+        return prog
+    ops = prog.ops
+    any_w = False
+    for i in range(prog.n_ops):
+        n_in, xin_len = int(ops[i, 0]), int(ops[i, 15])
+        if xin_len <= xw:
+            continue
+        pcs = prog.pieces[ops[i, 13] : ops[i, 14]]
+        modes = set(int(m) for m in pcs[:, 4])
+        spans = pcs[:, 3]
+        if not modes <= {MODE_N, MODE_NW} or (pcs[:, 7] & PI_XSTAGE).any() or int(spans.max()) > xw:
+            continue
+        if (np.diff(pcs[:, 5]) < 0).any():  # windows move forward only
+            continue
+        ops[i, 15] = xw
+        ops[i, 12] |= OP_XWIN
+        any_w = True
+    if any_w:
+        prog.xin_max = int(ops[:, 15].max())
+        prog.xwin = True
+    return prog

@@ -60,3 +60,30 @@ def test_checker_catches_corruption():
     p.fwd.pieces[i, 0] = len(p.arena)  # a bulk copy past the arena
     with pytest.raises(ProgramError):
         check_packed(p)
+
+
+def test_h_programs_in_bounds():
+    """H-format programs, including the windowed-input FAR ops (OP_XWIN) of config 2."""
+    import glob
+    import os
+
+    from conftest import GOLDEN
+    from program_check import check_packed
+
+    from paper_2405_15573_b200 import workloads
+    from paper_2405_15573_b200.packer import OP_XWIN
+    from paper_2405_15573_b200.packer_h import pack_h
+    from paper_2405_15573_b200.uh_io import load_h
+
+    for path in sorted(glob.glob(os.path.join(GOLDEN, "h_*.npz"))):
+        check_packed(pack_h(load_h(path)[0]))
+    import dataclasses
+
+    from paper_2405_15573_b200.packer_h import _window_inputs
+
+    p = pack_h(workloads.build_h_operator(2))  # 1 GB: packed without windows; window it here
+    w = dataclasses.replace(p, fwd=_window_inputs(dataclasses.replace(p.fwd, ops=p.fwd.ops.copy()), 704),
+                            adj=_window_inputs(dataclasses.replace(p.adj, ops=p.adj.ops.copy()), 704))
+    assert w.fwd.xwin and w.adj.xwin and w.fwd.xin_max <= 704
+    assert ((w.fwd.ops[:, 12] & OP_XWIN) != 0).sum() > 0
+    check_packed(w)
