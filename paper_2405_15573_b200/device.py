@@ -23,6 +23,19 @@ _MODES = {"phased": _lib.MODE_PHASED, "fused": _lib.MODE_FUSED, "bulk": _lib.MOD
 MODES = tuple(_MODES)
 
 
+def _torch_dtypes():
+    import torch
+
+    return {np.dtype(np.complex128): torch.complex128, np.dtype(np.complex64): torch.complex64,
+            np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}
+
+
+try:
+    _TORCH_DTYPES = _torch_dtypes()
+except ImportError:  # pragma: no cover
+    _TORCH_DTYPES = {}
+
+
 def default_mode() -> str:
     return os.environ.get("UHMV_MODE", "bulk")
 
@@ -546,8 +559,20 @@ class DeviceOperator:
                 self._staging = st
             xs, ws = st[adjoint]
             xs_np, ws_np = xs.numpy()[:n_in], ws.numpy()[:n_out]
-            np.copyto(xs_np, v, casting="unsafe" if np.iscomplexobj(v) else "same_kind")
+            torch = self.torch
+            # host copies in and out: torch's multi-threaded copy for the common dtypes (config 3:
+            # ~40 us per 1.3 MB instead of ~100-130 us for NumPy's single-threaded one)
+            tin = _TORCH_DTYPES.get(np.dtype(v.dtype))
+            if tin is not None and v.flags.c_contiguous and v.flags.writeable:
+                xs[:n_in].copy_(torch.from_numpy(v))
+            else:
+                np.copyto(xs_np, v, casting="unsafe" if np.iscomplexobj(v) else "same_kind")
             self._matvec_host_locked(xs_np, adjoint, ws_np, default_mode(), None, None)
+            tout = _TORCH_DTYPES.get(np.dtype(dtype))
+            if tout is not None:
+                res = torch.empty(n_out, dtype=tout)
+                res.copy_(ws[:n_out] if np.issubdtype(dtype, np.complexfloating) else ws[:n_out].real)
+                return res.numpy()  # a NEW array (it owns the tensor's storage)
             if np.issubdtype(dtype, np.complexfloating):
                 return ws_np.astype(dtype, copy=True)
             return ws_np.real.astype(dtype, copy=True)
