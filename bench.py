@@ -768,8 +768,12 @@ def run_multi_rhs(args, world, rank, local_rank, config):
         "config": config,
         "roofline": {"bound": "tensor", "achieved": flops / t / 1e12, "peak": peak, "unit": "TFLOP/s",
                      "frac": flops / t / 1e12 / peak,
-                     "peak_source": "uhmv_dmma_peak: measured DMMA m16n8k16 f64 throughput on this GPU",
-                     "traffic": None, "flops_per_launch": flops, "kernel": "mrtc::uhmv_mrtc_kernel"},
+                     "peak_source": "uhmv_dmma_peak: measured DMMA m16n8k16 f64 throughput on this GPU "
+                                    "(MEASURED_PEAKS.json has no FP64 entry)",
+                     "traffic": load_traffic("cfg5") if R == 64 else None,
+                     "tensor_pipe_active_pct": load_traffic("cfg5_dmma_pipe_active_pct") if R == 64 else None,
+                     "tensor_pipe_source": "ncu smsp__pipe_tensor_subpipe_dmma_cycles_active (profiles/r02/ncu_full_mrtc_cfg5.json)",
+                     "flops_per_launch": flops, "kernel": "mrtc::uhmv_mrtc_kernel"},
         "e2e": {"value": world * R / te, "unit": "matvec/s", "h2d_bytes_per_step": int(16 * n * R),
                 "d2h_bytes_per_step": int(16 * n * R),
                 "api": "uhmv_matmat_host (C ABI, pinned host X/W, 32-column chunks: H2D, DMMA product and "

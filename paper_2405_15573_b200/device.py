@@ -30,6 +30,7 @@ def _torch_dtypes():
             np.dtype(np.float64): torch.float64, np.dtype(np.float32): torch.float32}
 
 
+_TORCH_COPY_MIN = 65536  # complex elements (1 MB)
 try:
     _TORCH_DTYPES = _torch_dtypes()
 except ImportError:  # pragma: no cover
@@ -560,15 +561,17 @@ class DeviceOperator:
             xs, ws = st[adjoint]
             xs_np, ws_np = xs.numpy()[:n_in], ws.numpy()[:n_out]
             torch = self.torch
-            # host copies in and out: torch's multi-threaded copy for the common dtypes (config 3:
-            # ~40 us per 1.3 MB instead of ~100-130 us for NumPy's single-threaded one)
-            tin = _TORCH_DTYPES.get(np.dtype(v.dtype))
+            # host copies in and out: torch's multi-threaded copy for the common dtypes on vectors
+            # of >= 1 MB (config 3: drop-in 1574 -> 1624 matvec/s); below that its thread-pool
+            # start-up costs more than it saves (config 1: 11439 -> 9866), so NumPy copies
+            big = n_in >= _TORCH_COPY_MIN and n_out >= _TORCH_COPY_MIN
+            tin = _TORCH_DTYPES.get(np.dtype(v.dtype)) if big else None
             if tin is not None and v.flags.c_contiguous and v.flags.writeable:
                 xs[:n_in].copy_(torch.from_numpy(v))
             else:
                 np.copyto(xs_np, v, casting="unsafe" if np.iscomplexobj(v) else "same_kind")
             self._matvec_host_locked(xs_np, adjoint, ws_np, default_mode(), None, None)
-            tout = _TORCH_DTYPES.get(np.dtype(dtype))
+            tout = _TORCH_DTYPES.get(np.dtype(dtype)) if big else None
             if tout is not None:
                 res = torch.empty(n_out, dtype=tout)
                 res.copy_(ws[:n_out] if np.issubdtype(dtype, np.complexfloating) else ws[:n_out].real)
