@@ -36,6 +36,14 @@ namespace bulk {
 #ifndef UHMV_BULK_REGS
 #define UHMV_BULK_REGS 128
 #endif
+#ifndef UHMV_NACC1
+#define UHMV_NACC1 1
+#endif
+#ifdef UHMV_DIAGNOSTICS
+constexpr bool kDiag = true;
+#else
+constexpr bool kDiag = false;  // release builds: the skip-waits / skip-compute switches are compiled out
+#endif
 constexpr int kConsumerWarps = UHMV_CWARPS;
 constexpr int kConsumers = kConsumerWarps * 32;  // 128
 constexpr int kThreads = kConsumers + 32;        // + one producer warp
@@ -200,6 +208,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity), "r"(0x989680)
         : "memory");
 }
+// Non-blocking phase test (warp-uniform use: every lane reads the same barrier word).
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
     asm volatile(
@@ -294,6 +314,41 @@ __device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64
 // are reduced by shuffles at the flush.  (P = 4 up to 128 columns measured slower.)
 __device__ __forceinline__ int h_lanes(int cols) { return cols <= 32 ? 4 : (cols <= 64 ? 2 : 1); }
 
+// Producer-side prefetch of an op's first 32 run / piece records (one per lane), issued while
+// the previous op's pieces stream so that an op boundary costs no global round trip.
+struct OpPrefetch {
+    int64_t roff;          // lane's run record (lane < min(n_runs, 32))
+    int rlen, rdst, rbf;
+    int64_t f0, f1, f5, f7;  // lane's piece record (lane < min(n_pc, 32)): m_off, ld, in_off, info
+    int rc, md;              // rows << 16 | cols, mode
+    int4 pc;                 // the same piece, compressed for the consumers
+};
+
+__device__ __forceinline__ void prefetch_records(const Params& p, int lane, int in_b, int n_runs, int pc_b,
+                                                 int n_pc, OpPrefetch& R) {
+    R.f7 = kPiDirect;
+    R.f0 = R.f1 = R.f5 = 0;
+    R.rc = R.md = 0;
+    if (lane < n_runs) {
+        const int64_t* rd = p.runs + (int64_t)(in_b + lane) * kRunFields;
+        R.roff = __ldg(rd + 1);
+        R.rlen = (int)__ldg(rd + 2);
+        R.rdst = (int)__ldg(rd + 3);
+        R.rbf = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
+    }
+    if (lane < n_pc) {
+        const int64_t* d = p.pieces + (int64_t)(pc_b + lane) * kPieceFields;
+        R.f0 = __ldg(d + 0);
+        R.f1 = __ldg(d + 1);
+        const int64_t rows = __ldg(d + 2), cols = __ldg(d + 3), mode = __ldg(d + 4), out_off = __ldg(d + 6);
+        R.f5 = __ldg(d + 5);
+        R.f7 = __ldg(d + 7);
+        R.rc = (int)((rows << 16) | cols);
+        R.md = (int)mode;
+        R.pc = compress_piece(rows, cols, mode, R.f5, out_off, R.f7);
+    }
+}
+
 template <bool PROF, bool IO>
 __device__ __forceinline__ void producer(const Params& p, unsigned char* stages, uint64_t* full,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
@@ -308,18 +363,26 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
     uint32_t qphase = 0;
     unsigned long long c_empty = 0, c_slot = 0;
     const bool prof = PROF && lane == 0;
-    unsigned long long t_next = 0;
-    if (lane == 0) t_next = atomicAdd(p.ticket, 1ull);
-    t_next = __shfl_sync(0xffffffffu, t_next, 0);
+    auto claim = [&]() {
+        unsigned long long t = 0;
+        if (lane == 0) t = atomicAdd(p.ticket, 1ull);
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
+    auto order_of = [&](unsigned long long t) {
+        return (t < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t) : -1;
+    };
+    auto header_of = [&](int op) { return (op >= 0 && lane < 16) ? __ldg(p.ops + (int64_t)op * 16 + lane) : 0; };
+    // software pipeline over ops: while op k streams, the ticket -> order -> header -> records
+    // chain of op k+1 is issued one link per stage boundary (three dependent round trips hidden
+    // behind the copies); ops with fewer than three stages finish the chain after their loop
+    int op = order_of(claim());
+    int hv = header_of(op);
+    OpPrefetch R;
+    prefetch_records(p, lane, __shfl_sync(0xffffffffu, hv, 2),
+                     op >= 0 ? __shfl_sync(0xffffffffu, hv, 7) - __shfl_sync(0xffffffffu, hv, 2) : 0,
+                     __shfl_sync(0xffffffffu, hv, 13),
+                     op >= 0 ? __shfl_sync(0xffffffffu, hv, 14) - __shfl_sync(0xffffffffu, hv, 13) : 0, R);
     for (;;) {
-        const int op = (t_next < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t_next) : -1;
-        int hv = 0;
-        if (op >= 0) {
-            if (lane < 16) hv = __ldg(p.ops + (int64_t)op * 16 + lane);
-            unsigned long long t = 0;
-            if (lane == 0) t = atomicAdd(p.ticket, 1ull);  // next op, overlapped with this one
-            t_next = __shfl_sync(0xffffffffu, t, 0);
-        }
         const int in_b = __shfl_sync(0xffffffffu, hv, 2);
         const int out_e = __shfl_sync(0xffffffffu, hv, 7);
         const int pc_b = __shfl_sync(0xffffffffu, hv, 13);
@@ -332,7 +395,13 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
         if (lane < 16) S->hdr[lane] = hv;
         if (lane == 0) S->op = op;
         const int n_runs = op >= 0 ? out_e - in_b : 0;
-        for (int r = lane; r < n_runs && r < kSlotRuns; r += 32) {
+        if (lane < n_runs) {
+            S->roff[lane] = R.roff;
+            S->rlen[lane] = R.rlen;
+            S->rdst[lane] = R.rdst;
+            S->rbf[lane] = R.rbf;
+        }
+        for (int r = lane + 32; r < n_runs && r < kSlotRuns; r += 32) {
             const int64_t* rd = p.runs + (int64_t)(in_b + r) * kRunFields;
             S->roff[r] = __ldg(rd + 1);
             S->rlen[r] = (int)__ldg(rd + 2);
@@ -340,7 +409,8 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
             S->rbf[r] = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
         }
         const int n_pc = op >= 0 ? pc_e - pc_b : 0;
-        for (int i = lane; i < n_pc && i < kSlotPieces; i += 32) {
+        if (lane < n_pc) S->pc[lane] = R.pc;
+        for (int i = lane + 32; i < n_pc && i < kSlotPieces; i += 32) {
             const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
             S->pc[i] = compress_piece(__ldg(d + 2), __ldg(d + 3), __ldg(d + 4), __ldg(d + 5),
                                       __ldg(d + 6), __ldg(d + 7));
@@ -370,18 +440,42 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
             }
             break;
         }
+        // next op: claim its ticket now (one op ahead, as the dependency order assumes), then
+        // one link of ticket -> order -> header -> records per finished stage
+        const unsigned long long t_next = claim();
+        int op_n = -1;
+        int hv_n = 0;
+        OpPrefetch Rn;
+        int link = 0, begun = 0;
+        auto advance = [&]() {  // (warp-uniform call sites)
+            if (link == 0) {
+                op_n = order_of(t_next);
+            } else if (link == 1) {
+                hv_n = header_of(op_n);
+            } else if (link == 2) {
+                const int nb = __shfl_sync(0xffffffffu, hv_n, 2), ne = __shfl_sync(0xffffffffu, hv_n, 7);
+                const int pb = __shfl_sync(0xffffffffu, hv_n, 13), pe = __shfl_sync(0xffffffffu, hv_n, 14);
+                prefetch_records(p, lane, nb, op_n >= 0 ? ne - nb : 0, pb, op_n >= 0 ? pe - pb : 0, Rn);
+            }
+            ++link;
+        };
         for (int base = pc_b; base < pc_e; base += 32) {
             const int nb = min(32, pc_e - base);
-            int64_t f0 = 0, f1 = 0, f7 = kPiDirect, f5 = 0;
-            int rc = 0, md = 0;
-            if (lane < nb) {
-                const int64_t* d = p.pieces + (int64_t)(base + lane) * kPieceFields;
-                f0 = __ldg(d + 0);
-                f1 = __ldg(d + 1);
-                rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));
-                md = (int)__ldg(d + 4);
-                f5 = __ldg(d + 5);
-                f7 = __ldg(d + 7);
+            int64_t f0 = R.f0, f1 = R.f1, f7 = R.f7, f5 = R.f5;
+            int rc = R.rc, md = R.md;
+            if (base != pc_b) {
+                f0 = f1 = f5 = 0;
+                f7 = kPiDirect;
+                rc = md = 0;
+                if (lane < nb) {
+                    const int64_t* d = p.pieces + (int64_t)(base + lane) * kPieceFields;
+                    f0 = __ldg(d + 0);
+                    f1 = __ldg(d + 1);
+                    rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));
+                    md = (int)__ldg(d + 4);
+                    f5 = __ldg(d + 5);
+                    f7 = __ldg(d + 7);
+                }
             }
             for (int k = 0; k < nb; ++k) {
                 const int64_t info = __shfl_sync(0xffffffffu, f7, k);
@@ -393,6 +487,10 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 const int pmode = __shfl_sync(0xffffffffu, md, k);
                 const int64_t xo = __shfl_sync(0xffffffffu, f5, k);
                 if (info & kPiBegin) {
+                    // a link of the next op's chain whenever the ring is full (the warp would
+                    // block anyway), and at every stage from the op's third on
+                    if (link < 3 && (begun >= 2 || !mbar_test(&empty[stage], sphase ^ 1u))) advance();
+                    ++begun;
                     const long long te = prof ? clock64() : 0;
                     mbar_wait(&empty[stage], sphase ^ 1u);
                     if (prof) c_empty += clock64() - te;
@@ -424,6 +522,10 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 }
             }
         }
+        while (link < 3) advance();  // short ops: the rest of the chain, exposed
+        op = op_n;
+        hv = hv_n;
+        R = Rn;
     }
 }
 
@@ -511,7 +613,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         const bool dual = SYM && (S->hdr[12] & kOpDual) != 0;
         const int n_in_runs = in_e - in_b;
         const int n_runs = out_e - in_b;
-        if (!p.skip_waits) {  // every consumer thread polls one dependency counter in parallel
+        if (!(kDiag && p.skip_waits)) {  // every consumer thread polls one dependency counter in parallel
             const int wb = S->hdr[8], we = S->hdr[9];
             for (int i = wb + tid; i < we; i += kConsumers) {
                 const int c = __ldg(p.waits + 2 * i);
@@ -532,7 +634,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             if (p.trace) p.trace[(size_t)op * 4 + 1] = globaltimer_ns();
         }
         // gather the input vector: all loads of a batch issued before any smem store
-        const int n_in = (p.dbg & 2) ? 0 : S->hdr[15];  // work inputs only (x rides in stages)
+        const int n_in = (kDiag && (p.dbg & 2)) ? 0 : S->hdr[15];  // work inputs only (x rides in stages)
         const bool xwin = XWIN && (S->hdr[12] & kOpXWin) != 0;
         const int n_in_all = xwin ? S->hdr[0] : n_in;  // windowed: hdr[15] is the window length
         int xw_lo = 0;
@@ -566,10 +668,29 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
 
         double accr[kSlots], acci[kSlots];
         const bool nreg = n_out <= kSlots * kRowGroups && !dual;
+        // single-slot N ops (every NEAR op; n_out <= 16): row group rg owns output row rg in every
+        // piece, so the four accumulation chains of its row live in accr / acci[0..3] across the
+        // whole N group -- no per-row zeroing, fold or slot select (the narrow 40-column dense rows
+        // of configs 1-2 spent most of their instructions there)
+        const bool nacc1 = UHMV_NACC1 && n_out <= kRowGroups && !dual;
         int g_mode = -1, g_out = 0, g_cols = 0;
         auto flush = [&]() {
             if (g_mode == kModeN) {
-                if (nreg) {
+                if (nacc1) {
+                    double ar = (accr[0] + accr[1]) + (accr[2] + accr[3]);
+                    double ai = (acci[0] + acci[1]) + (acci[2] + acci[3]);
+#pragma unroll
+                    for (int o = 1; o < kLanesPerRow; o <<= 1) {
+                        ar += __shfl_xor_sync(0xffffffffu, ar, o);
+                        ai += __shfl_xor_sync(0xffffffffu, ai, o);
+                    }
+                    if (g == 0 && rg < n_out) {
+                        double2 v = outv[rg];
+                        v.x += ar;
+                        v.y += ai;
+                        outv[rg] = v;
+                    }
+                } else if (nreg) {
 #pragma unroll
                     for (int k = 0; k < kSlots; ++k) {
                         if (k * kRowGroups >= n_out) break;
@@ -674,8 +795,37 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
                        (c.w & 0xFFFF);
             }
             if (prof) pr[kind * 8 + 4] += 1;
-            if (p.dbg & 1) {
+            if (kDiag && (p.dbg & 1)) {
                 // diagnostics: no compute
+            } else if (mode == kModeN && nacc1) {
+                const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + (in_off - xw_lo);
+                const int r = wrapc<kRowGroups>(rg - out_off);  // this row group's row, if < rows
+                if (r < rows) {
+                    const double2* T = tile + r * cols + g;
+                    const double2* X = xv + g;
+#pragma unroll 2
+                    for (int k = cols >> 5; k > 0; --k) {
+                        const double2 t0 = T[0], x0 = X[0], t1 = T[8], x1 = X[8];
+                        const double2 t2 = T[16], x2 = X[16], t3 = T[24], x3 = X[24];
+                        cmac(accr[0], acci[0], t0, x0);
+                        cmac(accr[1], acci[1], t1, x1);
+                        cmac(accr[2], acci[2], t2, x2);
+                        cmac(accr[3], acci[3], t3, x3);
+                        T += 32;
+                        X += 32;
+                    }
+                    const int tail = cols & 31;  // warp-uniform: branch over the unused lane groups
+                    if (tail) {
+                        if (g < tail) cmac(accr[0], acci[0], T[0], X[0]);
+                        if (tail > 8) {
+                            if (g + 8 < tail) cmac(accr[1], acci[1], T[8], X[8]);
+                            if (tail > 16) {
+                                if (g + 16 < tail) cmac(accr[2], acci[2], T[16], X[16]);
+                                if (tail > 24 && g + 24 < tail) cmac(accr[3], acci[3], T[24], X[24]);
+                            }
+                        }
+                    }
+                }
             } else if (mode == kModeN) {
                 const double2* xv = (c.w & kCXStage) ? tile + rows * cols : xin + (in_off - xw_lo);
                 const int r0 = wrapc<kRowGroups>(rg - out_off);  // first row of this row group
@@ -838,7 +988,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
             t0 = t1;
         }
         // scatter the output vector
-        for (int pos = tid; pos < ((p.dbg & 2) ? 0 : n_out); pos += kConsumers) {
+        for (int pos = tid; pos < ((kDiag && (p.dbg & 2)) ? 0 : n_out); pos += kConsumers) {
             const RunRef R = get_run(p, S, in_b, find_run(p, S, in_b, n_in_runs, n_runs, pos));
             const int buf = R.bf & 0xFF, flags = R.bf >> 8;
             double2* dp = (buf == kBufW ? p.w : p.work) + R.off + (pos - R.dst);
@@ -859,7 +1009,7 @@ __device__ __forceinline__ void consumer(const Params& p, unsigned char* stages,
         const int sb = S->hdr[10], se = S->hdr[11];
         consumer_sync();  // all outputs issued; the slot is no longer read
         if (lane == 0) mbar_arrive(&opempty[q]);
-        if (tid == 0 && !p.skip_waits && se > sb) {
+        if (tid == 0 && !(kDiag && p.skip_waits) && se > sb) {
             if (peer_op) {  // (the slot may already hold another op: flag read at op start)
                 // the CTA's local and peer stores precede the system-scope fence through the
                 // bar.sync above; then one relaxed add per counter and rank

@@ -50,7 +50,7 @@ __all__ = ["PackedOperator", "Program", "pack", "MODE_N", "MODE_H", "MODE_S"]
 MODE_N, MODE_H, MODE_S = 0, 1, 2
 MODE_NW = 3  # bulk-kernel piece mode: an N piece of a wide-row op (one warp per row)
 MODE_T = 4  # out[j] += sum_r M[r,j] in[r]: H without the conjugation (symmetric variant, packer_sym)
-WIDE_COLS = 288  # an op whose N segments all have rows this long (<= 4 rows per stage) runs them warp-per-row
+WIDE_COLS = int(os.environ.get("UHMV_WIDE_COLS", 288))  # an op whose N segments all have rows this long (<= 4 rows per stage) runs them warp-per-row
 BUF_ARENA, BUF_WORK, BUF_X, BUF_W = 0, 1, 2, 3
 RUN_ADD = 1  # out run: read-modify-write add (single writer)
 RUN_ATOMIC = 2  # out run: fp64 red.add -- w is zeroed first; <= 2 addends per entry
@@ -100,8 +100,10 @@ P1_CHUNK = 256  # max input rows per P1 op
 # 1.36x / 1.59x slower at config 3 -- strided per-row copies make the producer the bottleneck)
 ADJ_NEAR_COLS = int(os.environ.get("UHMV_ADJ_NEAR_COLS", 1 << 30))
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
-BULK_NCOLS_MAX = 640  # widest N piece row (two rows + x window still fit a stage)
+BULK_NCOLS_MAX = int(os.environ.get("UHMV_NCOLS_MAX", 640))  # widest N piece row (two rows + x window still fit a stage)
 NW_COLS = int(os.environ.get("UHMV_NW_COLS", 640))  # widest panel of a warp-per-row op (sweeps: 352/176 slower)
+PANEL_ROWS = int(os.environ.get("UHMV_PANEL_ROWS", 0))  # N segments: column panels narrow enough for this many rows per stage (0: off)
+NOSPLIT = float(os.environ.get("UHMV_NOSPLIT", 0.3))  # see _pieces: largest stage fraction left empty instead of cutting an N segment
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 # work splitting of the farfield chain ops across CTAs (output entries per op)
 SPLIT_DEFAULTS = {"p1_out": 1 << 30, "u_cols": 1 << 30, "z_rows": 1 << 30, "far_rows": ROWS_PER_CHUNK}
@@ -1110,7 +1112,25 @@ def _order_segments(segs):
     return n + h
 
 
-def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_panel=BULK_HCOLS_MAX):
+def _ncols_panel(rows, cols, xs, stage_elems, ncols_max, panel_rows):
+    """Widest column panel of an N segment: ``ncols_max`` (and half a stage), or -- with
+    ``panel_rows`` -- narrow enough that a stage holds min(rows, panel_rows) rows, so every row
+    group of the consumers has a row in every piece (equal panels, multiples of 8 columns)."""
+    lim = min(ncols_max, stage_elems // 2)
+    if panel_rows > 0:
+        tgt = min(rows, panel_rows)
+        pw = stage_elems // (tgt + (1 if xs else 0))
+        if pw < cols:
+            n = -(-cols // max(32, pw))  # panels needed
+            pw = -(-cols // n)
+            pw = (pw + 7) // 8 * 8
+            while pw * tgt + (pw if xs else 0) > stage_elems and pw > 32:
+                pw -= 8
+        lim = min(lim, max(32, pw))
+    return lim
+
+
+def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_panel=BULK_HCOLS_MAX, panel_rows=0):
     """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages.
 
     Pieces whose input is a window of x (P1 and NEAR ops) carry that window inside the stage,
@@ -1135,8 +1155,9 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_pa
         if mode != MODE_N and cols > min(h_panel, stage_elems // 2):
             for c0, c1 in _chunks(0, cols, min(h_panel, stage_elems // 2)):
                 split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off, ()))
-        elif mode == MODE_N and cols > min(ncols_max, stage_elems // 2):  # rows wider than a stage
-            for c0, c1 in _chunks(0, cols, min(ncols_max, stage_elems // 2)):  # -> column panels
+        elif mode == MODE_N and cols > _ncols_panel(rows, cols, x_off >= 0 and has_x, stage_elems, ncols_max, panel_rows):
+            # rows wider than a stage (or than a stage of panel_rows rows) -> column panels
+            for c0, c1 in _chunks(0, cols, _ncols_panel(rows, cols, x_off >= 0 and has_x, stage_elems, ncols_max, panel_rows)):
                 sub = []  # the alias sub-blocks (column ranges) that fall into this panel
                 for a0, ac, amode, a_in, a_out in alias:
                     lo, hi = max(a0, c0), min(a0 + ac, c1)
@@ -1158,6 +1179,12 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_pa
         if per_row + extra > stage_elems:
             raise ValueError(f"segment row of {cols} elements exceeds a {stage_elems}-element stage")
         r = 0
+        # a narrow N segment that fits a whole stage is not cut at a stage boundary when the room
+        # left is small: the cut costs two half-empty passes of the 16 row groups
+        if (mode == MODE_N and NOSPLIT > 0 and fill > 0 and rows * per_row + extra <= stage_elems
+                and fill + rows * per_row + extra > stage_elems
+                and stage_elems - fill <= NOSPLIT * stage_elems):
+            close()
         while r < rows:
             room = (stage_elems - fill - extra) // per_row
             if room <= 0:
@@ -1309,7 +1336,8 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         nsg = [q for q in ordered if q[5] == MODE_N]
         wide = bool(nsg) and all(q[3] >= WIDE_COLS for q in nsg)
         # warp-per-row ops: panels narrow enough that a stage holds a row for every warp
-        pcs = _pieces(ordered, has_x, stage_elems, NW_COLS if wide else BULK_NCOLS_MAX, h_panel)
+        pcs = _pieces(ordered, has_x, stage_elems, NW_COLS if wide else BULK_NCOLS_MAX, h_panel,
+                      0 if wide else PANEL_ROWS)
         if wide:  # long rows: few per piece
             for pc in pcs:
                 if pc[4] == MODE_N:
