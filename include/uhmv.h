@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define UHMV_ABI_VERSION 12
+#define UHMV_ABI_VERSION 13
 #define UHMV_MAX_PHASES 8
 
 /* Execution modes of uhmv_execute. */
@@ -84,6 +84,10 @@ typedef struct uhmv_program {
 } uhmv_program;
 
 #define UHMV_PROG_SYM 1
+#define UHMV_PROG_WORDER 4 /* ordered output (packer w_order): the NEAR ops of an output leaf STORE
+                              their rows of w, its FAR ops wait for them and add (plain read-modify-
+                              write): uhmv_execute runs no memset and no atomics.  The multi-RHS
+                              engines always add atomically into a W they zero first.             */
 #define UHMV_PROG_XWIN 2 /* windowed-input ops (H-format FAR, packer_h OP_XWIN): the bulk engine runs
                             them with uhmv_bulk_xwin_kernel; no peer / host-I/O programs          */
 

@@ -160,7 +160,7 @@ def run_op_mr(prog, i, bufs, R):
     out_runs = prog.runs[out_b:out_e]
     if flags & MR_ZERO:
         for buf, off, ln, dst, fl in out_runs:
-            if not fl & RUN_ATOMIC:
+            if int(buf) != BUF_W:  # (w runs: atomic adds onto the zeroed W, whatever their single-RHS flags)
                 bufs[int(buf)][off : off + ln] = 0
 
     def flush(o0, blk, first):
@@ -168,7 +168,7 @@ def run_op_mr(prog, i, bufs, R):
             o = o0 + j
             buf, off, ln, dst, fl = next(r for r in out_runs if r[3] <= o < r[3] + r[2])
             tgt = bufs[int(buf)]
-            if (fl & RUN_ATOMIC) or not first:
+            if int(buf) == BUF_W or not first:
                 tgt[off + o - dst] += blk[j]
             else:
                 tgt[off + o - dst] = blk[j]

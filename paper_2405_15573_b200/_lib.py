@@ -14,7 +14,7 @@ __all__ = ["lib", "UhmvProgram", "UhmvDesc", "UhmvPeerRank", "check", "LIB_PATH"
 
 LIB_PATH = os.environ.get("UHMV_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_build", "libuhmv.so")
 MAX_PHASES = 8
-ABI_VERSION = 12
+ABI_VERSION = 13
 MODE_PHASED, MODE_FUSED, MODE_BULK = 0, 1, 2
 
 
@@ -47,6 +47,7 @@ class UhmvProgram(ctypes.Structure):
 
 
 PROG_SYM = 1  # uhmv_program.flags: symmetric single-triangle program (bulk engine only)
+PROG_WORDER = 4  # uhmv_program.flags: ordered output (NEAR stores, FAR waits and adds; no memset, no atomics)
 PROG_XWIN = 2  # uhmv_program.flags: windowed-input ops (H-format FAR; bulk engine only)
 
 

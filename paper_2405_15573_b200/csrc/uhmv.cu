@@ -949,7 +949,7 @@ static int execute_impl(uhmv_plan* plan, const void* x, void* w, int adjoint, in
     if ((pr.flags & UHMV_PROG_SYM) && mode != UHMV_MODE_BULK)
         return fail(UHMV_EINVAL, "uhmv_execute: symmetric single-triangle programs run on the bulk engine only");
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
-    if (n_out > 0 && pr.zero_output) {  // NEAR/FAR add into a zeroed output
+    if (n_out > 0 && pr.zero_output && !(plan->debug_flags & 4)) {  // NEAR/FAR add into a zeroed output
         if (!w) return fail(UHMV_EINVAL, "null output pointer");
         cudaError_t e0 = cudaMemsetAsync(w, 0, (size_t)n_out * 16, static_cast<cudaStream_t>(stream));
         if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(w)");
@@ -1140,7 +1140,7 @@ static int execute_mrhs_impl(uhmv_plan* plan, const void* x, void* w, void* work
     if (!pr.mr_segs || !pr.mr_ranges) return fail(UHMV_EINVAL, "program has no multi-RHS tables");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const int64_t n_out = adjoint ? plan->d.n_cols : plan->d.n_rows;
-    if (n_out > 0 && pr.zero_output) {
+    if (n_out > 0 && (pr.zero_output || (pr.flags & UHMV_PROG_WORDER))) {  // the engines add into W
         cudaError_t e0 = cudaMemsetAsync(w, 0, (size_t)n_out * nrhs * 16, st);
         if (e0 != cudaSuccess) return cuda_fail(e0, "cudaMemsetAsync(W)");
     }

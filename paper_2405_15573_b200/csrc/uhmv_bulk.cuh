@@ -208,18 +208,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity), "r"(0x989680)
         : "memory");
 }
-// Non-blocking phase test (warp-uniform use: every lane reads the same barrier word).
-__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(su32(b)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
     asm volatile(
@@ -314,41 +302,6 @@ __device__ __forceinline__ int4 compress_piece(int64_t rows, int64_t cols, int64
 // are reduced by shuffles at the flush.  (P = 4 up to 128 columns measured slower.)
 __device__ __forceinline__ int h_lanes(int cols) { return cols <= 32 ? 4 : (cols <= 64 ? 2 : 1); }
 
-// Producer-side prefetch of an op's first 32 run / piece records (one per lane), issued while
-// the previous op's pieces stream so that an op boundary costs no global round trip.
-struct OpPrefetch {
-    int64_t roff;          // lane's run record (lane < min(n_runs, 32))
-    int rlen, rdst, rbf;
-    int64_t f0, f1, f5, f7;  // lane's piece record (lane < min(n_pc, 32)): m_off, ld, in_off, info
-    int rc, md;              // rows << 16 | cols, mode
-    int4 pc;                 // the same piece, compressed for the consumers
-};
-
-__device__ __forceinline__ void prefetch_records(const Params& p, int lane, int in_b, int n_runs, int pc_b,
-                                                 int n_pc, OpPrefetch& R) {
-    R.f7 = kPiDirect;
-    R.f0 = R.f1 = R.f5 = 0;
-    R.rc = R.md = 0;
-    if (lane < n_runs) {
-        const int64_t* rd = p.runs + (int64_t)(in_b + lane) * kRunFields;
-        R.roff = __ldg(rd + 1);
-        R.rlen = (int)__ldg(rd + 2);
-        R.rdst = (int)__ldg(rd + 3);
-        R.rbf = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
-    }
-    if (lane < n_pc) {
-        const int64_t* d = p.pieces + (int64_t)(pc_b + lane) * kPieceFields;
-        R.f0 = __ldg(d + 0);
-        R.f1 = __ldg(d + 1);
-        const int64_t rows = __ldg(d + 2), cols = __ldg(d + 3), mode = __ldg(d + 4), out_off = __ldg(d + 6);
-        R.f5 = __ldg(d + 5);
-        R.f7 = __ldg(d + 7);
-        R.rc = (int)((rows << 16) | cols);
-        R.md = (int)mode;
-        R.pc = compress_piece(rows, cols, mode, R.f5, out_off, R.f7);
-    }
-}
-
 template <bool PROF, bool IO>
 __device__ __forceinline__ void producer(const Params& p, unsigned char* stages, uint64_t* full,
                                          uint64_t* empty, uint64_t* opfull, uint64_t* opempty,
@@ -363,26 +316,18 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
     uint32_t qphase = 0;
     unsigned long long c_empty = 0, c_slot = 0;
     const bool prof = PROF && lane == 0;
-    auto claim = [&]() {
-        unsigned long long t = 0;
-        if (lane == 0) t = atomicAdd(p.ticket, 1ull);
-        return __shfl_sync(0xffffffffu, t, 0);
-    };
-    auto order_of = [&](unsigned long long t) {
-        return (t < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t) : -1;
-    };
-    auto header_of = [&](int op) { return (op >= 0 && lane < 16) ? __ldg(p.ops + (int64_t)op * 16 + lane) : 0; };
-    // software pipeline over ops: while op k streams, the ticket -> order -> header -> records
-    // chain of op k+1 is issued one link per stage boundary (three dependent round trips hidden
-    // behind the copies); ops with fewer than three stages finish the chain after their loop
-    int op = order_of(claim());
-    int hv = header_of(op);
-    OpPrefetch R;
-    prefetch_records(p, lane, __shfl_sync(0xffffffffu, hv, 2),
-                     op >= 0 ? __shfl_sync(0xffffffffu, hv, 7) - __shfl_sync(0xffffffffu, hv, 2) : 0,
-                     __shfl_sync(0xffffffffu, hv, 13),
-                     op >= 0 ? __shfl_sync(0xffffffffu, hv, 14) - __shfl_sync(0xffffffffu, hv, 13) : 0, R);
+    unsigned long long t_next = 0;
+    if (lane == 0) t_next = atomicAdd(p.ticket, 1ull);
+    t_next = __shfl_sync(0xffffffffu, t_next, 0);
     for (;;) {
+        const int op = (t_next < (unsigned long long)p.op_count) ? __ldg(p.fused_order + t_next) : -1;
+        int hv = 0;
+        if (op >= 0) {
+            if (lane < 16) hv = __ldg(p.ops + (int64_t)op * 16 + lane);
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(p.ticket, 1ull);  // next op, overlapped with this one
+            t_next = __shfl_sync(0xffffffffu, t, 0);
+        }
         const int in_b = __shfl_sync(0xffffffffu, hv, 2);
         const int out_e = __shfl_sync(0xffffffffu, hv, 7);
         const int pc_b = __shfl_sync(0xffffffffu, hv, 13);
@@ -395,13 +340,7 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
         if (lane < 16) S->hdr[lane] = hv;
         if (lane == 0) S->op = op;
         const int n_runs = op >= 0 ? out_e - in_b : 0;
-        if (lane < n_runs) {
-            S->roff[lane] = R.roff;
-            S->rlen[lane] = R.rlen;
-            S->rdst[lane] = R.rdst;
-            S->rbf[lane] = R.rbf;
-        }
-        for (int r = lane + 32; r < n_runs && r < kSlotRuns; r += 32) {
+        for (int r = lane; r < n_runs && r < kSlotRuns; r += 32) {
             const int64_t* rd = p.runs + (int64_t)(in_b + r) * kRunFields;
             S->roff[r] = __ldg(rd + 1);
             S->rlen[r] = (int)__ldg(rd + 2);
@@ -409,8 +348,7 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
             S->rbf[r] = (int)(__ldg(rd + 0) | (__ldg(rd + 4) << 8));
         }
         const int n_pc = op >= 0 ? pc_e - pc_b : 0;
-        if (lane < n_pc) S->pc[lane] = R.pc;
-        for (int i = lane + 32; i < n_pc && i < kSlotPieces; i += 32) {
+        for (int i = lane; i < n_pc && i < kSlotPieces; i += 32) {
             const int64_t* d = p.pieces + (int64_t)(pc_b + i) * kPieceFields;
             S->pc[i] = compress_piece(__ldg(d + 2), __ldg(d + 3), __ldg(d + 4), __ldg(d + 5),
                                       __ldg(d + 6), __ldg(d + 7));
@@ -440,42 +378,18 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
             }
             break;
         }
-        // next op: claim its ticket now (one op ahead, as the dependency order assumes), then
-        // one link of ticket -> order -> header -> records per finished stage
-        const unsigned long long t_next = claim();
-        int op_n = -1;
-        int hv_n = 0;
-        OpPrefetch Rn;
-        int link = 0, begun = 0;
-        auto advance = [&]() {  // (warp-uniform call sites)
-            if (link == 0) {
-                op_n = order_of(t_next);
-            } else if (link == 1) {
-                hv_n = header_of(op_n);
-            } else if (link == 2) {
-                const int nb = __shfl_sync(0xffffffffu, hv_n, 2), ne = __shfl_sync(0xffffffffu, hv_n, 7);
-                const int pb = __shfl_sync(0xffffffffu, hv_n, 13), pe = __shfl_sync(0xffffffffu, hv_n, 14);
-                prefetch_records(p, lane, nb, op_n >= 0 ? ne - nb : 0, pb, op_n >= 0 ? pe - pb : 0, Rn);
-            }
-            ++link;
-        };
         for (int base = pc_b; base < pc_e; base += 32) {
             const int nb = min(32, pc_e - base);
-            int64_t f0 = R.f0, f1 = R.f1, f7 = R.f7, f5 = R.f5;
-            int rc = R.rc, md = R.md;
-            if (base != pc_b) {
-                f0 = f1 = f5 = 0;
-                f7 = kPiDirect;
-                rc = md = 0;
-                if (lane < nb) {
-                    const int64_t* d = p.pieces + (int64_t)(base + lane) * kPieceFields;
-                    f0 = __ldg(d + 0);
-                    f1 = __ldg(d + 1);
-                    rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));
-                    md = (int)__ldg(d + 4);
-                    f5 = __ldg(d + 5);
-                    f7 = __ldg(d + 7);
-                }
+            int64_t f0 = 0, f1 = 0, f7 = kPiDirect, f5 = 0;
+            int rc = 0, md = 0;
+            if (lane < nb) {
+                const int64_t* d = p.pieces + (int64_t)(base + lane) * kPieceFields;
+                f0 = __ldg(d + 0);
+                f1 = __ldg(d + 1);
+                rc = (int)((__ldg(d + 2) << 16) | __ldg(d + 3));
+                md = (int)__ldg(d + 4);
+                f5 = __ldg(d + 5);
+                f7 = __ldg(d + 7);
             }
             for (int k = 0; k < nb; ++k) {
                 const int64_t info = __shfl_sync(0xffffffffu, f7, k);
@@ -487,10 +401,6 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 const int pmode = __shfl_sync(0xffffffffu, md, k);
                 const int64_t xo = __shfl_sync(0xffffffffu, f5, k);
                 if (info & kPiBegin) {
-                    // a link of the next op's chain whenever the ring is full (the warp would
-                    // block anyway), and at every stage from the op's third on
-                    if (link < 3 && (begun >= 2 || !mbar_test(&empty[stage], sphase ^ 1u))) advance();
-                    ++begun;
                     const long long te = prof ? clock64() : 0;
                     mbar_wait(&empty[stage], sphase ^ 1u);
                     if (prof) c_empty += clock64() - te;
@@ -522,10 +432,6 @@ __device__ __forceinline__ void producer(const Params& p, unsigned char* stages,
                 }
             }
         }
-        while (link < 3) advance();  // short ops: the rest of the chain, exposed
-        op = op_n;
-        hv = hv_n;
-        R = Rn;
     }
 }
 

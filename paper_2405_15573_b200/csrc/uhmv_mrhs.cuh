@@ -89,7 +89,7 @@ __device__ __forceinline__ double2* out_ptr(const Params& p, int out_b, int out_
     }
     const int64_t* rd = p.runs + (int64_t)lo * kRunFields;
     const int buf = (int)__ldg(rd + 0);
-    *atomic = (__ldg(rd + 4) & 2) != 0;
+    *atomic = buf == kBufW;  // every w run: fp64 adds onto the zeroed W (whatever the single-RHS flags say)
     return (buf == kBufW ? p.w : p.work) + (__ldg(rd + 1) + (o - __ldg(rd + 3))) * (int64_t)p.nrhs;
 }
 
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kThreads) uhmv_mrhs_kernel(const Params p) {
         // zero the op's work outputs (groups add into them); w is zeroed by the launcher
         for (int r = out_b; r < out_e; ++r) {
             const int64_t* rd = p.runs + (int64_t)r * kRunFields;
-            if (__ldg(rd + 4) & 2) continue;
+            if ((int)__ldg(rd + 0) == kBufW) continue;
             double2* dp = p.work + __ldg(rd + 1) * (int64_t)R;
             const int64_t n = (int64_t)__ldg(rd + 2) * R;
             for (int64_t i = tid; i < n; i += kThreads) __stcg(dp + i, make_double2(0.0, 0.0));

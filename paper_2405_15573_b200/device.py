@@ -100,7 +100,8 @@ class _DeviceProgram:
         s.n_tmaps = len(self.tmap_lds)
         s.tmap_lds = self.tmap_lds.ctypes.data if len(self.tmap_lds) else None
         s.tmaps = self.tmaps.data_ptr()
-        s.flags = (_lib.PROG_SYM if getattr(p, "bulk_only", False) else 0) | (_lib.PROG_XWIN if getattr(p, "xwin", False) else 0)
+        s.flags = (_lib.PROG_SYM if getattr(p, "bulk_only", False) else 0) | (_lib.PROG_XWIN if getattr(p, "xwin", False) else 0) | (
+            _lib.PROG_WORDER if getattr(p, "w_order", False) else 0)
         return s
 
 

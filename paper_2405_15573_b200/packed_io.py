@@ -25,7 +25,7 @@ __all__ = ["save_packed", "load_packed", "FORMAT_VERSION"]
 
 FORMAT_VERSION = 1
 _ARRAYS = ("ops", "segs", "pieces", "runs", "waits", "sigs", "fused_order", "kinds", "mr_segs", "mr_ranges", "mr_lds")
-_SCALARS = ("in_max", "xin_max", "out_max", "n_counters", "zero_output", "arena_elems", "stage_elems")
+_SCALARS = ("in_max", "xin_max", "out_max", "n_counters", "zero_output", "arena_elems", "stage_elems", "w_order")
 
 
 def _put(out, meta, name, prog: Program):
@@ -56,6 +56,7 @@ def _get(z, meta, name) -> Program:
         n_counters=sc["n_counters"],
         kinds=z[f"{name}_kinds"],
         zero_output=bool(sc["zero_output"]),
+        w_order=bool(sc.get("w_order", False)),
         arena_elems=sc["arena_elems"],
         stage_elems=sc["stage_elems"],
         mr_segs=z[f"{name}_mr_segs"],

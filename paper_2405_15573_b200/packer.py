@@ -140,6 +140,7 @@ class Program:
     peer: bool = False  # multi-GPU peer-exchange program: ONE launch per rank, y/u stored into
     #                     the peers' work buffers and counters signalled across ranks (RUN_PEER)
     host_io: bool = False  # host-I/O program (OP_XHOST / OP_XWAIT / OP_DRAIN ops)
+    w_order: bool = False  # ordered output: NEAR stores, FAR waits for the leaf's NEAR ops and adds (no memset of w)
     bulk_only: bool = False  # T-mode / alias pieces (packer_sym): only the bulk engine runs it
     xwin: bool = False  # windowed-input ops (packer_h FAR, OP_XWIN): the bulk engine's xwin kernel
 
@@ -219,6 +220,7 @@ class PackedOperator:
         kw = dict(self.build_kw)
         kw["rows_per_chunk"] = rows_per_chunk
         kw["split"] = dict(kw["split"], far_rows=far_rows)
+        kw["w_order"] = False  # the multi-RHS engine adds into a zeroed W
         fwd, work_f, _ = _build_program(self.geo, adjoint=False, **kw)
         adj, work_a, _ = _build_program(self.geo, adjoint=True, **kw)
         _assign_tmaps([fwd, adj])
@@ -502,8 +504,11 @@ def pack(
     if os.environ.get("UHMV_NEAR_INTERLEAVE_ADJ"):
         near_interleave_adj = tuple(float(v) for v in os.environ["UHMV_NEAR_INTERLEAVE_ADJ"].split(","))
     split["far_rows"] = int(os.environ.get("UHMV_FAR_ROWS", FAR_ROWS))
+    split["z_elems"] = int(os.environ.get("UHMV_Z_ELEMS", 1 << 60))
+    split["u_elems"] = int(os.environ.get("UHMV_U_ELEMS", 1 << 60))
     kw = dict(rows_per_chunk=rows_per_chunk, near_interleave=near_interleave, part=part, stage_elems=stage_elems,
-              split=split, peer=bool(peer and world > 1), near_interleave_adj=near_interleave_adj)
+              split=split, peer=bool(peer and world > 1), near_interleave_adj=near_interleave_adj,
+              w_order=world == 1 and os.environ.get("UHMV_W_ORDER", "0") != "0")
     fwd, work_f, ex_f = _build_program(geo, adjoint=False, **kw)
     adj, work_a, ex_a = _build_program(geo, adjoint=True, **kw)
     _assign_tmaps([fwd, adj] + [q.part_b for q in (fwd, adj) if q.part_b is not None])
@@ -622,7 +627,7 @@ def _seg(m_off, buf, rows, cols, ld, mode, in_off, out_off, x_off=-1):
 
 def _build_program(
     geo, *, adjoint: bool, rows_per_chunk: int, near_interleave, part=None, stage_elems=STAGE_ELEMS, split=None,
-    peer=False, host_io=False, near_interleave_adj=None,
+    peer=False, host_io=False, near_interleave_adj=None, w_order=False,
 ):
     """Returns (program, work length, exchange layout).  ``host_io``: the single-GPU variant
     whose P1 ops read x from the caller's pinned host buffer (and publish it to device x for
@@ -859,6 +864,14 @@ def _build_program(
             y_wait[t] = [(c_y[t], 1)]
     # U: staging vectors of the factorized blocks.  l_t = 0 gives exact zeros (reference:
     # (k x 0) @ (0,)), which the zero-initialised, never-written work region already holds.
+    def u_panel_step(lt, n):
+        """Columns per U op: split["u_cols"], or equal panels (multiples of 8) of at most
+        split["u_elems"] matrix elements -- long U ops delay every Z op behind them."""
+        step = split["u_cols"]
+        if lt * n > split.get("u_elems", 1 << 60):
+            step = min(step, (-(-n // -(-(lt * n) // split["u_elems"])) + 7) // 8 * 8)
+        return max(step, 8)
+
     u_wait = {}
     for t in in_map:
         n, lt = u_len[t], in_rank[t]
@@ -867,7 +880,8 @@ def _build_program(
             continue
         if owner_in(t) != rank:
             if peer:  # the owner's U panels of t, signalled across ranks
-                u_wait[t] = [(c_u[t], len(_chunks(0, geo["cwidth"][t] if adjoint else n, split["u_cols"])))]
+                n_u = geo["cwidth"][t] if adjoint else n
+                u_wait[t] = [(c_u[t], len(_chunks(0, n_u, u_panel_step(lt, n_u))))]
                 remote_ctr.add(c_u[t])
             continue
         u_wait[t] = [(c_u[t], 1)]
@@ -881,7 +895,7 @@ def _build_program(
                 if bid in zp_slot:
                     outs.append((BUF_WORK, zp_slot[bid], out_rank[r2], geo["spos"][bid], 0))
             n = ld
-        for c0, c1 in _chunks(0, n, split["u_cols"]):  # column panels: one op each
+        for c0, c1 in _chunks(0, n, u_panel_step(lt, n)):  # column panels: one op each
             segs = [_seg(base + c0, BUF_ARENA, lt, c1 - c0, ld, MODE_H, 0, 0)]
             ops[KIND_U].append(
                 (KIND_U, lt, c1 - c0, [(BUF_WORK, y_off[t], lt, 0, 0)], segs, _clip_runs(outs, c0, c1),
@@ -931,7 +945,10 @@ def _build_program(
                 if bids:
                     segs.append(_seg(zp_off[(s, q)], BUF_WORK, len(bids), ls, ls, MODE_S, 0, 0))
                     nbytes += len(bids) * ls
-        for o0, o1 in _chunks(0, ls, split["z_rows"]):  # output-row parts: one op each
+        z_step = split["z_rows"]
+        if nbytes > split.get("z_elems", 1 << 60):  # long ops bound the Z phase: equal row parts
+            z_step = min(z_step, -(-ls // -(-nbytes // split["z_elems"])))
+        for o0, o1 in _chunks(0, ls, z_step):  # output-row parts: one op each
             part = _restrict(segs, o0, o1)
             nb = sum(q[2] * q[3] for q in part)
             ops[KIND_Z].append(
@@ -943,11 +960,24 @@ def _build_program(
     # The output w is zeroed by the launcher and every entry receives at most one NEAR and one
     # FAR contribution through fp64 atomic adds: with two addends onto zero the sum is
     # order-independent (fl(a+b) = fl(b+a)), so NEAR and FAR need no ordering between them.
+    # Ordered output (``w_order``, single-GPU programs): the NEAR ops of a leaf STORE their rows
+    # and signal the leaf's counter, its FAR ops wait for them and add with a plain
+    # read-modify-write -- no zeroing pass over w, no atomics, a fixed order.  It needs every
+    # output leaf to have a NEAR or a FAR op (else the launcher's memset + red.add scheme stays).
+    if w_order and not host_io and world == 1:
+        for p, leaf in enumerate(out_leaves):
+            if not dense_by_outleaf.get(leaf, []) and not out_anc[p]:
+                w_order = False
+    else:
+        w_order = False
+    c_near = {}
     for p, leaf in enumerate(out_leaves):
         n = out_nodes[leaf]
         if not (out_lo <= n.lo and n.hi <= out_hi):
             continue  # another rank's output rows
         dlist = dense_by_outleaf.get(leaf, [])
+        if w_order and dlist:
+            c_near[p] = ctr()
         # forward: row chunks of the leaf; adjoint: the whole column leaf (H segments reduce
         # over the block rows, so the op owns all |c| output entries of the leaf)
         # (adjoint: column panels of the leaf, ADJ_NEAR_COLS wide -- the H segments reduce over
@@ -974,13 +1004,14 @@ def _build_program(
                     segs.append(_seg(offs[("D", bid)] + (a - n.lo), BUF_ARENA, r.size, rows, n.size, MODE_H, pos, 0, r.lo))
                     pos += r.size
                     nbytes += r.size * rows
-            kind, waits_n, outs_n = KIND_NEAR, [], [(BUF_W, a, rows, 0, RUN_ATOMIC)]
+            kind, waits_n, outs_n = KIND_NEAR, [], [(BUF_W, a, rows, 0, 0 if w_order else RUN_ATOMIC)]
             if host_io:
                 kind |= OP_XWAIT | OP_DRAIN
                 leaves_in = sorted({in_pos[bct.nodes[bid].col if not adjoint else bct.nodes[bid].row] for bid in dlist})
                 waits_n = [(c_x[q], 0) for q in leaves_in]
                 outs_n.append((BUF_HOSTW, n.lo, n.size, c_w[p], 0))
-            ops[KIND_NEAR].append((kind, pos, rows, in_runs, segs, outs_n, waits_n, [], nbytes))
+            ops[KIND_NEAR].append((kind, pos, rows, in_runs, segs, outs_n, waits_n,
+                                   [c_near[p]] if p in c_near else [], nbytes))
         anc = out_anc[p]
         if not anc:
             continue
@@ -995,6 +1026,10 @@ def _build_program(
                 pos += ls
             segs = stack_segs(out_stack_key, out_stacks, leaf, n.lo, a, b, anc, out_rank, MODE_N, -1)
             kind, outs_f = KIND_FAR, [(BUF_W, a, rows, 0, RUN_ATOMIC)]
+            if w_order:  # after the leaf's NEAR stores (or alone on the leaf: a store)
+                outs_f = [(BUF_W, a, rows, 0, RUN_ADD if p in c_near else 0)]
+                if p in c_near:
+                    waits.append((c_near[p], 1))
             if host_io:
                 kind |= OP_DRAIN
                 outs_f.append((BUF_HOSTW, n.lo, n.size, c_w[p], 0))
@@ -1040,6 +1075,8 @@ def _build_program(
     near_parts = [near[cut[i] : cut[i + 1]] for i in range(len(near_interleave))]
     while len(near_parts) < 4:
         near_parts.append([])
+    if w_order:  # FAR ops wait for the NEAR ops of their leaf: no nearfield share behind them
+        near_parts = near_parts[:3] + [[o for part in near_parts[3:] for o in part]]
     # phased launches (multi-launch mode): [P1 + NEAR] [RED] [U] [Z] [FAR]
     phased = [ops[KIND_P1] + near]
     phased += [ops[k] for k in (KIND_RED, KIND_U, KIND_Z, KIND_FAR)]
@@ -1049,9 +1086,11 @@ def _build_program(
         # (no dependencies) are spread between the dependent farfield phases to cover latency
         fused = (
             ops[KIND_P1] + near_parts[0] + ops[KIND_RED] + near_parts[1] + ops[KIND_U] + near_parts[2]
-            + ops[KIND_Z] + near_parts[3] + ops[KIND_FAR]
+            + ops[KIND_Z] + near_parts[3] + ops[KIND_FAR] + [o for part in near_parts[4:] for o in part]
         )
         prog = _finish(phased, fused, n_ctr, stage_elems=stage_elems, peer_limit=world * ex_len if peer else None)
+        prog.zero_output = not w_order
+        prog.w_order = bool(w_order)
         return prog, work, ex
     # multi-GPU: launch A produces this rank's y/u (+ nearfield), the exchange fills every
     # rank's y/u, launch B consumes them.  Waits on ops outside a launch are dropped: they are

@@ -25,7 +25,7 @@ def test_library_exports_all_header_symbols():
         assert hasattr(L, s), s
     from paper_2405_15573_b200 import _lib
 
-    assert L.uhmv_abi_version() == _lib.ABI_VERSION == 12
+    assert L.uhmv_abi_version() == _lib.ABI_VERSION == 13
     assert L.uhmv_last_error() == b""
 
 

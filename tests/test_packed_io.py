@@ -17,7 +17,7 @@ def _same_prog(a, b):
     for f in ("ops", "segs", "pieces", "runs", "waits", "sigs", "fused_order", "kinds", "mr_segs", "mr_ranges", "mr_lds"):
         assert np.array_equal(getattr(a, f), getattr(b, f)), f
     assert [tuple(x) for x in a.phases] == [tuple(x) for x in b.phases]
-    for f in ("in_max", "xin_max", "out_max", "n_counters", "zero_output", "arena_elems", "stage_elems"):
+    for f in ("in_max", "xin_max", "out_max", "n_counters", "zero_output", "arena_elems", "stage_elems", "w_order"):
         assert getattr(a, f) == getattr(b, f), f
     assert (a.part_b is None) == (b.part_b is None)
     if a.part_b is not None:

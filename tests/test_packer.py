@@ -95,14 +95,36 @@ def test_program_invariants(golden):
                 assert all(pos[q] < pos[i] for q in ps)
         # w is zeroed by the launcher; each entry gets at most one NEAR and one FAR atomic add
         # (two addends onto zero: order-independent), and nothing else writes w
+        # -- or, ordered output (prog.w_order, no memset): every entry is STORED once (by its NEAR
+        # op, or by its FAR op on a leaf without nearfield) and a FAR op that adds (plain
+        # read-modify-write) waits for every NEAR op storing its rows, all on earlier tickets
         per_kind = {KIND_NEAR: np.zeros(n_out, dtype=np.int64), KIND_FAR: np.zeros(n_out, dtype=np.int64)}
+        stores = np.zeros(n_out, dtype=np.int64)
+        storer = {}
+        assert prog.zero_output == (not prog.w_order)
         for i in range(prog.n_ops):
             ob, oe = prog.ops[i, 6], prog.ops[i, 7]
             for buf, off, ln, dst, flags in prog.runs[ob:oe]:
                 if buf == 3:
-                    assert flags == RUN_ATOMIC and prog.kinds[i] in per_kind
+                    assert prog.kinds[i] in per_kind
                     per_kind[int(prog.kinds[i])][off : off + ln] += 1
+                    if not prog.w_order:
+                        assert flags == RUN_ATOMIC
+                    elif flags == 0:
+                        stores[off : off + ln] += 1
+                        for r in range(off, off + ln):
+                            storer[r] = i
+                    else:
+                        assert flags == 1 and prog.kinds[i] == KIND_FAR
         assert (per_kind[KIND_NEAR] <= 1).all() and (per_kind[KIND_FAR] <= 1).all()
+        if prog.w_order:
+            assert (stores == 1).all()
+            for i in range(prog.n_ops):
+                ob, oe = prog.ops[i, 6], prog.ops[i, 7]
+                for buf, off, ln, dst, flags in prog.runs[ob:oe]:
+                    if buf == 3 and flags == 1:
+                        waited = {q for c, _ in prog.waits[prog.ops[i, 8]:prog.ops[i, 9]] for q in producers.get(int(c), [])}
+                        assert {storer[r] for r in range(off, off + ln)} <= waited
         # segment limits the kernel relies on
         segs = prog.segs
         hmask = segs[:, 5] != MODE_N
