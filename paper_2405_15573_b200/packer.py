@@ -102,7 +102,6 @@ ADJ_NEAR_COLS = int(os.environ.get("UHMV_ADJ_NEAR_COLS", 1 << 30))
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_NCOLS_MAX = int(os.environ.get("UHMV_NCOLS_MAX", 640))  # widest N piece row (two rows + x window still fit a stage)
 NW_COLS = int(os.environ.get("UHMV_NW_COLS", 640))  # widest panel of a warp-per-row op (sweeps: 352/176 slower)
-PANEL_ROWS = int(os.environ.get("UHMV_PANEL_ROWS", 0))  # N segments: column panels narrow enough for this many rows per stage (0: off)
 NOSPLIT = float(os.environ.get("UHMV_NOSPLIT", 0.3))  # see _pieces: largest stage fraction left empty instead of cutting an N segment
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 # work splitting of the farfield chain ops across CTAs (output entries per op)
@@ -1151,25 +1150,7 @@ def _order_segments(segs):
     return n + h
 
 
-def _ncols_panel(rows, cols, xs, stage_elems, ncols_max, panel_rows):
-    """Widest column panel of an N segment: ``ncols_max`` (and half a stage), or -- with
-    ``panel_rows`` -- narrow enough that a stage holds min(rows, panel_rows) rows, so every row
-    group of the consumers has a row in every piece (equal panels, multiples of 8 columns)."""
-    lim = min(ncols_max, stage_elems // 2)
-    if panel_rows > 0:
-        tgt = min(rows, panel_rows)
-        pw = stage_elems // (tgt + (1 if xs else 0))
-        if pw < cols:
-            n = -(-cols // max(32, pw))  # panels needed
-            pw = -(-cols // n)
-            pw = (pw + 7) // 8 * 8
-            while pw * tgt + (pw if xs else 0) > stage_elems and pw > 32:
-                pw -= 8
-        lim = min(lim, max(32, pw))
-    return lim
-
-
-def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_panel=BULK_HCOLS_MAX, panel_rows=0):
+def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_panel=BULK_HCOLS_MAX):
     """Cut an op's logical segments into row ranges packed into STAGE_ELEMS stages.
 
     Pieces whose input is a window of x (P1 and NEAR ops) carry that window inside the stage,
@@ -1194,9 +1175,8 @@ def _pieces(segs, has_x, stage_elems=STAGE_ELEMS, ncols_max=BULK_NCOLS_MAX, h_pa
         if mode != MODE_N and cols > min(h_panel, stage_elems // 2):
             for c0, c1 in _chunks(0, cols, min(h_panel, stage_elems // 2)):
                 split.append((m_off + c0, buf, rows, c1 - c0, ld, mode, in_off, out_off + c0, x_off, ()))
-        elif mode == MODE_N and cols > _ncols_panel(rows, cols, x_off >= 0 and has_x, stage_elems, ncols_max, panel_rows):
-            # rows wider than a stage (or than a stage of panel_rows rows) -> column panels
-            for c0, c1 in _chunks(0, cols, _ncols_panel(rows, cols, x_off >= 0 and has_x, stage_elems, ncols_max, panel_rows)):
+        elif mode == MODE_N and cols > min(ncols_max, stage_elems // 2):  # rows wider than a stage
+            for c0, c1 in _chunks(0, cols, min(ncols_max, stage_elems // 2)):  # -> column panels
                 sub = []  # the alias sub-blocks (column ranges) that fall into this panel
                 for a0, ac, amode, a_in, a_out in alias:
                     lo, hi = max(a0, c0), min(a0 + ac, c1)
@@ -1375,8 +1355,7 @@ def _finish(phased, fused, n_ctr, keep_waits_on=None, stage_elems=STAGE_ELEMS, p
         nsg = [q for q in ordered if q[5] == MODE_N]
         wide = bool(nsg) and all(q[3] >= WIDE_COLS for q in nsg)
         # warp-per-row ops: panels narrow enough that a stage holds a row for every warp
-        pcs = _pieces(ordered, has_x, stage_elems, NW_COLS if wide else BULK_NCOLS_MAX, h_panel,
-                      0 if wide else PANEL_ROWS)
+        pcs = _pieces(ordered, has_x, stage_elems, NW_COLS if wide else BULK_NCOLS_MAX, h_panel)
         if wide:  # long rows: few per piece
             for pc in pcs:
                 if pc[4] == MODE_N:
