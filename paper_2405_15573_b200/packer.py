@@ -102,6 +102,11 @@ ADJ_NEAR_COLS = int(os.environ.get("UHMV_ADJ_NEAR_COLS", 1 << 30))
 STAGE_ELEMS = 1408  # default complex128 per shared-memory stage (22 KiB: 16 x 80 dense + x window)
 BULK_NCOLS_MAX = int(os.environ.get("UHMV_NCOLS_MAX", 640))  # widest N piece row (two rows + x window still fit a stage)
 NW_COLS = int(os.environ.get("UHMV_NW_COLS", 640))  # widest panel of a warp-per-row op (sweeps: 352/176 slower)
+# Stored form of an admissible block: factorized (s_x, s_y: k_b (l_s + l_t) elements, one more
+# phase -- the U ops -- in the forward chain) iff k_b (l_s + l_t) < FACTOR_BIAS * l_s l_t, else
+# the product S_b = s_x s_y^H.  1.0 is the byte minimum.
+FACTOR_BIAS = 1.0
+FACTOR_BIAS_SMALL = 0.5  # operators under 1 GB (pack(): the forward chain loses its U phase for most blocks)
 NOSPLIT = float(os.environ.get("UHMV_NOSPLIT", 0.3))  # see _pieces: largest stage fraction left empty instead of cutting an N segment
 BULK_HCOLS_MAX = 512  # widest H/S piece of the bulk kernel (= csrc bulk::kSlots x 128 consumers)
 # work splitting of the farfield chain ops across CTAs (output entries per op)
@@ -321,6 +326,7 @@ def pack(
     world: int = 1,
     stage_elems: int | None = None,
     peer: bool = False,
+    factor_bias: float | None = None,
 ) -> PackedOperator:
     """Pack a UniformHMatrix (reference object or mirror) into arena + programs.
 
@@ -354,14 +360,23 @@ def pack(
             adm.append((bct.block_of[(s, t)], s, t))
     rank_r = {s: int(u.row_basis.matrices[s].shape[1]) for s in bct.row_map}
     rank_c = {t: int(u.col_basis.matrices[t].shape[1]) for t in bct.col_map}
+    if factor_bias is None:
+        # operators under ~1 GB are bound by the forward dependency chain: product
+        # form for every block whose factors are not at most half its size drops the U phase of
+        # most blocks for ~2 % more streamed bytes (config 2 forward 0.61 -> 0.645; its adjoint,
+        # which then sums more product-block partials, 0.56 -> 0.52)
+        approx = sum(min(int(u.coeffs[bid].s_x.shape[1]) * (rank_r[s] + rank_c[t]), rank_r[s] * rank_c[t]) for bid, s, t in adm)
+        approx += sum(int(np.prod(d.shape)) for d in u.dense.values())
+        approx += sum(cnodes[t].size * rank_c[t] for t in bct.col_map) + sum(rnodes[s].size * rank_r[s] for s in bct.row_map)
+        factor_bias = float(os.environ.get("UHMV_FACTOR_BIAS", FACTOR_BIAS_SMALL if 16 * approx < 1e9 else FACTOR_BIAS))
     kb, factorized = {}, {}
     bytes_coupling = 0
     for bid, s, t in adm:
         k = int(u.coeffs[bid].s_x.shape[1])
         kb[bid] = k
         ls, lt = rank_r[s], rank_c[t]
-        factorized[bid] = k * (ls + lt) < ls * lt
-        bytes_coupling += min(k * (ls + lt), ls * lt)
+        factorized[bid] = k * (ls + lt) < factor_bias * ls * lt
+        bytes_coupling += min(k * (ls + lt), ls * lt)  # the algorithmic bytes keep the min form
     dense_ids = list(u.dense.keys())
 
     # ---- arena layout ----
