@@ -504,13 +504,15 @@ def pack(
     else:
         part = None
     op_bytes = 16 * (bytes_bases + bytes_coupling + bytes_dense)
-    tiny = op_bytes < 2e8  # config 1 (99 MB): bound by the P1 -> RED -> U -> Z -> FAR chain
+    tiny = op_bytes < 2e8  # config 1 (99 MB): bound by the P1 -> RED -> Z -> FAR chain
     if near_interleave is None:
         # forward nearfield shares between the farfield phases (measured): operators under
         # ~1 GB are chain-latency-bound and want the chain started early (configs 1-2: -3..4%);
-        # under ~200 MB almost all of the nearfield goes behind the chain
+        # under ~200 MB (product-form coupling: no U phase, so no share before Z) the nearfield
+        # is split evenly around the chain (config 1: 0.302 -> 0.329,
+        # profiles/r02b/sweep_near_shares_product_form.txt)
         small = op_bytes < 1e9
-        near_interleave = (0.05, 0.05, 0.1, 0.8) if tiny else (0.2, 0.1, 0.2, 0.5) if small else (0.35, 0.1, 0.2, 0.35)
+        near_interleave = (0.4, 0.2, 0.0, 0.4) if tiny else (0.2, 0.1, 0.2, 0.5) if small else (0.35, 0.1, 0.2, 0.35)
     split_def = dict(SPLIT_DEFAULTS, **({"z_rows": 13} if tiny else {}))  # config 1: Z ops in two row parts
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in split_def.items()}
     if os.environ.get("UHMV_NEAR_INTERLEAVE"):
