@@ -369,6 +369,7 @@ def pack(
         approx += sum(int(np.prod(d.shape)) for d in u.dense.values())
         approx += sum(cnodes[t].size * rank_c[t] for t in bct.col_map) + sum(rnodes[s].size * rank_r[s] for s in bct.row_map)
         factor_bias = float(os.environ.get("UHMV_FACTOR_BIAS", FACTOR_BIAS_SMALL if 16 * approx < 1e9 else FACTOR_BIAS))
+    adj_copy = world == 1 and os.environ.get("UHMV_ADJ_COPY", "1" if factor_bias < 1.0 else "0") != "0"
     kb, factorized = {}, {}
     bytes_coupling = 0
     for bid, s, t in adm:
@@ -438,6 +439,23 @@ def pack(
                 pos += kb[bid]
         ycols[t] = (cols, pos)
         alloc(("Y", t), rank_c[t] * pos, pos)
+    # Adjoint copy (operators stored product-biased, i.e. under 1 GB): CT_t = [S_b^H ...] over the
+    # product blocks of column cluster t, l_t rows, so the adjoint Z op of t is ONE long-row GEMV
+    # over [y'_s ...] like the forward one over C_s -- no adjoint U ops and partial sums for
+    # those blocks (a four-phase adjoint chain too).  Each direction streams its own copy: the
+    # bytes per matvec do not change, the arena grows by the product-form coupling.
+    ctpos, ctwidth = {}, {}
+    if adj_copy:
+        for t in sorted(bct.col_map):
+            w = 0
+            for s in bct.col_map[t]:
+                bid = bct.block_of[(s, t)]
+                if not factorized[bid] and rank_r[s] > 0 and rank_c[t] > 0:
+                    ctpos[bid] = w
+                    w += rank_r[s]
+            if w:
+                ctwidth[t] = w
+                alloc(("CT", t), rank_c[t] * w, w)
     dense_by_rleaf, dense_by_cleaf = {}, {}
     for bid in dense_ids:
         b = bct.nodes[bid]
@@ -478,6 +496,14 @@ def pack(
                     pair = u.coeffs[bid]
                     cs[:, spos[bid] : spos[bid] + rank_c[t]] = pair.s_x @ np.conj(pair.s_y).T
             put(("C", s), cs)
+    for t, w in ctwidth.items():
+        ct = np.empty((rank_c[t], w), dtype=np.complex128)
+        for s in bct.col_map[t]:
+            bid = bct.block_of[(s, t)]
+            if bid in ctpos:
+                pair = u.coeffs[bid]
+                ct[:, ctpos[bid] : ctpos[bid] + rank_r[s]] = np.conj(pair.s_x @ np.conj(pair.s_y).T).T
+        put(("CT", t), ct)
     for t, (cols, ktot) in ycols.items():
         lt = rank_c[t]
         if lt and ktot:
@@ -497,7 +523,7 @@ def pack(
     geo = dict(
         bct=bct, rank_r=rank_r, rank_c=rank_c, kb=kb, factorized=factorized,
         fcols=fcols, ycols=ycols, offs=offs, dense_by_rleaf=dense_by_rleaf, dense_by_cleaf=dense_by_cleaf,
-        vstack=vstack, ustack=ustack, cwidth=cwidth, spos=spos,
+        vstack=vstack, ustack=ustack, cwidth=cwidth, spos=spos, ctpos=ctpos, ctwidth=ctwidth,
     )
     if world > 1:
         part = _partition(geo, world, rank)
@@ -513,6 +539,10 @@ def pack(
         # profiles/r02b/sweep_near_shares_product_form.txt)
         small = op_bytes < 1e9
         near_interleave = (0.4, 0.2, 0.0, 0.4) if tiny else (0.2, 0.1, 0.2, 0.5) if small else (0.35, 0.1, 0.2, 0.35)
+    if adj_copy and near_interleave_adj == (0.4, 0.15, 0.3, 0.15):
+        # with the adjoint copy the adjoint chain mirrors the forward one (no U phase for the
+        # product blocks): config 2 adjoint 0.600 -> 0.627 with the forward shares of small operators
+        near_interleave_adj = (0.2, 0.1, 0.2, 0.5)
     split_def = dict(SPLIT_DEFAULTS, **({"z_rows": 13} if tiny else {}))  # config 1: Z ops in two row parts
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in split_def.items()}
     if os.environ.get("UHMV_NEAR_INTERLEAVE"):
@@ -551,6 +581,10 @@ def pack(
             bases=16 * bytes_bases,
             coupling=16 * bytes_coupling,
             dense=16 * bytes_dense,
+            # stored beyond §8d's minimum: the product-biased forms and the adjoint copy CT_t
+            form_extra=16 * int(sum((kb[bid] * (rank_r[s] + rank_c[t]) if factorized[bid] else rank_r[s] * rank_c[t])
+                                    for bid, s, t in adm) - bytes_coupling),
+            adjoint_copy=16 * int(sum(rank_c[t] * w for t, w in ctwidth.items())),
             n_factorized=int(sum(factorized.values())),
             n_product=int(len(adm) - sum(factorized.values())),
         ),
@@ -757,7 +791,8 @@ def _build_program(
     # stored per output cluster t and producing rank, contiguous, summed by t's Z op.
     u_len = {t: (ycols[t][1] if not adjoint else fcols[t][1]) for t in in_map}
     zparts = {}  # adjoint: (t, rank q) -> [product blocks (r, t) with owner_in(r) == q]
-    if adjoint:
+    use_ct = adjoint and world == 1 and bool(geo.get("ctwidth"))  # adjoint copy CT_t: no partials
+    if adjoint and not use_ct:
         for t in sorted(out_map, key=lambda t: out_nodes[t].lo):
             if out_rank[t] == 0:
                 continue
@@ -892,7 +927,7 @@ def _build_program(
     for t in in_map:
         n, lt = u_len[t], in_rank[t]
         u_wait[t] = []
-        if (n == 0 and not (adjoint and geo["cwidth"][t])) or lt == 0:
+        if (n == 0 and not (adjoint and not use_ct and geo["cwidth"][t])) or lt == 0:
             continue
         if owner_in(t) != rank:
             if peer:  # the owner's U panels of t, signalled across ranks
@@ -903,6 +938,8 @@ def _build_program(
         u_wait[t] = [(c_u[t], 1)]
         if not adjoint:
             base, ld, outs = offs[("Y", t)], n, [(BUF_WORK, u_off[t], n, 0, 0)]
+        elif use_ct:  # adjoint copy: only F_s -> [u'_b ...]; the product blocks go through CT_t in the Z ops
+            base, ld, outs = offs[("C", t)], geo["cwidth"][t], [(BUF_WORK, u_off[t], n, 0, 0)]
         else:  # the whole C_s: [F_s | S_b ...] -> [u'_b ... | partial slots of the product blocks]
             base, ld = offs[("C", t)], geo["cwidth"][t]
             outs = [(BUF_WORK, u_off[t], n, 0, 0)] if n else []
@@ -952,6 +989,16 @@ def _build_program(
                 segs.append(_seg(offs[("Y", s)], BUF_ARENA, ls, ktot, ktot, MODE_N, 0, 0))
             n_in = ktot
             nbytes = ls * ktot
+            ctw = geo["ctwidth"].get(s, 0) if use_ct else 0
+            if ctw:  # + CT_s [y'_r ...]: the product blocks of column cluster s in one long-row GEMV
+                for r in bct.col_map[s]:
+                    bid = bct.block_of[(r, s)]
+                    if bid in geo["ctpos"]:
+                        in_runs.append((BUF_WORK, y_off[r], in_rank[r], ktot + geo["ctpos"][bid], 0))
+                        waits.extend(y_wait[r])
+                segs.append(_seg(offs[("CT", s)], BUF_ARENA, ls, ctw, ctw, MODE_N, ktot, 0))
+                n_in = ktot + ctw
+                nbytes += ls * ctw
             for r in out_map[s]:  # + S_b^H y'_r of product blocks: computed by U_r ...
                 bid = bct.block_of[(r, s)]
                 if bid in zp_slot:
