@@ -369,7 +369,7 @@ def pack(
         approx += sum(int(np.prod(d.shape)) for d in u.dense.values())
         approx += sum(cnodes[t].size * rank_c[t] for t in bct.col_map) + sum(rnodes[s].size * rank_r[s] for s in bct.row_map)
         factor_bias = float(os.environ.get("UHMV_FACTOR_BIAS", FACTOR_BIAS_SMALL if 16 * approx < 1e9 else FACTOR_BIAS))
-    adj_copy = world == 1 and os.environ.get("UHMV_ADJ_COPY", "1" if factor_bias < 1.0 else "0") != "0"
+    adj_copy = world == 1 and os.environ.get("UHMV_ADJ_COPY", "1") != "0"
     kb, factorized = {}, {}
     bytes_coupling = 0
     for bid, s, t in adm:
@@ -439,7 +439,7 @@ def pack(
                 pos += kb[bid]
         ycols[t] = (cols, pos)
         alloc(("Y", t), rank_c[t] * pos, pos)
-    # Adjoint copy (operators stored product-biased, i.e. under 1 GB): CT_t = [S_b^H ...] over the
+    # Adjoint copy (single-GPU packs; UHMV_ADJ_COPY=0 turns it off): CT_t = [S_b^H ...] over the
     # product blocks of column cluster t, l_t rows, so the adjoint Z op of t is ONE long-row GEMV
     # over [y'_s ...] like the forward one over C_s -- no adjoint U ops and partial sums for
     # those blocks (a four-phase adjoint chain too).  Each direction streams its own copy: the
@@ -540,9 +540,10 @@ def pack(
         small = op_bytes < 1e9
         near_interleave = (0.4, 0.2, 0.0, 0.4) if tiny else (0.2, 0.1, 0.2, 0.5) if small else (0.35, 0.1, 0.2, 0.35)
     if adj_copy and near_interleave_adj == (0.4, 0.15, 0.3, 0.15):
-        # with the adjoint copy the adjoint chain mirrors the forward one (no U phase for the
-        # product blocks): config 2 adjoint 0.600 -> 0.627 with the forward shares of small operators
-        near_interleave_adj = (0.2, 0.1, 0.2, 0.5)
+        # with the adjoint copy the adjoint chain mirrors the forward one (no U op or partial for
+        # the product blocks) and wants the forward shares: config 2 adjoint 0.600 -> 0.627,
+        # config 3 adjoint 0.913 -> 0.948 (profiles/r02b/ab_adjoint_copy{,_large}.txt)
+        near_interleave_adj = (0.2, 0.1, 0.2, 0.5) if op_bytes < 1e9 else (0.35, 0.1, 0.2, 0.35)
     split_def = dict(SPLIT_DEFAULTS, **({"z_rows": 13} if tiny else {}))  # config 1: Z ops in two row parts
     split = {k: int(os.environ.get(f"UHMV_SPLIT_{k.upper()}", v)) for k, v in split_def.items()}
     if os.environ.get("UHMV_NEAR_INTERLEAVE"):

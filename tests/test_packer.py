@@ -204,8 +204,13 @@ def test_bytes_accounting(golden):
     extra = p.storage["form_extra"] + p.storage["adjoint_copy"]
     assert p.bytes_arena >= p.bytes_alg + extra
     assert p.bytes_arena - p.bytes_alg - extra <= 128 * (len(u.coeffs) + len(u.dense) + 5 * len(u.bct.nodes) + 8)
-    q = pack(u, factor_bias=1.0)  # the byte minimum (default from 1 GB on): nothing extra
+    os.environ["UHMV_ADJ_COPY"] = "0"
+    try:
+        q = pack(u, factor_bias=1.0)  # the byte minimum: nothing extra
+    finally:
+        del os.environ["UHMV_ADJ_COPY"]
     assert q.storage["form_extra"] == 0 and q.storage["adjoint_copy"] == 0
+    assert pack(u, factor_bias=1.0).storage["form_extra"] == 0  # (default from 1 GB on: the copy only)
     assert q.bytes_arena - q.bytes_alg <= 128 * (len(u.coeffs) + len(u.dense) + 4 * len(u.bct.nodes) + 8)
 
 

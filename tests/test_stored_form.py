@@ -16,9 +16,18 @@ BIASES = [0.0, 0.5, 1.0, 1e9]  # all product ... all factorized
 
 
 def _pack(u, bias):
+    """bias 1.0 also runs WITHOUT the adjoint copy (partials per product block: the multi-GPU scheme)."""
+    import os
+
     from paper_2405_15573_b200.packer import pack
 
-    return pack(u, factor_bias=bias)
+    if bias != 1.0:
+        return pack(u, factor_bias=bias)
+    os.environ["UHMV_ADJ_COPY"] = "0"
+    try:
+        return pack(u, factor_bias=bias)
+    finally:
+        del os.environ["UHMV_ADJ_COPY"]
 
 
 @pytest.mark.parametrize("name", NAMES)
